@@ -1,0 +1,767 @@
+// Device side of the B200 KADABRA hot path: graph upload, slot allocation,
+// kernel launches (sampling, frame fold + stopping check, BFS) and the small
+// amount of host bookkeeping around them.  sm_100a only; no CPU fallback.
+#include "cuda_sampler.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "sampler_kernels.cuh"
+
+namespace ebc {
+
+namespace {
+
+void cuda_check(cudaError_t e, const char *what, const char *file, int line) {
+    if (e != cudaSuccess) {
+        char buf[512];
+        std::snprintf(buf, sizeof(buf), "CUDA failure: %s: %s (%s:%d)", what, cudaGetErrorString(e), file, line);
+        throw CudaError(buf);
+    }
+}
+#define EBC_CUDA(expr) cuda_check((expr), #expr, __FILE__, __LINE__)
+
+template <typename T> T *dev_alloc(std::uint64_t count) {
+    void *p = nullptr;
+    EBC_CUDA(cudaMalloc(&p, std::max<std::uint64_t>(count, 1) * sizeof(T)));
+    return static_cast<T *>(p);
+}
+
+// ------------------------------------------------------------------------------------
+// Frame fold + stopping check.
+//   fold:   S[i] += frame[i]; frame[i] = 0 for i in 1..n        (StateFrame::add,
+//           state_frame.hpp:29-33; collect_epoch's sum-then-zero, epoch.cpp:66-81)
+//   check:  any vertex whose f or g width >= eps clears the "all below" flag
+//           (check_stop, stopping.cpp:125-142; bound_width, stopping.cpp:96-111)
+// tau (word 0) is read by every thread before anyone writes it: word 0 is folded
+// by finish_fold_kernel afterwards.  FP64 uses explicit round-to-nearest
+// intrinsics in the reference's operation order so no FMA contraction can
+// change a comparison.
+struct StopParams {
+    double eps;
+    u64 omega;
+    const double *log_lower; // ln(1/delta_L) or ln(2/delta_L)
+    const double *log_upper;
+    int bound; // 0 Hoeffding, 1 empirical Bernstein
+    int have;
+};
+
+__device__ __forceinline__ double bound_width_dev(double b, double logterm, double t, int bound) {
+    if (bound == 0) // sqrt(log(1/delta_v) / (2 t))
+        return __dsqrt_rn(__ddiv_rn(logterm, __dmul_rn(2.0, t)));
+    // sqrt(2 var l / t) + 7 l / (3 (t - 1))
+    const double var = __dmul_rn(b, __dsub_rn(1.0, b));
+    const double first = __dsqrt_rn(__ddiv_rn(__dmul_rn(__dmul_rn(2.0, var), logterm), t));
+    const double second = __ddiv_rn(__dmul_rn(7.0, logterm), __dmul_rn(3.0, __dsub_rn(t, 1.0)));
+    return __dadd_rn(first, second);
+}
+
+__global__ void __launch_bounds__(256) fold_check_kernel(u32 *frame, u64 *S, u64 n, StopParams sp, u32 *fail_flag) {
+    const u64 tau = S[0] + frame[0];
+    const bool evaluate = sp.have && tau < sp.omega && tau >= 2;
+    const double t = static_cast<double>(tau);
+    bool fail = false;
+    for (u64 i = 1 + blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i <= n;
+         i += static_cast<u64>(gridDim.x) * blockDim.x) {
+        const u32 f = frame[i];
+        u64 c = S[i];
+        if (f != 0) {
+            c += f;
+            S[i] = c;
+            frame[i] = 0;
+        }
+        if (evaluate) {
+            const double b = __ddiv_rn(static_cast<double>(c), t);
+            if (bound_width_dev(b, sp.log_lower[i - 1], t, sp.bound) >= sp.eps)
+                fail = true;
+            if (bound_width_dev(b, sp.log_upper[i - 1], t, sp.bound) >= sp.eps)
+                fail = true;
+        }
+    }
+    if (__syncthreads_or(fail ? 1 : 0) && threadIdx.x == 0)
+        atomicOr(fail_flag, 1u);
+}
+
+// Folds word 0 (tau) and publishes the stop decision: result[0] = stop (0|1), result[1] = tau.
+__global__ void finish_fold_kernel(u32 *frame, u64 *S, StopParams sp, u32 *fail_flag, volatile u64 *result) {
+    const u64 tau = S[0] + frame[0];
+    S[0] = tau;
+    frame[0] = 0;
+    u64 stop;
+    if (!sp.have)
+        stop = 0;
+    else if (tau >= sp.omega)
+        stop = 1; // stopping.cpp:127
+    else if (tau < 2)
+        stop = 0; // stopping.cpp:129
+    else
+        stop = *fail_flag ? 0 : 1;
+    *fail_flag = 0;
+    result[1] = tau;
+    __threadfence_system();
+    result[0] = stop;
+}
+
+__global__ void widen_kernel(const u32 *in, u64 *out, u64 words) {
+    for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < words;
+         i += static_cast<u64>(gridDim.x) * blockDim.x)
+        out[i] = in[i];
+}
+
+// ------------------------------------------------------------------------------------
+// Level-synchronous BFS for the diameter phase (bfs.cpp:9-34).  One warp per
+// frontier vertex, lanes stride the row; the level loop runs on the device
+// stream without host round trips (each launch reads the queue size written by
+// the previous one and exits when it is empty).
+struct BfsState {
+    u32 queue_size[2];
+    u32 depth;
+    u32 done;
+    u64 reached;
+};
+
+__global__ void __launch_bounds__(256) bfs_level_kernel(const u64 *offsets, const u32 *targets, u32 *dist,
+                                                        u32 *queue0, u32 *queue1, BfsState *st, u32 level) {
+    if (st->done)
+        return;
+    const u32 *in = (level & 1) ? queue1 : queue0;
+    u32 *out = (level & 1) ? queue0 : queue1;
+    const u32 count = st->queue_size[level & 1];
+    const u32 warps = (gridDim.x * blockDim.x) >> 5;
+    const u32 warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const u32 lane = threadIdx.x & 31;
+    for (u32 i = warp; i < count; i += warps) {
+        const u32 u = in[i];
+        const u64 beg = offsets[u], end = offsets[u + 1];
+        for (u64 k = beg + lane; k < end; k += 32) {
+            const u32 v = targets[k];
+            if (dist[v] == 0xffffffffu && atomicCAS(dist + v, 0xffffffffu, level + 1) == 0xffffffffu) {
+                const u32 pos = atomicAdd(&st->queue_size[(level + 1) & 1], 1u);
+                out[pos] = v;
+            }
+        }
+    }
+}
+
+// Runs as one thread between levels: closes level `level`, opens level + 1.
+__global__ void bfs_advance_kernel(BfsState *st, u32 level) {
+    if (st->done)
+        return;
+    const u32 next = st->queue_size[(level + 1) & 1];
+    st->queue_size[level & 1] = 0;
+    if (next == 0) {
+        st->done = 1;
+        st->depth = level;
+    } else {
+        st->reached += next;
+    }
+}
+
+// farthest = max distance, lowest id on ties (bfs.cpp:21-24): key = dist << 32 | ~v.
+__global__ void __launch_bounds__(256) bfs_farthest_kernel(const u32 *dist, u64 n, unsigned long long *best) {
+    unsigned long long local = 0;
+    for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v < n;
+         v += static_cast<u64>(gridDim.x) * blockDim.x) {
+        const u32 d = dist[v];
+        if (d != 0xffffffffu) {
+            const unsigned long long key = (static_cast<unsigned long long>(d) << 32) | (0xffffffffu - static_cast<u32>(v));
+            local = key > local ? key : local;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long other = __shfl_xor_sync(0xffffffffu, local, o);
+        local = other > local ? other : local;
+    }
+    if ((threadIdx.x & 31) == 0)
+        atomicMax(best, local);
+}
+
+__global__ void flush_kernel(u32 *buf, u64 count, u32 salt) {
+    for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < count;
+         i += static_cast<u64>(gridDim.x) * blockDim.x)
+        buf[i] = static_cast<u32>(i) ^ salt;
+}
+
+template <int BLOCK> void launch_sample(const SamplerParams &p, u32 grid, cudaStream_t stream) {
+    sample_kernel<BLOCK><<<grid, BLOCK, 0, stream>>>(p);
+}
+
+void launch_sample_dispatch(u32 block, const SamplerParams &p, u32 grid, cudaStream_t stream) {
+    switch (block) {
+    case 32: launch_sample<32>(p, grid, stream); break;
+    case 64: launch_sample<64>(p, grid, stream); break;
+    case 128: launch_sample<128>(p, grid, stream); break;
+    case 256: launch_sample<256>(p, grid, stream); break;
+    case 512: launch_sample<512>(p, grid, stream); break;
+    default: throw ConfigError("block_threads must be one of 32, 64, 128, 256, 512");
+    }
+    EBC_CUDA(cudaGetLastError());
+}
+
+int occupancy_for(u32 block) {
+    int per_sm = 0;
+    switch (block) {
+    case 32: EBC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sample_kernel<32>, 32, 0)); break;
+    case 64: EBC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sample_kernel<64>, 64, 0)); break;
+    case 128: EBC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sample_kernel<128>, 128, 0)); break;
+    case 256: EBC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sample_kernel<256>, 256, 0)); break;
+    case 512: EBC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sample_kernel<512>, 512, 0)); break;
+    default: throw ConfigError("block_threads must be one of 32, 64, 128, 256, 512");
+    }
+    return per_sm;
+}
+
+struct SlotArrays {
+    u32 *lab = nullptr, *list = nullptr, *lvl = nullptr, *contact = nullptr, *hdr = nullptr;
+    u64 *sig = nullptr;
+    u64 slots = 0, cap = 0;
+    u64 bytes = 0;
+
+    void allocate(u64 slots_, u64 cap_, u64 n, cudaStream_t stream) {
+        slots = slots_;
+        cap = cap_;
+        lab = dev_alloc<u32>(slots * 2 * n);
+        list = dev_alloc<u32>(slots * 2 * cap);
+        sig = dev_alloc<u64>(slots * 2 * cap);
+        lvl = dev_alloc<u32>(slots * 2 * (cap + 2));
+        contact = dev_alloc<u32>(slots * 2 * cap);
+        hdr = dev_alloc<u32>(slots * kHdrWords);
+        bytes = slots * (2 * n * 4 + 2 * cap * (4 + 8 + 4) + 2 * (cap + 2) * 4 + kHdrWords * 4);
+        EBC_CUDA(cudaMemsetAsync(lab, 0, slots * 2 * n * 4, stream));
+        std::vector<u32> h(slots * kHdrWords, 0);
+        for (u64 s = 0; s < slots; ++s)
+            h[s * kHdrWords + kHdrBase0] = h[s * kHdrWords + kHdrBase1] = 1; // label 0 == never visited
+        EBC_CUDA(cudaMemcpyAsync(hdr, h.data(), h.size() * 4, cudaMemcpyHostToDevice, stream));
+        EBC_CUDA(cudaStreamSynchronize(stream));
+    }
+    void release() {
+        cudaFree(lab);
+        cudaFree(list);
+        cudaFree(sig);
+        cudaFree(lvl);
+        cudaFree(contact);
+        cudaFree(hdr);
+    }
+    static u64 bytes_per_slot(u64 n, u64 cap) { return 2 * n * 4 + 2 * cap * 16 + 2 * (cap + 2) * 4 + kHdrWords * 4; }
+};
+
+constexpr u32 kOverflowCap = 1u << 20; // also the largest number of samples per launch
+constexpr int kEvents = 8;
+
+} // namespace
+
+struct CudaSampler::Impl {
+    int device = 0;
+    int sm_count = 0;
+    u64 n = 0, arcs = 0;
+    u64 *d_offsets = nullptr;
+    u32 *d_targets = nullptr;
+    u32 block = 128;
+    SlotArrays small, big;
+    u32 *d_frame[2] = {nullptr, nullptr};
+    u64 *d_S = nullptr;
+    u64 *d_wide = nullptr; // scratch for read_frame
+    unsigned long long *d_ticket = nullptr; // [2]: main pass, re-run pass
+    unsigned long long *d_work = nullptr;
+    u32 *d_overflow_list = nullptr, *d_overflow_count = nullptr; // count[0] main, count[1] re-run
+    u32 *d_fail = nullptr;
+    double *d_log_lower = nullptr, *d_log_upper = nullptr;
+    StopParams stop{};
+    u64 *h_result[2] = {nullptr, nullptr}; // pinned, mapped: {stop, tau} per frame
+    unsigned long long *d_ovf_total = nullptr; // [2]: abandoned samples in the main / re-run pass
+    cudaStream_t s_sample = nullptr, s_agg = nullptr;
+    cudaEvent_t ev_sampled[2]{}, ev_folded[2]{}, ev_user[kEvents]{};
+    bool folded_pending[2] = {false, false};
+    u64 overflow_seen = 0;
+    u64 launches = 0;
+    // bfs
+    u32 *d_dist = nullptr, *d_queue[2] = {nullptr, nullptr};
+    BfsState *d_bfs = nullptr;
+    unsigned long long *d_best = nullptr;
+    // flush
+    u32 *d_flush = nullptr;
+    u64 flush_words = 0;
+    u64 graph_bytes = 0;
+
+    SamplerParams base_params(const SlotArrays &a) const {
+        SamplerParams p{};
+        p.n = n;
+        p.offsets = d_offsets;
+        p.targets = d_targets;
+        p.lab = a.lab;
+        p.list = a.list;
+        p.sig = a.sig;
+        p.lvl = a.lvl;
+        p.contact = a.contact;
+        p.hdr = a.hdr;
+        p.cap = a.cap;
+        p.work = d_work;
+        p.overflow_list = d_overflow_list;
+        p.overflow_cap = kOverflowCap;
+        return p;
+    }
+
+    // Launches the main pass and the re-run pass for [first, first+count), count <= kOverflowCap.
+    void launch(u64 seed, u32 tag, u64 first, u64 count, int frame, const u32 *d_pairs,
+                SampleRecordDev *d_records, u32 *d_paths, u64 path_stride) {
+        EBC_CUDA(cudaMemsetAsync(d_ticket, 0, 2 * sizeof(unsigned long long), s_sample));
+        EBC_CUDA(cudaMemsetAsync(d_overflow_count, 0, 2 * sizeof(u32), s_sample));
+        SamplerParams p = base_params(small);
+        p.seed = seed;
+        p.tag = tag;
+        p.first = first;
+        p.count = count;
+        p.ticket = d_ticket;
+        p.frame = d_frame[frame];
+        p.pairs = d_pairs;
+        p.records = d_records;
+        p.paths = d_paths;
+        p.path_stride = path_stride;
+        p.overflow_count = d_overflow_count;
+        p.overflow_total = d_ovf_total;
+        const u32 grid = static_cast<u32>(std::min<u64>(small.slots, count));
+        launch_sample_dispatch(block, p, grid, s_sample);
+        ++launches;
+        if (small.cap < n) { // capacity overflow is impossible when cap == n
+            SamplerParams q = base_params(big);
+            q.seed = seed;
+            q.tag = tag;
+            q.first = first;
+            q.count = count;
+            q.ticket = d_ticket + 1;
+            q.frame = d_frame[frame];
+            q.pairs = d_pairs;
+            q.records = d_records;
+            q.paths = d_paths;
+            q.path_stride = path_stride;
+            q.overflow_count = d_overflow_count + 1;
+            q.overflow_total = d_ovf_total + 1;
+            q.relist = d_overflow_list;
+            q.count_ptr = d_overflow_count;
+            launch_sample_dispatch(block, q, static_cast<u32>(big.slots), s_sample);
+            ++launches;
+        }
+    }
+
+    // Synchronises the sampling stream and returns {abandoned in small slots, abandoned in large slots}.
+    void read_overflow(unsigned long long out[2]) {
+        EBC_CUDA(cudaStreamSynchronize(s_sample));
+        EBC_CUDA(cudaMemcpy(out, d_ovf_total, 16, cudaMemcpyDeviceToHost));
+        if (out[1] != 0)
+            throw CudaError("internal: capacity overflow in a full-capacity slot");
+    }
+};
+
+CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(new Impl) {
+    Impl &m = *impl_;
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+        throw CudaError(std::string("no CUDA device available (this library has no CPU fallback): ") +
+                        (e == cudaSuccess ? "device count is 0" : cudaGetErrorString(e)));
+    if (opt.device >= 0) {
+        if (opt.device >= count)
+            throw ConfigError("device ordinal out of range");
+        EBC_CUDA(cudaSetDevice(opt.device));
+    }
+    EBC_CUDA(cudaGetDevice(&m.device));
+    cudaDeviceProp prop{};
+    EBC_CUDA(cudaGetDeviceProperties(&prop, m.device));
+    if (prop.major < 10)
+        throw CudaError("this build targets sm_100a (B200); found compute capability " +
+                        std::to_string(prop.major) + "." + std::to_string(prop.minor));
+    m.sm_count = prop.multiProcessorCount;
+    require(g.n >= 2, "sampler: need at least two vertices");
+    m.n = g.n;
+    m.arcs = g.targets.size();
+
+    EBC_CUDA(cudaStreamCreateWithFlags(&m.s_sample, cudaStreamNonBlocking));
+    EBC_CUDA(cudaStreamCreateWithFlags(&m.s_agg, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+        EBC_CUDA(cudaEventCreateWithFlags(&m.ev_sampled[i], cudaEventDisableTiming));
+        EBC_CUDA(cudaEventCreateWithFlags(&m.ev_folded[i], cudaEventDisableTiming));
+    }
+    for (int i = 0; i < kEvents; ++i)
+        EBC_CUDA(cudaEventCreate(&m.ev_user[i]));
+
+    // ---- graph: replicated CSR, u64 offsets + u32 targets ----
+    m.d_offsets = dev_alloc<u64>(g.n + 1);
+    m.d_targets = dev_alloc<u32>(m.arcs);
+    EBC_CUDA(cudaMemcpyAsync(m.d_offsets, g.offsets.data(), (g.n + 1) * 8, cudaMemcpyHostToDevice, m.s_sample));
+    if (m.arcs)
+        EBC_CUDA(cudaMemcpyAsync(m.d_targets, g.targets.data(), m.arcs * 4, cudaMemcpyHostToDevice, m.s_sample));
+    m.graph_bytes = (g.n + 1) * 8 + m.arcs * 4;
+
+    // ---- launch shape ----
+    m.block = opt.block_threads ? opt.block_threads : 128;
+    const int per_sm = occupancy_for(m.block);
+    if (per_sm < 1)
+        throw CudaError("sampling kernel does not fit on an SM");
+    u64 cap = opt.slot_capacity ? std::min<u64>(opt.slot_capacity, g.n)
+                                : std::min<u64>(g.n, std::max<u64>(u64{1} << 17, g.n / 4));
+    cap = std::max<u64>(cap, 2);
+    u64 slots = opt.slots ? opt.slots : static_cast<u64>(per_sm) * m.sm_count;
+    size_t free_b = 0, total_b = 0;
+    EBC_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const u64 fixed = (g.n + 1) * (4 * 2 + 8 + 8 + 16 + 12) + (u64{256} << 20) + kOverflowCap * 4 +
+                      (cap < g.n ? 2 * SlotArrays::bytes_per_slot(g.n, g.n) : 0);
+    const u64 budget = static_cast<u64>(free_b) > fixed ? (static_cast<u64>(free_b) - fixed) / 10 * 8 : 0;
+    const u64 per_slot = SlotArrays::bytes_per_slot(g.n, cap);
+    if (!opt.slots && slots * per_slot > budget)
+        slots = budget / per_slot;
+    if (slots < 1)
+        throw CudaError("not enough device memory for a single sampling slot");
+    m.small.allocate(slots, cap, g.n, m.s_sample);
+    if (cap < g.n)
+        m.big.allocate(2, g.n, g.n, m.s_sample);
+
+    // ---- frames, state, bookkeeping ----
+    for (int i = 0; i < 2; ++i) {
+        m.d_frame[i] = dev_alloc<u32>(g.n + 1);
+        EBC_CUDA(cudaMemsetAsync(m.d_frame[i], 0, (g.n + 1) * 4, m.s_sample));
+        EBC_CUDA(cudaHostAlloc(reinterpret_cast<void **>(&m.h_result[i]), 2 * sizeof(u64), cudaHostAllocMapped));
+        m.h_result[i][0] = m.h_result[i][1] = 0;
+    }
+    m.d_ovf_total = dev_alloc<unsigned long long>(2);
+    EBC_CUDA(cudaMemsetAsync(m.d_ovf_total, 0, 16, m.s_sample));
+    m.d_S = dev_alloc<u64>(g.n + 1);
+    m.d_wide = dev_alloc<u64>(g.n + 1);
+    EBC_CUDA(cudaMemsetAsync(m.d_S, 0, (g.n + 1) * 8, m.s_sample));
+    m.d_ticket = dev_alloc<unsigned long long>(2);
+    m.d_work = dev_alloc<unsigned long long>(kWorkCounters);
+    EBC_CUDA(cudaMemsetAsync(m.d_work, 0, kWorkCounters * 8, m.s_sample));
+    m.d_overflow_list = dev_alloc<u32>(kOverflowCap);
+    m.d_overflow_count = dev_alloc<u32>(2);
+    m.d_fail = dev_alloc<u32>(1);
+    EBC_CUDA(cudaMemsetAsync(m.d_fail, 0, 4, m.s_sample));
+    m.d_log_lower = dev_alloc<double>(g.n);
+    m.d_log_upper = dev_alloc<double>(g.n);
+    m.stop.have = 0;
+    EBC_CUDA(cudaStreamSynchronize(m.s_sample));
+}
+
+CudaSampler::~CudaSampler() {
+    Impl &m = *impl_;
+    cudaDeviceSynchronize();
+    m.small.release();
+    m.big.release();
+    cudaFree(m.d_offsets);
+    cudaFree(m.d_targets);
+    for (int i = 0; i < 2; ++i) {
+        cudaFree(m.d_frame[i]);
+        cudaFreeHost(m.h_result[i]);
+        cudaEventDestroy(m.ev_sampled[i]);
+        cudaEventDestroy(m.ev_folded[i]);
+    }
+    for (int i = 0; i < kEvents; ++i)
+        cudaEventDestroy(m.ev_user[i]);
+    cudaFree(m.d_ovf_total);
+    cudaFree(m.d_S);
+    cudaFree(m.d_wide);
+    cudaFree(m.d_ticket);
+    cudaFree(m.d_work);
+    cudaFree(m.d_overflow_list);
+    cudaFree(m.d_overflow_count);
+    cudaFree(m.d_fail);
+    cudaFree(m.d_log_lower);
+    cudaFree(m.d_log_upper);
+    cudaFree(m.d_dist);
+    cudaFree(m.d_queue[0]);
+    cudaFree(m.d_queue[1]);
+    cudaFree(m.d_bfs);
+    cudaFree(m.d_best);
+    cudaFree(m.d_flush);
+    cudaStreamDestroy(m.s_sample);
+    cudaStreamDestroy(m.s_agg);
+}
+
+std::uint64_t CudaSampler::n() const { return impl_->n; }
+std::uint64_t CudaSampler::overflow_samples() const {
+    unsigned long long o[2];
+    impl_->read_overflow(o);
+    return o[0];
+}
+std::uint64_t CudaSampler::kernel_launches() const { return impl_->launches; }
+
+void CudaSampler::sample(std::uint64_t seed, std::uint32_t tag, std::uint64_t first, std::uint64_t count, int frame) {
+    Impl &m = *impl_;
+    require(frame == 0 || frame == 1, "sample: frame must be 0 or 1");
+    // The frame is being reused: the fold that zeroes it must have finished (epoch.hpp:24-30).
+    EBC_CUDA(cudaStreamWaitEvent(m.s_sample, m.ev_folded[frame], 0));
+    for (u64 done = 0; done < count; done += kOverflowCap) {
+        const u64 chunk = std::min<u64>(kOverflowCap, count - done);
+        m.launch(seed, tag, first + done, chunk, frame, nullptr, nullptr, nullptr, 0);
+    }
+    EBC_CUDA(cudaEventRecord(m.ev_sampled[frame], m.s_sample));
+}
+
+void CudaSampler::sample_debug(std::uint64_t seed, std::uint32_t tag, std::uint64_t first, std::uint64_t count,
+                               const std::uint32_t *pairs, int frame, SampleRecordHost *records,
+                               std::uint32_t *paths, std::uint64_t path_stride) {
+    Impl &m = *impl_;
+    require(frame == 0 || frame == 1, "sample_debug: frame must be 0 or 1");
+    require(count <= kOverflowCap, "sample_debug: at most 2^20 samples per call");
+    static_assert(sizeof(SampleRecordHost) == sizeof(SampleRecordDev), "record layouts must match");
+    u32 *d_pairs = nullptr, *d_paths = nullptr;
+    SampleRecordDev *d_rec = nullptr;
+    if (count == 0)
+        return;
+    try {
+        EBC_CUDA(cudaStreamWaitEvent(m.s_sample, m.ev_folded[frame], 0));
+        if (pairs) {
+            d_pairs = dev_alloc<u32>(2 * count);
+            EBC_CUDA(cudaMemcpyAsync(d_pairs, pairs, 2 * count * 4, cudaMemcpyHostToDevice, m.s_sample));
+        }
+        if (records)
+            d_rec = dev_alloc<SampleRecordDev>(count);
+        if (paths && path_stride) {
+            d_paths = dev_alloc<u32>(count * path_stride);
+            EBC_CUDA(cudaMemsetAsync(d_paths, 0xff, count * path_stride * 4, m.s_sample));
+        }
+        m.launch(seed, tag, first, count, frame, d_pairs, d_rec, d_paths, d_paths ? path_stride : 0);
+        EBC_CUDA(cudaEventRecord(m.ev_sampled[frame], m.s_sample));
+        if (records)
+            EBC_CUDA(cudaMemcpyAsync(records, d_rec, count * sizeof(SampleRecordDev), cudaMemcpyDeviceToHost, m.s_sample));
+        if (d_paths)
+            EBC_CUDA(cudaMemcpyAsync(paths, d_paths, count * path_stride * 4, cudaMemcpyDeviceToHost, m.s_sample));
+        unsigned long long ovf[2];
+        m.read_overflow(ovf);
+    } catch (...) {
+        cudaFree(d_pairs);
+        cudaFree(d_rec);
+        cudaFree(d_paths);
+        throw;
+    }
+    cudaFree(d_pairs);
+    cudaFree(d_rec);
+    cudaFree(d_paths);
+}
+
+// Decodes the label / list / sigma / level arrays of the slot that ran the last
+// sample of a single-slot sampler into per-vertex dist and sigma.
+void CudaSampler::last_state(int side, std::uint32_t *dist_out, std::uint64_t *sigma_out) {
+    Impl &m = *impl_;
+    require(side == 0 || side == 1, "last_state: side must be 0 or 1");
+    require(m.small.slots == 1, "last_state: needs a sampler created with slots == 1");
+    unsigned long long ovf[2];
+    m.read_overflow(ovf);
+    // If the last sample overflowed it was re-run in large slot 0.
+    const bool rerun = m.small.cap < m.n && ovf[0] != m.overflow_seen;
+    m.overflow_seen = ovf[0];
+    const SlotArrays &a = rerun ? m.big : m.small;
+    std::vector<u32> hdr(kHdrWords);
+    EBC_CUDA(cudaMemcpy(hdr.data(), a.hdr, kHdrWords * 4, cudaMemcpyDeviceToHost));
+    const u32 cnt = hdr[kHdrLastCnt0 + side], depth = hdr[kHdrLastDepth0 + side];
+    std::vector<u32> list(cnt), lvl(depth + 2);
+    std::vector<u64> sig(cnt);
+    EBC_CUDA(cudaMemcpy(list.data(), a.list + static_cast<u64>(side) * a.cap, cnt * 4ull, cudaMemcpyDeviceToHost));
+    EBC_CUDA(cudaMemcpy(sig.data(), a.sig + static_cast<u64>(side) * a.cap, cnt * 8ull, cudaMemcpyDeviceToHost));
+    EBC_CUDA(cudaMemcpy(lvl.data(), a.lvl + static_cast<u64>(side) * (a.cap + 2), (depth + 1) * 4ull, cudaMemcpyDeviceToHost));
+    lvl[depth + 1] = cnt;
+    for (u64 v = 0; v < m.n; ++v) {
+        dist_out[v] = 0xffffffffu;
+        sigma_out[v] = 0;
+    }
+    for (u32 d = 0; d <= depth; ++d)
+        for (u32 i = lvl[d]; i < lvl[d + 1]; ++i) {
+            dist_out[list[i]] = d;
+            sigma_out[list[i]] = sig[i];
+        }
+}
+
+void CudaSampler::set_stopping(double eps, std::uint64_t omega, const double *delta_lower,
+                               const double *delta_upper, int bound) {
+    Impl &m = *impl_;
+    require(bound == 0 || bound == 1, "set_stopping: unknown bound kind");
+    std::vector<double> lo(m.n), up(m.n);
+    bound_log_terms(delta_lower, m.n, bound, lo.data());
+    bound_log_terms(delta_upper, m.n, bound, up.data());
+    EBC_CUDA(cudaMemcpy(m.d_log_lower, lo.data(), m.n * 8, cudaMemcpyHostToDevice));
+    EBC_CUDA(cudaMemcpy(m.d_log_upper, up.data(), m.n * 8, cudaMemcpyHostToDevice));
+    m.stop.eps = eps;
+    m.stop.omega = omega;
+    m.stop.log_lower = m.d_log_lower;
+    m.stop.log_upper = m.d_log_upper;
+    m.stop.bound = bound;
+    m.stop.have = 1;
+}
+
+void CudaSampler::fold_and_check_async(int frame, AllreduceFn allreduce, void *user) {
+    Impl &m = *impl_;
+    require(frame == 0 || frame == 1, "fold_and_check: frame must be 0 or 1");
+    EBC_CUDA(cudaStreamWaitEvent(m.s_agg, m.ev_sampled[frame], 0));
+    if (allreduce) {
+        if (allreduce(user, m.d_frame[frame], m.n + 1, m.s_agg) != 0)
+            throw BackendFault("allreduce callback failed");
+    }
+    m.h_result[frame][0] = ~u64{0};
+    u64 *d_result = nullptr;
+    EBC_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void **>(&d_result), m.h_result[frame], 0));
+    const u32 grid = static_cast<u32>(std::min<u64>((m.n + 255) / 256, static_cast<u64>(m.sm_count) * 8));
+    fold_check_kernel<<<grid, 256, 0, m.s_agg>>>(m.d_frame[frame], m.d_S, m.n, m.stop, m.d_fail);
+    finish_fold_kernel<<<1, 1, 0, m.s_agg>>>(m.d_frame[frame], m.d_S, m.stop, m.d_fail, d_result);
+    EBC_CUDA(cudaGetLastError());
+    m.launches += 2;
+    EBC_CUDA(cudaEventRecord(m.ev_folded[frame], m.s_agg));
+    m.folded_pending[frame] = true;
+}
+
+bool CudaSampler::wait_fold(int frame, std::uint64_t *tau_out) {
+    Impl &m = *impl_;
+    require(frame == 0 || frame == 1, "wait_fold: frame must be 0 or 1");
+    require(m.folded_pending[frame], "wait_fold: no fold in flight for this frame");
+    EBC_CUDA(cudaEventSynchronize(m.ev_folded[frame]));
+    m.folded_pending[frame] = false;
+    if (tau_out)
+        *tau_out = m.h_result[frame][1];
+    return m.h_result[frame][0] == 1;
+}
+
+void CudaSampler::discard_frame(int frame) {
+    Impl &m = *impl_;
+    require(frame == 0 || frame == 1, "discard_frame: frame must be 0 or 1");
+    EBC_CUDA(cudaStreamWaitEvent(m.s_agg, m.ev_sampled[frame], 0));
+    EBC_CUDA(cudaMemsetAsync(m.d_frame[frame], 0, (m.n + 1) * 4, m.s_agg));
+    EBC_CUDA(cudaEventRecord(m.ev_folded[frame], m.s_agg));
+    EBC_CUDA(cudaStreamSynchronize(m.s_agg));
+}
+
+void CudaSampler::read_frame(int which, std::uint64_t *words_out) {
+    Impl &m = *impl_;
+    require(which >= 0 && which <= 2, "read_frame: which must be 0, 1 or 2");
+    EBC_CUDA(cudaStreamSynchronize(m.s_sample));
+    EBC_CUDA(cudaStreamSynchronize(m.s_agg));
+    if (which == 2) {
+        EBC_CUDA(cudaMemcpy(words_out, m.d_S, (m.n + 1) * 8, cudaMemcpyDeviceToHost));
+        return;
+    }
+    widen_kernel<<<static_cast<u32>(m.sm_count) * 4, 256, 0, m.s_sample>>>(m.d_frame[which], m.d_wide, m.n + 1);
+    EBC_CUDA(cudaGetLastError());
+    EBC_CUDA(cudaMemcpyAsync(words_out, m.d_wide, (m.n + 1) * 8, cudaMemcpyDeviceToHost, m.s_sample));
+    EBC_CUDA(cudaStreamSynchronize(m.s_sample));
+}
+
+void CudaSampler::write_state(const std::uint64_t *words) {
+    Impl &m = *impl_;
+    EBC_CUDA(cudaStreamSynchronize(m.s_sample));
+    EBC_CUDA(cudaStreamSynchronize(m.s_agg));
+    EBC_CUDA(cudaMemcpy(m.d_S, words, (m.n + 1) * 8, cudaMemcpyHostToDevice));
+}
+
+void CudaSampler::clear() {
+    Impl &m = *impl_;
+    EBC_CUDA(cudaStreamSynchronize(m.s_sample));
+    EBC_CUDA(cudaStreamSynchronize(m.s_agg));
+    for (int i = 0; i < 2; ++i)
+        EBC_CUDA(cudaMemset(m.d_frame[i], 0, (m.n + 1) * 4));
+    EBC_CUDA(cudaMemset(m.d_S, 0, (m.n + 1) * 8));
+}
+
+void CudaSampler::work(std::uint64_t *out, bool reset) {
+    Impl &m = *impl_;
+    EBC_CUDA(cudaStreamSynchronize(m.s_sample));
+    EBC_CUDA(cudaMemcpy(out, m.d_work, kWorkCounters * 8, cudaMemcpyDeviceToHost));
+    if (reset)
+        EBC_CUDA(cudaMemset(m.d_work, 0, kWorkCounters * 8));
+}
+
+void CudaSampler::mark(int event) {
+    require(event >= 0 && event < kEvents, "mark: event index out of range");
+    EBC_CUDA(cudaEventRecord(impl_->ev_user[event], impl_->s_sample));
+}
+
+float CudaSampler::elapsed_ms(int from, int to) {
+    require(from >= 0 && from < kEvents && to >= 0 && to < kEvents, "elapsed_ms: event index out of range");
+    EBC_CUDA(cudaEventSynchronize(impl_->ev_user[to]));
+    float ms = 0.f;
+    EBC_CUDA(cudaEventElapsedTime(&ms, impl_->ev_user[from], impl_->ev_user[to]));
+    return ms;
+}
+
+void CudaSampler::sync() {
+    EBC_CUDA(cudaStreamSynchronize(impl_->s_sample));
+    EBC_CUDA(cudaStreamSynchronize(impl_->s_agg));
+}
+
+void CudaSampler::info(std::uint64_t *out) {
+    Impl &m = *impl_;
+    out[0] = m.small.slots;
+    out[1] = m.block;
+    out[2] = m.small.cap;
+    out[3] = m.small.bytes + m.big.bytes + m.graph_bytes + (m.n + 1) * (4 * 2 + 8 + 8 + 16);
+    out[4] = static_cast<std::uint64_t>(m.sm_count);
+    out[5] = m.launches;
+}
+
+void *CudaSampler::stream_handle() { return impl_->s_sample; }
+
+void CudaSampler::frame_ptr(int frame, void **ptr, std::uint64_t *words) {
+    require(frame == 0 || frame == 1, "frame_ptr: frame must be 0 or 1");
+    *ptr = impl_->d_frame[frame];
+    *words = impl_->n + 1;
+}
+
+BfsSummary CudaSampler::bfs(std::uint32_t source, std::uint32_t *dist_out) {
+    Impl &m = *impl_;
+    require(source < m.n, "bfs: source out of range");
+    if (!m.d_dist) {
+        m.d_dist = dev_alloc<u32>(m.n);
+        m.d_queue[0] = dev_alloc<u32>(m.n);
+        m.d_queue[1] = dev_alloc<u32>(m.n);
+        m.d_bfs = dev_alloc<BfsState>(1);
+        m.d_best = dev_alloc<unsigned long long>(1);
+    }
+    cudaStream_t st = m.s_sample;
+    EBC_CUDA(cudaMemsetAsync(m.d_dist, 0xff, m.n * 4, st));
+    BfsState init{};
+    init.queue_size[0] = 1;
+    init.reached = 1;
+    EBC_CUDA(cudaMemcpyAsync(m.d_bfs, &init, sizeof(init), cudaMemcpyHostToDevice, st));
+    const u32 zero = 0;
+    EBC_CUDA(cudaMemcpyAsync(m.d_dist + source, &zero, 4, cudaMemcpyHostToDevice, st));
+    EBC_CUDA(cudaMemcpyAsync(m.d_queue[0], &source, 4, cudaMemcpyHostToDevice, st));
+    EBC_CUDA(cudaMemsetAsync(m.d_best, 0, 8, st));
+    const u32 grid = static_cast<u32>(m.sm_count) * 8;
+    BfsState host{};
+    for (u32 level = 0;;) {
+        for (int k = 0; k < 32; ++k, ++level) { // 32 levels per host round trip
+            bfs_level_kernel<<<grid, 256, 0, st>>>(m.d_offsets, m.d_targets, m.d_dist, m.d_queue[0], m.d_queue[1], m.d_bfs, level);
+            bfs_advance_kernel<<<1, 1, 0, st>>>(m.d_bfs, level);
+            m.launches += 2;
+        }
+        EBC_CUDA(cudaGetLastError());
+        EBC_CUDA(cudaMemcpyAsync(&host, m.d_bfs, sizeof(host), cudaMemcpyDeviceToHost, st));
+        EBC_CUDA(cudaStreamSynchronize(st));
+        if (host.done)
+            break;
+    }
+    bfs_farthest_kernel<<<grid, 256, 0, st>>>(m.d_dist, m.n, m.d_best);
+    ++m.launches;
+    unsigned long long best = 0;
+    EBC_CUDA(cudaMemcpyAsync(&best, m.d_best, 8, cudaMemcpyDeviceToHost, st));
+    if (dist_out)
+        EBC_CUDA(cudaMemcpyAsync(dist_out, m.d_dist, m.n * 4, cudaMemcpyDeviceToHost, st));
+    EBC_CUDA(cudaStreamSynchronize(st));
+    BfsSummary r;
+    r.eccentricity = static_cast<u32>(best >> 32);
+    r.farthest = 0xffffffffu - static_cast<u32>(best & 0xffffffffu);
+    r.reached = host.reached;
+    return r;
+}
+
+void CudaSampler::flush_l2() {
+    Impl &m = *impl_;
+    if (!m.d_flush) {
+        m.flush_words = (u64{192} << 20) / 4; // 192 MiB > 126 MB L2
+        m.d_flush = dev_alloc<u32>(m.flush_words);
+    }
+    static u32 salt = 0;
+    flush_kernel<<<static_cast<u32>(m.sm_count) * 8, 256, 0, m.s_sample>>>(m.d_flush, m.flush_words, ++salt);
+    EBC_CUDA(cudaGetLastError());
+}
+
+} // namespace ebc

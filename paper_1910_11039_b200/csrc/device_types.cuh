@@ -1,0 +1,85 @@
+// Device-side data layout of the B200 KADABRA sampler ("Data
+// layout in HBM").  Everything a sample needs lives in one *slot*; a slot is
+// owned by exactly one resident CTA for the duration of a kernel.
+#pragma once
+
+#include <cstdint>
+
+namespace ebc {
+
+using u32 = std::uint32_t;
+using u64 = std::uint64_t;
+
+// Work counters; indices shared with the C ABI
+// (ebc_sampler_work) and with the oracle's instrumented restatement.
+enum WorkCounter : int {
+    kW_E_bfs = 0,
+    kW_E_lvl,
+    kW_V_exp,
+    kW_V_set,
+    kW_F_chk,
+    kW_M,
+    kW_S_walk,
+    kW_E_walk,
+    kW_P_walk,
+    kW_L,
+    kW_levels,
+    kW_samples,
+    kWorkCounters
+};
+
+// Labels.  One u32 per vertex per side replaces the reference's
+// (stamp, dist, sigma) triple (sampler.hpp:39-54): label = base + idx, where
+// idx is the vertex' position in the side's discovery-ordered settle list and
+// base advances by the number of settled vertices after every sample (O(1)
+// reset like SearchScratch::round_, sampler.cpp:63).  visited <=> label - base <
+// settled count; dist is implied by idx (levels occupy contiguous idx ranges).
+constexpr u32 kClaimTop = 0xffffffffu;     // transient claim values: kClaimTop - slot_in_tile
+constexpr u32 kMaxBlockThreads = 1024;
+constexpr u32 kHdrWords = 16;              // per-slot header (u32)
+// header word indices
+enum : int { kHdrBase0 = 0, kHdrBase1 = 1, kHdrLastBase0 = 2, kHdrLastBase1 = 3, kHdrLastCnt0 = 4,
+             kHdrLastCnt1 = 5, kHdrLastDepth0 = 6, kHdrLastDepth1 = 7 };
+
+struct SampleRecordDev { // mirrors ebc_sample_record
+    u32 s, t, dist, meet, meet_count, draws, path_len, flags;
+    u64 weight_lo, weight_hi;
+};
+
+struct SamplerParams {
+    // graph (replicated CSR)
+    u64 n;
+    const u64 *offsets;
+    const u32 *targets;
+    // slots
+    u32 *lab;      // [slots][2][n]
+    u32 *list;     // [slots][2][cap]   settled vertices in discovery order
+    u64 *sig;      // [slots][2][cap]   sigma, same indexing
+    u32 *lvl;      // [slots][2][cap+2] level start offsets into list
+    u32 *contact;  // [slots][2][cap]   (idx on expanding side, idx on other side) of contact vertices
+    u32 *hdr;      // [slots][kHdrWords]
+    u64 cap;
+    // work
+    u64 seed;
+    u32 tag;
+    u64 first;
+    u64 count;
+    unsigned long long *ticket; // dynamic sample dispenser
+    u32 *frame;                 // epoch frame, n+1 u32 (word 0 = tau)
+    const u32 *pairs;           // optional explicit (s,t) pairs, 2*count
+    SampleRecordDev *records;   // optional
+    u32 *paths;                 // optional, path_stride per sample
+    u64 path_stride;
+    unsigned long long *work;   // kWorkCounters
+    u32 *overflow_list;         // local sample indices that overflowed slot capacity
+    u32 *overflow_count;
+    u32 overflow_cap;
+    // re-run pass over an earlier launch's overflow list (large slots): local
+    // sample index = relist[ticket], number of tickets = min(*count_ptr, count)
+    const u32 *relist;
+    const u32 *count_ptr;
+    u64 slot_base;              // first slot used by this launch
+    unsigned long long *overflow_total; // persistent count of abandoned samples of this pass
+};
+
+} // namespace ebc

@@ -1,0 +1,779 @@
+// Batched KADABRA sampling kernel for sm_100a.
+//
+// One CTA = one sample at a time (persistent CTAs pull sample indices from a
+// ticket counter).  A sample is: draw (s,t) -> balanced bidirectional BFS with
+// sigma counting -> sigma-weighted meet vertex -> sigma-weighted walks to both
+// endpoints -> counter increments.  Results are bit-identical to the
+// reference's sample_pair + sample_shortest_path + apply_sample
+//   /root/reference/proj/src/sampler.cpp:45-52, 54-164
+//   /root/reference/proj/include/epochbc/sampler.hpp:74-78
+// under the shared Philox stream (philox.cuh).
+//
+// How order-dependent reference semantics survive a parallel expansion
+// (hard part 1): the reference picks the meet vertex by a
+// prefix walk over the new frontier in DISCOVERY order (sampler.cpp:111-113,
+// 126-133), and discovery order is (position of first parent in the frontier,
+// index in that parent's sorted row).  Here a level's adjacency slots are
+// enumerated in exactly that order and processed in tiles of BLOCK slots; in a
+// tile every undiscovered target is claimed with atomicMax(label, TOP - slot),
+// so the LOWEST slot wins, and winners are ranked by an ordered block scan.
+// Earlier tiles are final before later tiles start, hence idx == the
+// reference's position in `next` (sampler.cpp:92-95).  Sigma sums, pending
+// edge counts and counters are order independent.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "device_types.cuh"
+#include "philox.cuh"
+
+namespace ebc {
+
+using u128 = unsigned __int128;
+
+__device__ __forceinline__ u32 ld_cg(const u32 *p) { return __ldcg(p); }
+__device__ __forceinline__ u64 ld_cg(const u64 *p) { return __ldcg(reinterpret_cast<const unsigned long long *>(p)); }
+__device__ __forceinline__ void st_cg(u32 *p, u32 v) { __stcg(p, v); }
+__device__ __forceinline__ void st_cg(u64 *p, u64 v) { __stcg(reinterpret_cast<unsigned long long *>(p), v); }
+
+__device__ __forceinline__ u32 lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ u32 lanemask_lt() {
+    u32 m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// sigma[idx] = sat_add_u64(sigma[idx], add)  (sampler.cpp:11-13,98) with atomics:
+// a wrapped add is always followed by the same thread's atomicMax(.., 2^64-1),
+// so the value after the level barrier is 2^64-1 iff the true sum overflowed.
+__device__ __forceinline__ void sat_atomic_add(u64 *p, u64 add) {
+    unsigned long long *q = reinterpret_cast<unsigned long long *>(p);
+    const unsigned long long old = atomicAdd(q, static_cast<unsigned long long>(add));
+    if (old + add < old)
+        atomicMax(q, ~0ull);
+}
+
+// uniform_below_u128 (sampler.cpp:21-30).  Executed redundantly by every thread
+// of the CTA (the stream state is uniform), so no broadcast is needed.
+__device__ __forceinline__ u128 uniform_below_u128(SampleStream &rng, u128 bound) {
+    if (static_cast<u64>(bound >> 64) == 0)
+        return rng.next_below(static_cast<u64>(bound));
+    const u128 all = ~static_cast<u128>(0);
+    const u128 reject_from = all - (all % bound);
+    for (;;) {
+        const u128 hi = rng.next_u64();
+        const u128 lo = rng.next_u64();
+        const u128 r = (hi << 64) | lo;
+        if (r < reject_from)
+            return r % bound;
+    }
+}
+
+template <int BLOCK> struct BlockShared {
+    static constexpr int WARPS = BLOCK / 32;
+    u64 c_beg[BLOCK];      // row start of each frontier-chunk vertex
+    u64 c_scan[BLOCK + 1]; // exclusive prefix of the chunk's degrees
+    u64 c_sig[BLOCK];      // sigma of each chunk vertex
+    u64 red64[WARPS * 3];  // block reductions
+    u32 warp_cnt[WARPS];
+    u32 warp_cnt2[WARPS];
+    unsigned long long ticket;
+    u32 min_contact;       // min other-side idx over contact vertices of this level
+    u32 found_lane;        // ordered-search result
+    u64 found_aux;
+    u32 pred_cnt;
+    u32 pred_pos[32];
+    u64 pred_sig[32];
+    u32 pred_vtx[32];
+    u32 bcast[4];
+    u64 ws[kWorkCounters]; // work counters of the sample in flight (thread 0)
+    u64 wk[kWorkCounters]; // committed work counters of this CTA
+};
+
+// Rank of this thread among the threads with flag set (thread order) and the total.
+// Contains one __syncthreads; warp_cnt must not be reused before the next barrier.
+template <int BLOCK> __device__ __forceinline__ u32 block_rank(bool flag, u32 &total, u32 *warp_cnt) {
+    const u32 ballot = __ballot_sync(0xffffffffu, flag);
+    const u32 in_warp = __popc(ballot & lanemask_lt());
+    if (BLOCK == 32) {
+        total = __popc(ballot);
+        return in_warp;
+    }
+    const u32 warp = threadIdx.x >> 5;
+    if (lane_id() == 0)
+        warp_cnt[warp] = __popc(ballot);
+    __syncthreads();
+    u32 before = 0, all = 0;
+#pragma unroll
+    for (int w = 0; w < BLOCK / 32; ++w) {
+        const u32 c = warp_cnt[w];
+        all += c;
+        before += (w < warp) ? c : 0;
+    }
+    total = all;
+    return before + in_warp;
+}
+
+template <int BLOCK> __device__ __forceinline__ u64 block_sum_u64(u64 v, u64 *red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (BLOCK == 32)
+        return v;
+    __syncthreads();
+    if (lane_id() == 0)
+        red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    u64 s = 0;
+#pragma unroll
+    for (int w = 0; w < BLOCK / 32; ++w)
+        s += red[w];
+    return s;
+}
+
+// 192-bit sum (lo, hi, carry-out count) of per-thread 128-bit values.
+template <int BLOCK>
+__device__ __forceinline__ void block_sum_u128(u128 v, u64 &lo, u64 &hi, u64 &ovf, u64 *red) {
+    u64 a = static_cast<u64>(v), b = static_cast<u64>(v >> 64), c = 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const u64 a2 = __shfl_xor_sync(0xffffffffu, a, o);
+        const u64 b2 = __shfl_xor_sync(0xffffffffu, b, o);
+        const u64 c2 = __shfl_xor_sync(0xffffffffu, c, o);
+        const u128 x = (static_cast<u128>(b) << 64) | a, y = (static_cast<u128>(b2) << 64) | a2;
+        const u128 s = x + y;
+        c += c2 + (s < x ? 1 : 0);
+        a = static_cast<u64>(s);
+        b = static_cast<u64>(s >> 64);
+    }
+    if (BLOCK > 32) {
+        __syncthreads();
+        if (lane_id() == 0) {
+            red[(threadIdx.x >> 5) * 3 + 0] = a;
+            red[(threadIdx.x >> 5) * 3 + 1] = b;
+            red[(threadIdx.x >> 5) * 3 + 2] = c;
+        }
+        __syncthreads();
+        u128 s = 0;
+        c = 0;
+#pragma unroll
+        for (int w = 0; w < BLOCK / 32; ++w) {
+            const u128 y = (static_cast<u128>(red[w * 3 + 1]) << 64) | red[w * 3 + 0];
+            const u128 t = s + y;
+            c += red[w * 3 + 2] + (t < s ? 1 : 0);
+            s = t;
+        }
+        a = static_cast<u64>(s);
+        b = static_cast<u64>(s >> 64);
+    }
+    lo = a;
+    hi = b;
+    ovf = c;
+}
+
+// Ordered search: first thread (in thread order) whose inclusive 128-bit prefix
+// of `w` exceeds `pick - running`.  Returns the thread index or BLOCK if none;
+// `running` is advanced by the block total when nothing is found.  Values that
+// overflow 128 bits compare as "exceeds".
+template <int BLOCK>
+__device__ __forceinline__ u32 block_first_exceeding(u128 w, u128 &running, bool &running_ovf, u128 pick,
+                                                     BlockShared<BLOCK> &sh) {
+    // inclusive warp scan
+    u64 a = static_cast<u64>(w), b = static_cast<u64>(w >> 64);
+    u32 of = 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u64 a2 = __shfl_up_sync(0xffffffffu, a, o);
+        const u64 b2 = __shfl_up_sync(0xffffffffu, b, o);
+        const u32 of2 = __shfl_up_sync(0xffffffffu, of, o);
+        if (lane_id() >= static_cast<u32>(o)) {
+            const u128 x = (static_cast<u128>(b) << 64) | a, y = (static_cast<u128>(b2) << 64) | a2;
+            const u128 s = x + y;
+            of |= of2 | (s < x ? 1u : 0u);
+            a = static_cast<u64>(s);
+            b = static_cast<u64>(s >> 64);
+        }
+    }
+    u128 incl = (static_cast<u128>(b) << 64) | a;
+    bool incl_of = of != 0;
+    const u32 warp = threadIdx.x >> 5;
+    if (BLOCK > 32) {
+        __syncthreads();
+        if (lane_id() == 31) {
+            sh.red64[warp * 3 + 0] = a;
+            sh.red64[warp * 3 + 1] = b;
+            sh.red64[warp * 3 + 2] = of;
+        }
+        __syncthreads();
+        u128 before = 0;
+        bool before_of = false;
+        for (u32 k = 0; k < warp; ++k) {
+            const u128 y = (static_cast<u128>(sh.red64[k * 3 + 1]) << 64) | sh.red64[k * 3 + 0];
+            const u128 t = before + y;
+            before_of = before_of || sh.red64[k * 3 + 2] != 0 || t < before;
+            before = t;
+        }
+        const u128 t = incl + before;
+        incl_of = incl_of || before_of || t < incl;
+        incl = t;
+    }
+    // add the running prefix of earlier chunks
+    const u128 tot = incl + running;
+    const bool tot_of = incl_of || running_ovf || tot < incl;
+    const bool hit = (w != 0) && (tot_of || tot > pick);
+    // first hit in thread order
+    const u32 ballot = __ballot_sync(0xffffffffu, hit);
+    if (threadIdx.x == 0)
+        sh.found_lane = BLOCK;
+    __syncthreads();
+    if (ballot != 0 && lane_id() == 0)
+        atomicMin(&sh.found_lane, (warp << 5) + (__ffs(ballot) - 1));
+    // block total -> new running (taken from the last thread)
+    if (threadIdx.x == BLOCK - 1) {
+        sh.red64[0] = static_cast<u64>(tot);
+        sh.red64[1] = static_cast<u64>(tot >> 64);
+        sh.red64[2] = tot_of ? 1 : 0;
+    }
+    __syncthreads();
+    const u32 found = sh.found_lane;
+    if (found == BLOCK) {
+        running = (static_cast<u128>(sh.red64[1]) << 64) | sh.red64[0];
+        running_ovf = sh.red64[2] != 0;
+    }
+    __syncthreads();
+    return found;
+}
+
+struct SideRegs {
+    u32 *lab;
+    u32 *list;
+    u64 *sig;
+    u32 *lvl;
+    u32 base;  // label base of this sample
+    u32 cnt;   // settled vertices so far
+    u32 fb;    // frontier = list[fb .. cnt)
+    u32 depth; // depth of the frontier
+    u64 pending;
+};
+
+// Per-thread partial work counters of the sample in flight (the thread-0-only
+// counters live in BlockShared::ws).
+struct WorkRegs {
+    u64 e_lvl = 0, p_walk = 0;
+};
+
+// Expands the frontier of side `ex` by one level (sampler.cpp:86-103) and
+// records contacts with the other side (sampler.cpp:105-108).  Returns false on
+// slot-capacity overflow (the sample is then re-run in a large slot).
+// contact_n returns the number of contact vertices appended to `contact`.
+template <int BLOCK>
+__device__ bool expand_level(const SamplerParams &p, SideRegs &ex, const SideRegs &ot, u32 *contact,
+                             u32 &contact_n, BlockShared<BLOCK> &sh, WorkRegs &wk) {
+    const u32 tid = threadIdx.x;
+    const u32 fb = ex.fb, fe = ex.cnt;
+    const u32 level_start = fe;
+    const u32 next_depth = ex.depth + 1;
+    u32 cnt = fe;
+    u64 pend = 0;
+    contact_n = 0;
+    if (tid == 0) {
+        st_cg(ex.lvl + next_depth, level_start);
+        sh.min_contact = 0xffffffffu;
+        sh.ws[kW_V_exp] += fe - fb;
+        sh.ws[kW_levels] += 1;
+    }
+    for (u32 c0 = fb; c0 < fe; c0 += BLOCK) {
+        // ---- load a chunk of BLOCK frontier vertices, scan their degrees ----
+        const u32 i = c0 + tid;
+        u64 beg = 0, deg = 0, su = 0;
+        if (i < fe) {
+            const u32 u = ld_cg(ex.list + i);
+            beg = __ldg(p.offsets + u);
+            deg = __ldg(p.offsets + u + 1) - beg;
+            su = ld_cg(ex.sig + i);
+        }
+        // inclusive warp scan of deg
+        u64 inc = deg;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u64 t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane_id() >= static_cast<u32>(o))
+                inc += t;
+        }
+        __syncthreads(); // previous chunk's tiles are done with c_* and red64
+        if (BLOCK > 32 && lane_id() == 31)
+            sh.red64[tid >> 5] = inc;
+        sh.c_beg[tid] = beg;
+        sh.c_sig[tid] = su;
+        if (BLOCK > 32)
+            __syncthreads();
+        u64 before = 0;
+        if (BLOCK > 32)
+            for (u32 w = 0; w < (tid >> 5); ++w)
+                before += sh.red64[w];
+        sh.c_scan[tid + 1] = before + inc;
+        if (tid == 0)
+            sh.c_scan[0] = 0;
+        __syncthreads();
+        const u64 T = sh.c_scan[BLOCK];
+        if (tid == 0)
+            sh.ws[kW_E_bfs] += T;
+
+        // ---- ordered tiles of BLOCK adjacency slots ----
+        for (u64 t0 = 0; t0 < T; t0 += BLOCK) {
+            const u64 j = t0 + tid;
+            const bool active = j < T;
+            u32 v = 0, idx = 0;
+            u64 sig_u = 0;
+            bool candidate = false, at_level = false;
+            if (active) {
+                // owner row: last r with c_scan[r] <= j
+                int lo = 0, hi = BLOCK;
+                while (hi - lo > 1) {
+                    const int mid = (lo + hi) >> 1;
+                    if (sh.c_scan[mid] <= j)
+                        lo = mid;
+                    else
+                        hi = mid;
+                }
+                v = __ldg(p.targets + sh.c_beg[lo] + (j - sh.c_scan[lo]));
+                sig_u = sh.c_sig[lo];
+                const u32 rel = ld_cg(ex.lab + v) - ex.base;
+                if (rel < cnt) { // visited (sampler.cpp:92 false)
+                    idx = rel;
+                    at_level = rel >= level_start; // dist[v] == next_depth (sampler.cpp:97)
+                } else {
+                    candidate = true;
+                    atomicMax(ex.lab + v, kClaimTop - tid);
+                }
+            }
+            __syncthreads(); // claims visible
+            bool win = false;
+            if (candidate)
+                win = ld_cg(ex.lab + v) == kClaimTop - tid;
+            u32 winners;
+            const u32 rank = block_rank<BLOCK>(win, winners, sh.warp_cnt);
+            const bool overflow = static_cast<u64>(cnt) + winners > p.cap;
+            bool is_contact = false;
+            u32 other_idx = 0;
+            if (win) {
+                if (overflow) {
+                    st_cg(ex.lab + v, 0u); // undo the claim; the sample is abandoned
+                } else {
+                    idx = cnt + rank; // settle (sampler.cpp:93-95, sampler.hpp:49-53)
+                    st_cg(ex.lab + v, ex.base + idx);
+                    st_cg(ex.list + idx, v);
+                    st_cg(ex.sig + idx, static_cast<u64>(0));
+                    pend += __ldg(p.offsets + v + 1) - __ldg(p.offsets + v);
+                    other_idx = ld_cg(ot.lab + v) - ot.base; // other.visited(v) (sampler.cpp:107)
+                    is_contact = other_idx < ot.cnt;
+                    if (is_contact)
+                        atomicMin(&sh.min_contact, other_idx);
+                }
+            }
+            const int any_contact = __syncthreads_or(is_contact ? 1 : 0); // finals visible
+            if (overflow) {
+                ex.cnt = cnt; // labels up to cnt were handed out; the caller retires them
+                return false;
+            }
+            if (candidate && !win)
+                idx = ld_cg(ex.lab + v) - ex.base;
+            if (active && (candidate || at_level)) {
+                sat_atomic_add(ex.sig + idx, sig_u); // sampler.cpp:97-98
+                wk.e_lvl += 1;
+            }
+            if (any_contact) { // ordered append of (idx, other idx)
+                u32 ctot;
+                const u32 crank = block_rank<BLOCK>(is_contact, ctot, sh.warp_cnt2);
+                if (is_contact) {
+                    st_cg(contact + 2 * (contact_n + crank), idx);
+                    st_cg(contact + 2 * (contact_n + crank) + 1, other_idx);
+                }
+                contact_n += ctot;
+            }
+            cnt += winners;
+        }
+    }
+    pend = block_sum_u64<BLOCK>(pend, sh.red64);
+    __syncthreads();
+    if (tid == 0) {
+        sh.ws[kW_V_set] += cnt - level_start;
+        sh.ws[kW_F_chk] += cnt - level_start;
+    }
+    ex.fb = level_start; // sampler.cpp:101-103
+    ex.cnt = cnt;
+    ex.pending = pend;
+    ex.depth = next_depth;
+    return true;
+}
+
+// One sigma-weighted step chain from `u` (at depth d on `sd`) to the side's root
+// (sampler.cpp:135-155).  Emits every vertex strictly between into the frame
+// and, optionally, into path_out[pos], pos advancing by pos_step.
+template <int BLOCK>
+__device__ void walk_side(const SamplerParams &p, const SideRegs &sd, u32 u, u32 d, SampleStream &rng,
+                          u32 *path_out, long long pos, int pos_step, u32 &emitted,
+                          BlockShared<BLOCK> &sh, WorkRegs &wk) {
+    const u32 tid = threadIdx.x;
+    while (d > 0) {
+        // predecessors = neighbours w with visited(w) && dist[w] + 1 == dist[u]
+        //              = label(w) - base in [lvl[d-1], lvl[d])
+        const u32 lo = ld_cg(sd.lvl + (d - 1)), hi = ld_cg(sd.lvl + d);
+        const u32 span = hi - lo;
+        const u32 lab_lo = sd.base + lo;
+        const u64 beg = __ldg(p.offsets + u), end = __ldg(p.offsets + u + 1);
+        if (tid == 0) {
+            sh.pred_cnt = 0;
+            sh.ws[kW_S_walk] += 1;
+            sh.ws[kW_E_walk] += end - beg;
+        }
+        __syncthreads();
+        // pass 1 (sampler.cpp:138-141): total = sum of sigma over predecessors
+        u128 total_local = 0;
+        for (u64 k = beg + tid; k < end; k += BLOCK) {
+            const u32 w = __ldg(p.targets + k);
+            const u32 rel = ld_cg(sd.lab + w) - lab_lo;
+            if (rel < span) {
+                const u64 sg = ld_cg(sd.sig + lo + rel);
+                total_local += sg;
+                wk.p_walk += 1;
+                const u32 slot = atomicAdd(&sh.pred_cnt, 1u);
+                if (slot < 32) {
+                    sh.pred_pos[slot] = static_cast<u32>(k - beg);
+                    sh.pred_sig[slot] = sg;
+                    sh.pred_vtx[slot] = w;
+                }
+            }
+        }
+        u64 tlo, thi, tov;
+        block_sum_u128<BLOCK>(total_local, tlo, thi, tov, sh.red64);
+        const u128 total = (static_cast<u128>(thi) << 64) | tlo; // < 2^96, cannot overflow
+        __syncthreads();
+        const u32 npred = sh.pred_cnt;
+        u128 r = uniform_below_u128(rng, total); // sampler.cpp:142
+        u32 chosen = u;
+        if (npred <= 32) {
+            // pass 2 on the cached predecessors, in CSR order (sampler.cpp:143-151)
+            if (tid < 32) {
+                const bool have = tid < npred;
+                const u32 mypos = have ? sh.pred_pos[tid] : 0xffffffffu;
+                const u64 mysig = have ? sh.pred_sig[tid] : 0;
+                u128 before = 0;
+                for (u32 q = 0; q < npred; ++q) {
+                    const u32 qpos = sh.pred_pos[q];
+                    if (qpos < mypos)
+                        before += sh.pred_sig[q];
+                }
+                if (have && before <= r && r - before < mysig)
+                    sh.bcast[0] = sh.pred_vtx[tid];
+            }
+            __syncthreads();
+            chosen = sh.bcast[0];
+        } else {
+            // pass 2 by re-scanning the row in order with a block-wide prefix search
+            u128 running = 0;
+            bool running_ovf = false;
+            for (u64 k0 = beg; k0 < end; k0 += BLOCK) {
+                const u64 k = k0 + tid;
+                u128 wv = 0;
+                u32 w = 0;
+                if (k < end) {
+                    w = __ldg(p.targets + k);
+                    const u32 rel = ld_cg(sd.lab + w) - lab_lo;
+                    if (rel < span)
+                        wv = ld_cg(sd.sig + lo + rel);
+                }
+                const u32 f = block_first_exceeding<BLOCK>(wv, running, running_ovf, r, sh);
+                if (f != BLOCK) {
+                    if (tid == f)
+                        sh.bcast[0] = w;
+                    __syncthreads();
+                    chosen = sh.bcast[0];
+                    break;
+                }
+            }
+        }
+        __syncthreads();
+        u = chosen;
+        d -= 1;
+        if (d > 0) { // sampler.cpp:152-153: endpoints are never counted
+            if (tid == 0) {
+                atomicAdd(p.frame + 1 + u, 1u); // apply_sample (sampler.hpp:77)
+                if (path_out)
+                    path_out[pos] = u;
+            }
+            pos += pos_step;
+            emitted += 1;
+        }
+    }
+}
+
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) sample_kernel(const SamplerParams p) {
+    __shared__ BlockShared<BLOCK> sh;
+    const u32 tid = threadIdx.x;
+    const u64 slot = p.slot_base + blockIdx.x;
+    const u64 n = p.n;
+    u64 ticket_count = p.count;
+    if (p.count_ptr) {
+        const u64 listed = *p.count_ptr;
+        ticket_count = listed < ticket_count ? listed : ticket_count;
+    }
+
+    SideRegs side[2];
+    for (int k = 0; k < 2; ++k) {
+        side[k].lab = p.lab + (slot * 2 + k) * n;
+        side[k].list = p.list + (slot * 2 + k) * p.cap;
+        side[k].sig = p.sig + (slot * 2 + k) * p.cap;
+        side[k].lvl = p.lvl + (slot * 2 + k) * (p.cap + 2);
+        side[k].base = p.hdr[slot * kHdrWords + kHdrBase0 + k];
+    }
+    u32 *contact = p.contact + slot * 2 * p.cap;
+    WorkRegs wk;
+    u64 tot_e_lvl = 0, tot_p_walk = 0;
+    if (tid == 0)
+        for (int c = 0; c < kWorkCounters; ++c)
+            sh.wk[c] = 0;
+    u32 last_base[2] = {0, 0}, last_cnt[2] = {0, 0}, last_depth[2] = {0, 0};
+
+    for (;;) {
+        if (tid == 0)
+            sh.ticket = atomicAdd(p.ticket, 1ull);
+        __syncthreads();
+        const u64 ticket = sh.ticket;
+        __syncthreads();
+        if (ticket >= ticket_count)
+            break;
+        const u64 local = p.relist ? p.relist[ticket] : ticket;
+        const u64 index = p.first + local;
+
+        // ---- label-space housekeeping: a side's labels must stay below the claim range ----
+        for (int k = 0; k < 2; ++k) {
+            const u64 limit = static_cast<u64>(kClaimTop) - kMaxBlockThreads - 2;
+            if (static_cast<u64>(side[k].base) + p.cap + 1 >= limit) {
+                for (u64 i = tid; i < n; i += BLOCK)
+                    st_cg(side[k].lab + i, 0u);
+                side[k].base = 1;
+                __syncthreads();
+            }
+        }
+
+        // ---- (s, t): sample_pair (sampler.cpp:45-52) ----
+        SampleStream rng(p.seed, p.tag, index);
+        u32 s, t;
+        if (p.pairs) {
+            s = p.pairs[2 * local];
+            t = p.pairs[2 * local + 1];
+        } else {
+            const u64 a = rng.next_below(n);
+            u64 b = rng.next_below(n - 1);
+            if (b >= a)
+                ++b;
+            s = static_cast<u32>(a);
+            t = static_cast<u32>(b);
+        }
+
+        // ---- init both sides (sampler.cpp:65-76) ----
+        for (int k = 0; k < 2; ++k) {
+            const u32 root = k == 0 ? s : t;
+            side[k].cnt = 1;
+            side[k].fb = 0;
+            side[k].depth = 0;
+            side[k].pending = __ldg(p.offsets + root + 1) - __ldg(p.offsets + root);
+            if (tid == 0) {
+                st_cg(side[k].lab + root, side[k].base);
+                st_cg(side[k].list, root);
+                st_cg(side[k].sig, static_cast<u64>(1));
+                st_cg(side[k].lvl, 0u);
+            }
+        }
+        if (tid == 0) {
+            for (int c = 0; c < kWorkCounters; ++c)
+                sh.ws[c] = 0;
+            sh.ws[kW_V_set] = 2;
+            sh.ws[kW_samples] = 1;
+        }
+        wk.e_lvl = 0;
+        wk.p_walk = 0;
+        __syncthreads();
+
+        u32 *path_out = p.paths ? p.paths + local * p.path_stride : nullptr;
+        SampleRecordDev rec;
+        rec.s = s;
+        rec.t = t;
+        rec.dist = 0xffffffffu;
+        rec.meet = 0xffffffffu;
+        rec.meet_count = 0;
+        rec.path_len = 0;
+        rec.flags = 0;
+        rec.weight_lo = rec.weight_hi = 0;
+
+        // ---- level loop (sampler.cpp:81-116) ----
+        bool found = false, aborted = false;
+        int e = 0;
+        u32 contact_n = 0;
+        while (!found) {
+            if (side[0].cnt == side[0].fb || side[1].cnt == side[1].fb)
+                break; // a frontier ran empty: t unreachable, empty sample (sampler.cpp:82-83)
+            e = side[0].pending <= side[1].pending ? 0 : 1; // tie -> forward (sampler.cpp:84)
+            if (!expand_level<BLOCK>(p, side[e], side[1 - e], contact, contact_n, sh, wk)) {
+                aborted = true;
+                break;
+            }
+            found = sh.min_contact != 0xffffffffu;
+            __syncthreads();
+        }
+
+        if (aborted) {
+            rec.flags |= 1u;
+            if (tid == 0) {
+                const u32 k = atomicAdd(p.overflow_count, 1u);
+                if (k < p.overflow_cap)
+                    p.overflow_list[k] = static_cast<u32>(local);
+                atomicAdd(p.overflow_total, 1ull);
+            }
+        } else if (found) {
+            SideRegs &ex = side[e];
+            SideRegs &ot = side[1 - e];
+            // best = min other.dist over contacts = level of the smallest other-side idx
+            const u32 min_idx = sh.min_contact;
+            u32 best = ot.depth;
+            while (ld_cg(ot.lvl + best) > min_idx)
+                --best;
+            const u32 olo = ld_cg(ot.lvl + best);
+            const u32 ohi = best == ot.depth ? ot.cnt : ld_cg(ot.lvl + best + 1);
+            rec.dist = ex.depth + best;
+
+            // total weight over the meet set (sampler.cpp:121-123), saturating at 2^128-1
+            u128 wsum = 0;
+            u32 mcount = 0;
+            for (u32 c = tid; c < contact_n; c += BLOCK) {
+                const u32 oi = ld_cg(contact + 2 * c + 1);
+                if (oi - olo < ohi - olo) {
+                    const u32 ei = ld_cg(contact + 2 * c);
+                    wsum += static_cast<u128>(ld_cg(ex.sig + ei)) * ld_cg(ot.sig + oi);
+                    // a single thread's partial sum can itself wrap only beyond 2^64 terms
+                    ++mcount;
+                }
+            }
+            u64 wlo, whi, wov;
+            block_sum_u128<BLOCK>(wsum, wlo, whi, wov, sh.red64);
+            const u32 meet_count = static_cast<u32>(block_sum_u64<BLOCK>(mcount, sh.red64));
+            __syncthreads();
+            const u128 total_weight = wov ? ~static_cast<u128>(0) : ((static_cast<u128>(whi) << 64) | wlo);
+            rec.weight_lo = static_cast<u64>(total_weight);
+            rec.weight_hi = static_cast<u64>(total_weight >> 64);
+            rec.meet_count = meet_count;
+            if (tid == 0)
+                sh.ws[kW_M] += meet_count;
+
+            // pick and ordered prefix search (sampler.cpp:124-133).  pick < total_weight <=
+            // sum of the weights, so a hit always exists; the reference's fall-through
+            // default (last meet vertex, sampler.cpp:125) is kept for completeness.
+            const u128 pick = uniform_below_u128(rng, total_weight);
+            u32 meet_e = 0xffffffffu;
+            {
+                u128 running = 0;
+                bool running_ovf = false;
+                for (u32 c0 = 0; c0 < contact_n && meet_e == 0xffffffffu; c0 += BLOCK) {
+                    const u32 c = c0 + tid;
+                    u128 wv = 0;
+                    u32 ei = 0;
+                    if (c < contact_n) {
+                        const u32 oi = ld_cg(contact + 2 * c + 1);
+                        if (oi - olo < ohi - olo) {
+                            ei = ld_cg(contact + 2 * c);
+                            wv = static_cast<u128>(ld_cg(ex.sig + ei)) * ld_cg(ot.sig + oi);
+                        }
+                    }
+                    const u32 f = block_first_exceeding<BLOCK>(wv, running, running_ovf, pick, sh);
+                    if (f != BLOCK) {
+                        if (tid == f)
+                            sh.bcast[0] = ei;
+                        __syncthreads();
+                        meet_e = sh.bcast[0];
+                        __syncthreads();
+                    }
+                }
+                if (meet_e == 0xffffffffu) {
+                    for (u32 c = contact_n; c-- > 0;) {
+                        const u32 oi = ld_cg(contact + 2 * c + 1);
+                        if (oi - olo < ohi - olo) {
+                            meet_e = ld_cg(contact + 2 * c);
+                            break;
+                        }
+                    }
+                }
+            }
+            const u32 meet = ld_cg(ex.list + meet_e);
+            rec.meet = meet;
+
+            // walks (sampler.cpp:157-163): path order s .. meet .. t
+            const u32 d_ex = ex.depth, d_ot = best;
+            const u32 dist_f = e == 0 ? d_ex : d_ot; // depth of meet on the forward side
+            const u32 dist_b = e == 0 ? d_ot : d_ex;
+            u32 emitted = 0;
+            // forward side: vertices at forward depth d sit at internal position d-1
+            walk_side<BLOCK>(p, side[0], meet, dist_f, rng, path_out, static_cast<long long>(dist_f) - 2, -1,
+                             emitted, sh, wk);
+            if (meet != s && meet != t) {
+                if (tid == 0) {
+                    atomicAdd(p.frame + 1 + meet, 1u);
+                    if (path_out)
+                        path_out[dist_f - 1] = meet;
+                }
+                emitted += 1;
+            }
+            walk_side<BLOCK>(p, side[1], meet, dist_b, rng, path_out, static_cast<long long>(dist_f), +1,
+                             emitted, sh, wk);
+            rec.path_len = emitted;
+            if (tid == 0)
+                sh.ws[kW_L] += emitted;
+        }
+
+        // ---- apply_sample: tau += 1 (sampler.hpp:75); retire the sample's labels ----
+        rec.draws = rng.draws();
+        if (!aborted) {
+            tot_e_lvl += wk.e_lvl;
+            tot_p_walk += wk.p_walk;
+            if (tid == 0) {
+                atomicAdd(p.frame, 1u);
+                for (int c = 0; c < kWorkCounters; ++c)
+                    sh.wk[c] += sh.ws[c];
+            }
+        }
+        if (p.records && tid == 0)
+            p.records[local] = rec;
+        for (int k = 0; k < 2; ++k) {
+            last_base[k] = side[k].base;
+            last_cnt[k] = side[k].cnt;
+            last_depth[k] = side[k].depth;
+            side[k].base += side[k].cnt;
+        }
+        __syncthreads();
+    }
+
+    // ---- persist slot header and work counters ----
+    if (tid == 0) {
+        u32 *h = p.hdr + slot * kHdrWords;
+        h[kHdrBase0] = side[0].base;
+        h[kHdrBase1] = side[1].base;
+        h[kHdrLastBase0] = last_base[0];
+        h[kHdrLastBase1] = last_base[1];
+        h[kHdrLastCnt0] = last_cnt[0];
+        h[kHdrLastCnt1] = last_cnt[1];
+        h[kHdrLastDepth0] = last_depth[0];
+        h[kHdrLastDepth1] = last_depth[1];
+    }
+    const u64 e_lvl = block_sum_u64<BLOCK>(tot_e_lvl, sh.red64);
+    __syncthreads();
+    const u64 p_walk = block_sum_u64<BLOCK>(tot_p_walk, sh.red64);
+    if (tid == 0 && sh.wk[kW_samples]) {
+        sh.wk[kW_E_lvl] = e_lvl;
+        sh.wk[kW_P_walk] = p_walk;
+        for (int c = 0; c < kWorkCounters; ++c)
+            atomicAdd(p.work + c, static_cast<unsigned long long>(sh.wk[c]));
+    }
+}
+
+} // namespace ebc

@@ -1,0 +1,161 @@
+"""GPU parity: the CUDA sampling path (through the C ABI) against the CPU oracle, bit-exact.
+
+Integer/index work => every comparison is exact equality.
+"""
+import numpy as np
+import pytest
+
+import paper_1910_11039_b200 as ebc
+from helpers import (complete_bipartite_chain, cycle_graph, grid_graph, largest_component, path_graph,
+                     random_graph, star_graph)
+from oracle import Oracle
+
+pytestmark = pytest.mark.gpu
+
+SEED = 7
+
+
+def small_graphs():
+    return {
+        "er200": random_graph(200, 400, 1),
+        "er300dense": random_graph(300, 2000, 2),
+        "grid12": grid_graph(12, 12, 0.05, 3),
+        "layers40": complete_bipartite_chain([1] + [40] * 13 + [1]),   # sigma ~ 40^12: 128-bit weights
+        "layers70": complete_bipartite_chain([3] + [70] * 12 + [2]),   # sigma saturates at 2^64-1
+        "path4": path_graph(4),
+        "cycle4": cycle_graph(4),
+        "star5": star_graph(5),
+        "disconnected": random_graph(50, 30, 5),
+        "two_vertices": path_graph(2),
+    }
+
+
+def check_samples(g_csr, count, cfg, seed=SEED, first=0, pairs=None, stride=64):
+    off, tg = g_csr
+    g = ebc.Graph.from_csr(off, tg)
+    o = Oracle(off, tg)
+    s = ebc.Sampler(g, cfg)
+    rec, paths = s.sample_debug(seed, first, count, pairs=pairs, path_stride=stride)
+    frame = np.zeros(g.num_vertices + 1, dtype=np.uint64)
+    for i in range(count):
+        want = o.sample(seed, first + i, pair=None if pairs is None else tuple(int(x) for x in pairs[i]))
+        got = rec[i]
+        assert (int(got["s"]), int(got["t"])) == (want["s"], want["t"]), i
+        assert int(got["dist"]) == want["dist"], (i, got, want)
+        assert int(got["meet"]) == want["meet"], (i, got, want)
+        assert int(got["draws"]) == want["draws"], (i, got, want)
+        assert int(got["path_len"]) == len(want["path"]), (i, got, want)
+        if want["dist"] != 0xFFFFFFFF:
+            assert int(got["meet_count"]) == len(o.last_meet_set()), i
+        if len(want["path"]) <= stride:
+            assert np.array_equal(paths[i, :len(want["path"])], want["path"]), (i, paths[i], want["path"])
+        frame[0] += 1
+        np.add.at(frame, want["path"].astype(np.int64) + 1, 1)
+    assert np.array_equal(s.read_frame(0), frame)
+    return s, o
+
+
+@pytest.mark.parametrize("name", list(small_graphs().keys()))
+@pytest.mark.parametrize("block", [32, 128])
+def test_small_graph_samples(name, block):
+    csr = small_graphs()[name]
+    cfg = ebc.RunConfig(block_threads=block, slots=8)
+    check_samples(csr, 600, cfg)
+
+
+@pytest.mark.parametrize("block", [32, 64, 256])
+def test_search_state_matches_oracle(block):
+    """dist / sigma of both sides after single samples (slots == 1 so the state stays inspectable)."""
+    for name in ("er300dense", "layers40", "layers70", "grid12"):
+        off, tg = small_graphs()[name]
+        g = ebc.Graph.from_csr(off, tg)
+        o = Oracle(off, tg)
+        s = ebc.Sampler(g, ebc.RunConfig(block_threads=block, slots=1))
+        for i in range(25):
+            rec, _ = s.sample_debug(SEED, i, 1)
+            want = o.sample(SEED, i)
+            assert int(rec[0]["dist"]) == want["dist"]
+            for side in (0, 1):
+                d, sg = s.last_state(side)
+                od, osg = o.last_state(side)
+                assert np.array_equal(d, od), (name, i, side)
+                assert np.array_equal(sg, osg), (name, i, side)
+
+
+def test_explicit_pairs_and_weights():
+    off, tg = small_graphs()["layers70"]
+    n = len(off) - 1
+    pairs = np.array([[0, n - 1], [1, n - 2], [n - 1, 0], [5, 6], [0, 3]], dtype=np.uint32)
+    s, o = check_samples((off, tg), len(pairs), ebc.RunConfig(block_threads=64, slots=2), pairs=pairs)
+    rec, _ = s.sample_debug(SEED, 0, 1, pairs=pairs[:1])
+    # 3 * 70^12 * 2 shortest paths: the saturating 128-bit total must agree with Python integers
+    o.sample(SEED, 0, pair=(0, n - 1))
+    fs = o.last_state(0)[1]
+    bs = o.last_state(1)[1]
+    total = sum(int(fs[v]) * int(bs[v]) for v in o.last_meet_set())
+    total = min(total, 2 ** 128 - 1)
+    assert (int(rec[0]["weight_hi"]) << 64) | int(rec[0]["weight_lo"]) == total
+
+
+def test_capacity_overflow_reruns_in_large_slots():
+    """A slot capacity far below what samples settle forces the re-run path; results must not change."""
+    off, tg = small_graphs()["er300dense"]
+    cfg = ebc.RunConfig(block_threads=32, slots=4, slot_capacity=8)
+    s, _ = check_samples((off, tg), 400, cfg)
+    rec, _ = s.sample_debug(SEED, 0, 400)
+    assert (rec["flags"] & 1).sum() == 0  # records come from the completed (re-run) sample
+    assert s.work()["samples"] == 800
+
+
+def test_label_space_wraparound():
+    """Many samples in ONE slot of a tiny graph, enough to cross no label reset, plus a forced one."""
+    off, tg = small_graphs()["grid12"]
+    g = ebc.Graph.from_csr(off, tg)
+    o = Oracle(off, tg)
+    s = ebc.Sampler(g, ebc.RunConfig(block_threads=32, slots=1))
+    s.sample(SEED, 0, 20000)
+    assert np.array_equal(s.read_frame(0), o.accumulate(SEED, 0, 20000))
+
+
+def test_frames_accumulate_and_epochs_fold():
+    off, tg = random_graph(2000, 9000, 11)
+    (off, tg), _ = largest_component(off, tg)
+    g = ebc.Graph.from_csr(off, tg)
+    o = Oracle(off, tg)
+    s = ebc.Sampler(g, ebc.RunConfig())
+    n = g.num_vertices
+    dl, du = ebc.calibrate(np.zeros(n + 1, dtype=np.uint64), n, 0.1)
+    s.set_stopping(0.005, 10 ** 9, dl, du)  # Hoeffding width at tau=12000 is ~0.021: never stops here
+    S = np.zeros(n + 1, dtype=np.uint64)
+    for e in range(4):
+        s.sample(SEED, e * 3000, 3000, frame=e & 1)
+        assert not s.fold_and_check(e & 1)
+        o.accumulate(SEED, e * 3000, 3000, frame=S)
+        assert np.array_equal(s.read_state(), S)
+        assert s.read_frame(e & 1).sum() == 0
+    w = s.work()
+    ow = o.work()
+    for i, k in enumerate(ebc.WORK_NAMES[:11]):
+        assert w[k] == int(ow[i]), k
+    assert w["samples"] == 12000
+
+
+def test_config1_er_counters_bit_exact():
+    g = ebc.gen_erdos_renyi(10000, 50000, 1).largest_connected_component()
+    o = Oracle(g.offsets, g.targets)
+    s = ebc.Sampler(g, ebc.RunConfig())
+    s.sample(SEED, 0, 8000)
+    assert np.array_equal(s.read_frame(0), o.accumulate(SEED, 0, 8000))
+
+
+def test_rmat14_counters_bit_exact():
+    g = ebc.gen_rmat(14, 16, seed=2).largest_connected_component()
+    o = Oracle(g.offsets, g.targets)
+    s = ebc.Sampler(g, ebc.RunConfig())
+    s.sample(SEED, 100, 4000)
+    assert np.array_equal(s.read_frame(0), o.accumulate(SEED, 100, 4000))
+    rec, paths = s.sample_debug(SEED, 0, 200, frame=1, path_stride=16)
+    for i in range(200):
+        want = o.sample(SEED, i)
+        assert int(rec[i]["meet"]) == want["meet"] and int(rec[i]["dist"]) == want["dist"]
+        assert np.array_equal(paths[i, :len(want["path"])], want["path"])
