@@ -145,6 +145,7 @@ typedef struct ebc_run_config {
     uint32_t slots;            /* concurrent samples (resident CTAs): 0 = auto             */
     uint64_t slot_capacity;    /* settled vertices per side per slot: 0 = auto             */
     int overlap;               /* 1 = sample epoch e+1 while epoch e is reduced/checked    */
+    uint32_t items_per_thread; /* adjacency slots per thread per tile (1|2|4): 0 = auto    */
 } ebc_run_config;
 
 EBC_API void ebc_run_config_default(ebc_run_config *cfg);

@@ -227,13 +227,14 @@ class RunConfig:
     slots: int = 0
     slot_capacity: int = 0
     overlap: bool = True
+    items_per_thread: int = 0
 
     def to_c(self) -> _CRunConfig:
         c = _CRunConfig()
         _capi.load().ebc_run_config_default(C.byref(c))
         for f in ("eps", "delta", "seed", "bound", "allocator", "omega_override", "calib_samples",
                   "diameter_sweeps", "vertex_diameter_override", "epoch_samples", "max_epochs", "device",
-                  "rank", "world_size", "block_threads", "slots", "slot_capacity"):
+                  "rank", "world_size", "block_threads", "slots", "slot_capacity", "items_per_thread"):
             setattr(c, f, getattr(self, f))
         c.overlap = int(self.overlap)
         if self.allreduce is not None:
@@ -385,7 +386,8 @@ class Sampler:
         w = np.zeros(6, dtype=np.uint64)
         _check(_capi.load().ebc_sampler_info(self._h, _p(w, _capi.u64p)))
         return dict(slots=int(w[0]), block_threads=int(w[1]), slot_capacity=int(w[2]),
-                    device_bytes=int(w[3]), sm_count=int(w[4]), launches=int(w[5]))
+                    device_bytes=int(w[3]), sm_count=int(w[4]), launches=int(w[5]) & ((1 << 56) - 1),
+                    items_per_thread=int(w[5]) >> 56)
 
     def stream(self) -> int:
         p = C.c_void_p()

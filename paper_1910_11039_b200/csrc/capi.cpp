@@ -73,6 +73,7 @@ SamplerOptions sampler_options(const ebc_run_config *cfg) {
         o.block_threads = cfg->block_threads;
         o.slots = cfg->slots;
         o.slot_capacity = cfg->slot_capacity;
+        o.items_per_thread = cfg->items_per_thread;
     }
     return o;
 }
@@ -236,7 +237,7 @@ ebc_status ebc_diameter_upper_bound(const ebc_graph *g, int sweeps, uint64_t see
         need(g, "ebc_diameter_upper_bound: null graph");
         need(out, "ebc_diameter_upper_bound: null out");
         // GPU BFS sweeps; the host only drives the restart logic.
-        CudaSampler s(g->g, SamplerOptions{-1, 32, 1, 2});
+        CudaSampler s(g->g, SamplerOptions{-1, 32, 1, 2, 1});
         DiameterBounds b = diameter_upper_bound(g->g, sweeps, seed,
                                                 [&](std::uint32_t v) { return s.bfs(v, nullptr); });
         out[0] = b.upper;

@@ -186,32 +186,34 @@ __global__ void flush_kernel(u32 *buf, u64 count, u32 salt) {
         buf[i] = static_cast<u32>(i) ^ salt;
 }
 
-template <int BLOCK> void launch_sample(const SamplerParams &p, u32 grid, cudaStream_t stream) {
-    sample_kernel<BLOCK><<<grid, BLOCK, 0, stream>>>(p);
-}
+// (BLOCK, ITEMS) instantiations of the sampling kernel.
+#define EBC_FOR_EACH_SHAPE(X) \
+    X(32, 1) X(32, 2) X(32, 4) X(64, 1) X(64, 2) X(64, 4) X(128, 1) X(128, 2) X(128, 4) X(256, 1) X(256, 2) \
+    X(256, 4) X(512, 1) X(512, 2) X(512, 4)
 
-void launch_sample_dispatch(u32 block, const SamplerParams &p, u32 grid, cudaStream_t stream) {
-    switch (block) {
-    case 32: launch_sample<32>(p, grid, stream); break;
-    case 64: launch_sample<64>(p, grid, stream); break;
-    case 128: launch_sample<128>(p, grid, stream); break;
-    case 256: launch_sample<256>(p, grid, stream); break;
-    case 512: launch_sample<512>(p, grid, stream); break;
-    default: throw ConfigError("block_threads must be one of 32, 64, 128, 256, 512");
+void launch_sample_dispatch(u32 block, u32 items, const SamplerParams &p, u32 grid, cudaStream_t stream) {
+    bool done = false;
+#define EBC_LAUNCH(B, I)                                       \
+    if (!done && block == B && items == I) {                   \
+        sample_kernel<B, I><<<grid, B, 0, stream>>>(p);        \
+        done = true;                                           \
     }
+    EBC_FOR_EACH_SHAPE(EBC_LAUNCH)
+#undef EBC_LAUNCH
+    if (!done)
+        throw ConfigError("block_threads must be one of 32, 64, 128, 256, 512 and items_per_thread one of 1, 2, 4");
     EBC_CUDA(cudaGetLastError());
 }
 
-int occupancy_for(u32 block) {
-    int per_sm = 0;
-    switch (block) {
-    case 32: EBC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sample_kernel<32>, 32, 0)); break;
-    case 64: EBC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sample_kernel<64>, 64, 0)); break;
-    case 128: EBC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sample_kernel<128>, 128, 0)); break;
-    case 256: EBC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sample_kernel<256>, 256, 0)); break;
-    case 512: EBC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sample_kernel<512>, 512, 0)); break;
-    default: throw ConfigError("block_threads must be one of 32, 64, 128, 256, 512");
-    }
+int occupancy_for(u32 block, u32 items) {
+    int per_sm = -1;
+#define EBC_OCC(B, I)                                                                                   \
+    if (per_sm < 0 && block == B && items == I)                                                         \
+        EBC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sample_kernel<B, I>, B, 0));
+    EBC_FOR_EACH_SHAPE(EBC_OCC)
+#undef EBC_OCC
+    if (per_sm < 0)
+        throw ConfigError("block_threads must be one of 32, 64, 128, 256, 512 and items_per_thread one of 1, 2, 4");
     return per_sm;
 }
 
@@ -261,6 +263,7 @@ struct CudaSampler::Impl {
     u64 *d_offsets = nullptr;
     u32 *d_targets = nullptr;
     u32 block = 128;
+    u32 items = 4;
     SlotArrays small, big;
     u32 *d_frame[2] = {nullptr, nullptr};
     u64 *d_S = nullptr;
@@ -324,7 +327,7 @@ struct CudaSampler::Impl {
         p.overflow_count = d_overflow_count;
         p.overflow_total = d_ovf_total;
         const u32 grid = static_cast<u32>(std::min<u64>(small.slots, count));
-        launch_sample_dispatch(block, p, grid, s_sample);
+        launch_sample_dispatch(block, items, p, grid, s_sample);
         ++launches;
         if (small.cap < n) { // capacity overflow is impossible when cap == n
             SamplerParams q = base_params(big);
@@ -342,7 +345,7 @@ struct CudaSampler::Impl {
             q.overflow_total = d_ovf_total + 1;
             q.relist = d_overflow_list;
             q.count_ptr = d_overflow_count;
-            launch_sample_dispatch(block, q, static_cast<u32>(big.slots), s_sample);
+            launch_sample_dispatch(block, items, q, static_cast<u32>(big.slots), s_sample);
             ++launches;
         }
     }
@@ -398,7 +401,8 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
 
     // ---- launch shape ----
     m.block = opt.block_threads ? opt.block_threads : 128;
-    const int per_sm = occupancy_for(m.block);
+    m.items = opt.items_per_thread ? opt.items_per_thread : 4;
+    const int per_sm = occupancy_for(m.block, m.items);
     if (per_sm < 1)
         throw CudaError("sampling kernel does not fit on an SM");
     u64 cap = opt.slot_capacity ? std::min<u64>(opt.slot_capacity, g.n)
@@ -694,7 +698,7 @@ void CudaSampler::info(std::uint64_t *out) {
     out[2] = m.small.cap;
     out[3] = m.small.bytes + m.big.bytes + m.graph_bytes + (m.n + 1) * (4 * 2 + 8 + 8 + 16);
     out[4] = static_cast<std::uint64_t>(m.sm_count);
-    out[5] = m.launches;
+    out[5] = m.launches | (static_cast<std::uint64_t>(m.items) << 56);
 }
 
 void *CudaSampler::stream_handle() { return impl_->s_sample; }

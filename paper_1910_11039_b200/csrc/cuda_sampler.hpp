@@ -18,6 +18,7 @@ struct SamplerOptions {
     std::uint32_t block_threads = 0; // 0 = auto
     std::uint32_t slots = 0;         // 0 = auto
     std::uint64_t slot_capacity = 0; // 0 = auto
+    std::uint32_t items_per_thread = 0; // 0 = auto
 };
 
 struct SampleRecordHost { // == ebc_sample_record

@@ -36,6 +36,7 @@ enum WorkCounter : int {
 // settled count; dist is implied by idx (levels occupy contiguous idx ranges).
 constexpr u32 kClaimTop = 0xffffffffu;     // transient claim values: kClaimTop - slot_in_tile
 constexpr u32 kMaxBlockThreads = 1024;
+constexpr u32 kMaxTileSlots = 4096;        // BLOCK * ITEMS never exceeds this
 constexpr u32 kHdrWords = 16;              // per-slot header (u32)
 // header word indices
 enum : int { kHdrBase0 = 0, kHdrBase1 = 1, kHdrLastBase0 = 2, kHdrLastBase1 = 3, kHdrLastCnt0 = 4,

@@ -14,12 +14,15 @@
 // prefix walk over the new frontier in DISCOVERY order (sampler.cpp:111-113,
 // 126-133), and discovery order is (position of first parent in the frontier,
 // index in that parent's sorted row).  Here a level's adjacency slots are
-// enumerated in exactly that order and processed in tiles of BLOCK slots; in a
-// tile every undiscovered target is claimed with atomicMax(label, TOP - slot),
-// so the LOWEST slot wins, and winners are ranked by an ordered block scan.
-// Earlier tiles are final before later tiles start, hence idx == the
-// reference's position in `next` (sampler.cpp:92-95).  Sigma sums, pending
-// edge counts and counters are order independent.
+// enumerated in exactly that order and processed in tiles of BLOCK*ITEMS slots.
+//   * A tile that lies inside ONE row cannot contain duplicate targets (rows
+//     are strictly ascending), so every unvisited target is a winner at once.
+//   * In a tile spanning several rows every unvisited target is claimed with
+//     atomicMax(label, TOP - slot): the LOWEST slot wins.
+// Winners are ranked by an ordered ballot/popc block scan and receive
+// idx = cnt + rank.  Earlier tiles are final before later tiles start, hence
+// idx == the reference's position in `next` (sampler.cpp:92-95).  Sigma sums,
+// pending edge counts and counters are order independent.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -55,9 +58,7 @@ __device__ __forceinline__ void sat_atomic_add(u64 *p, u64 add) {
 
 // uniform_below_u128 (sampler.cpp:21-30).  Executed redundantly by every thread
 // of the CTA (the stream state is uniform), so no broadcast is needed.
-__device__ __forceinline__ u128 uniform_below_u128(SampleStream &rng, u128 bound) {
-    if (static_cast<u64>(bound >> 64) == 0)
-        return rng.next_below(static_cast<u64>(bound));
+__device__ __noinline__ u128 uniform_below_wide(SampleStream &rng, u128 bound) {
     const u128 all = ~static_cast<u128>(0);
     const u128 reject_from = all - (all % bound);
     for (;;) {
@@ -68,50 +69,61 @@ __device__ __forceinline__ u128 uniform_below_u128(SampleStream &rng, u128 bound
             return r % bound;
     }
 }
+__device__ __forceinline__ u128 uniform_below_u128(SampleStream &rng, u128 bound) {
+    if (static_cast<u64>(bound >> 64) == 0)
+        return rng.next_below(static_cast<u64>(bound));
+    return uniform_below_wide(rng, bound);
+}
 
-template <int BLOCK> struct BlockShared {
+constexpr int kPredCache = 32;
+
+template <int BLOCK, int ITEMS> struct BlockShared {
     static constexpr int WARPS = BLOCK / 32;
     u64 c_beg[BLOCK];      // row start of each frontier-chunk vertex
     u64 c_scan[BLOCK + 1]; // exclusive prefix of the chunk's degrees
     u64 c_sig[BLOCK];      // sigma of each chunk vertex
     u64 red64[WARPS * 3];  // block reductions
-    u32 warp_cnt[WARPS];
-    u32 warp_cnt2[WARPS];
+    u32 warp_cnt[ITEMS * WARPS];
+    u32 warp_cnt2[ITEMS * WARPS];
     unsigned long long ticket;
     u32 min_contact;       // min other-side idx over contact vertices of this level
     u32 found_lane;        // ordered-search result
-    u64 found_aux;
     u32 pred_cnt;
-    u32 pred_pos[32];
-    u64 pred_sig[32];
-    u32 pred_vtx[32];
+    u32 pred_pos[kPredCache];
+    u64 pred_sig[kPredCache];
+    u32 pred_vtx[kPredCache];
     u32 bcast[4];
     u64 ws[kWorkCounters]; // work counters of the sample in flight (thread 0)
     u64 wk[kWorkCounters]; // committed work counters of this CTA
 };
 
-// Rank of this thread among the threads with flag set (thread order) and the total.
-// Contains one __syncthreads; warp_cnt must not be reused before the next barrier.
-template <int BLOCK> __device__ __forceinline__ u32 block_rank(bool flag, u32 &total, u32 *warp_cnt) {
-    const u32 ballot = __ballot_sync(0xffffffffu, flag);
-    const u32 in_warp = __popc(ballot & lanemask_lt());
-    if (BLOCK == 32) {
-        total = __popc(ballot);
-        return in_warp;
-    }
+// Ordered ranks for ITEMS flags per thread, slot order = (item, warp, lane).
+// rank[k] = number of set flags before slot (k, tid); returns the total.
+// One __syncthreads; `cnt` (ITEMS*WARPS words) must not be reused before the next barrier.
+template <int BLOCK, int ITEMS>
+__device__ __forceinline__ u32 block_ranks(const bool (&flag)[ITEMS], u32 (&rank)[ITEMS], u32 *cnt) {
+    constexpr int WARPS = BLOCK / 32;
     const u32 warp = threadIdx.x >> 5;
-    if (lane_id() == 0)
-        warp_cnt[warp] = __popc(ballot);
-    __syncthreads();
-    u32 before = 0, all = 0;
+    u32 in_warp[ITEMS];
 #pragma unroll
-    for (int w = 0; w < BLOCK / 32; ++w) {
-        const u32 c = warp_cnt[w];
-        all += c;
-        before += (w < warp) ? c : 0;
+    for (int k = 0; k < ITEMS; ++k) {
+        const u32 ballot = __ballot_sync(0xffffffffu, flag[k]);
+        in_warp[k] = __popc(ballot & lanemask_lt());
+        if (lane_id() == 0)
+            cnt[k * WARPS + warp] = __popc(ballot);
     }
-    total = all;
-    return before + in_warp;
+    __syncthreads();
+    u32 running = 0;
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+#pragma unroll
+        for (int w = 0; w < WARPS; ++w) {
+            if (static_cast<u32>(w) == warp)
+                rank[k] = running + in_warp[k];
+            running += cnt[k * WARPS + w];
+        }
+    }
+    return running;
 }
 
 template <int BLOCK> __device__ __forceinline__ u64 block_sum_u64(u64 v, u64 *red) {
@@ -133,7 +145,7 @@ template <int BLOCK> __device__ __forceinline__ u64 block_sum_u64(u64 v, u64 *re
 
 // 192-bit sum (lo, hi, carry-out count) of per-thread 128-bit values.
 template <int BLOCK>
-__device__ __forceinline__ void block_sum_u128(u128 v, u64 &lo, u64 &hi, u64 &ovf, u64 *red) {
+__device__ __noinline__ void block_sum_u128(u128 v, u64 &lo, u64 &hi, u64 &ovf, u64 *red) {
     u64 a = static_cast<u64>(v), b = static_cast<u64>(v >> 64), c = 0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -165,6 +177,7 @@ __device__ __forceinline__ void block_sum_u128(u128 v, u64 &lo, u64 &hi, u64 &ov
         }
         a = static_cast<u64>(s);
         b = static_cast<u64>(s >> 64);
+        __syncthreads();
     }
     lo = a;
     hi = b;
@@ -172,13 +185,12 @@ __device__ __forceinline__ void block_sum_u128(u128 v, u64 &lo, u64 &hi, u64 &ov
 }
 
 // Ordered search: first thread (in thread order) whose inclusive 128-bit prefix
-// of `w` exceeds `pick - running`.  Returns the thread index or BLOCK if none;
-// `running` is advanced by the block total when nothing is found.  Values that
-// overflow 128 bits compare as "exceeds".
+// of `w`, added to `running`, exceeds `pick`.  Returns the thread index or BLOCK
+// if none; `running` is advanced by the block total when nothing is found.
+// Values that overflow 128 bits compare as "exceeds".
 template <int BLOCK>
-__device__ __forceinline__ u32 block_first_exceeding(u128 w, u128 &running, bool &running_ovf, u128 pick,
-                                                     BlockShared<BLOCK> &sh) {
-    // inclusive warp scan
+__device__ __noinline__ u32 block_first_exceeding(u128 w, u128 &running, bool &running_ovf, u128 pick,
+                                                  u64 *red64, u32 *found_lane) {
     u64 a = static_cast<u64>(w), b = static_cast<u64>(w >> 64);
     u32 of = 0;
 #pragma unroll
@@ -200,52 +212,51 @@ __device__ __forceinline__ u32 block_first_exceeding(u128 w, u128 &running, bool
     if (BLOCK > 32) {
         __syncthreads();
         if (lane_id() == 31) {
-            sh.red64[warp * 3 + 0] = a;
-            sh.red64[warp * 3 + 1] = b;
-            sh.red64[warp * 3 + 2] = of;
+            red64[warp * 3 + 0] = a;
+            red64[warp * 3 + 1] = b;
+            red64[warp * 3 + 2] = of;
         }
         __syncthreads();
         u128 before = 0;
         bool before_of = false;
         for (u32 k = 0; k < warp; ++k) {
-            const u128 y = (static_cast<u128>(sh.red64[k * 3 + 1]) << 64) | sh.red64[k * 3 + 0];
+            const u128 y = (static_cast<u128>(red64[k * 3 + 1]) << 64) | red64[k * 3 + 0];
             const u128 t = before + y;
-            before_of = before_of || sh.red64[k * 3 + 2] != 0 || t < before;
+            before_of = before_of || red64[k * 3 + 2] != 0 || t < before;
             before = t;
         }
         const u128 t = incl + before;
         incl_of = incl_of || before_of || t < incl;
         incl = t;
     }
-    // add the running prefix of earlier chunks
     const u128 tot = incl + running;
     const bool tot_of = incl_of || running_ovf || tot < incl;
     const bool hit = (w != 0) && (tot_of || tot > pick);
-    // first hit in thread order
     const u32 ballot = __ballot_sync(0xffffffffu, hit);
     if (threadIdx.x == 0)
-        sh.found_lane = BLOCK;
+        *found_lane = BLOCK;
     __syncthreads();
     if (ballot != 0 && lane_id() == 0)
-        atomicMin(&sh.found_lane, (warp << 5) + (__ffs(ballot) - 1));
-    // block total -> new running (taken from the last thread)
+        atomicMin(found_lane, (warp << 5) + (__ffs(ballot) - 1));
     if (threadIdx.x == BLOCK - 1) {
-        sh.red64[0] = static_cast<u64>(tot);
-        sh.red64[1] = static_cast<u64>(tot >> 64);
-        sh.red64[2] = tot_of ? 1 : 0;
+        red64[0] = static_cast<u64>(tot);
+        red64[1] = static_cast<u64>(tot >> 64);
+        red64[2] = tot_of ? 1 : 0;
     }
     __syncthreads();
-    const u32 found = sh.found_lane;
+    const u32 found = *found_lane;
     if (found == BLOCK) {
-        running = (static_cast<u128>(sh.red64[1]) << 64) | sh.red64[0];
-        running_ovf = sh.red64[2] != 0;
+        running = (static_cast<u128>(red64[1]) << 64) | red64[0];
+        running_ovf = red64[2] != 0;
     }
     __syncthreads();
     return found;
 }
 
+// Labels of both sides of a vertex share one 8-byte word: lab[2v + side].  One
+// 32-byte sector therefore serves the visit test of the expanding side AND the
+// contact test against the other side.
 struct SideRegs {
-    u32 *lab;
     u32 *list;
     u64 *sig;
     u32 *lvl;
@@ -262,19 +273,23 @@ struct WorkRegs {
     u64 e_lvl = 0, p_walk = 0;
 };
 
-// Expands the frontier of side `ex` by one level (sampler.cpp:86-103) and
+__device__ __forceinline__ u32 half_of(u64 both, int side) { return static_cast<u32>(both >> (32 * side)); }
+
+// Expands the frontier of side `e` by one level (sampler.cpp:86-103) and
 // records contacts with the other side (sampler.cpp:105-108).  Returns false on
 // slot-capacity overflow (the sample is then re-run in a large slot).
 // contact_n returns the number of contact vertices appended to `contact`.
-template <int BLOCK>
-__device__ bool expand_level(const SamplerParams &p, SideRegs &ex, const SideRegs &ot, u32 *contact,
-                             u32 &contact_n, BlockShared<BLOCK> &sh, WorkRegs &wk) {
+// ex.pending is NOT updated here (see sum_frontier_degrees).
+template <int BLOCK, int ITEMS>
+__device__ bool expand_level(const SamplerParams &p, u32 *lab, int e, SideRegs &ex, const SideRegs &ot,
+                             u32 *contact, u32 &contact_n, BlockShared<BLOCK, ITEMS> &sh, WorkRegs &wk) {
+    constexpr int TILE = BLOCK * ITEMS;
     const u32 tid = threadIdx.x;
     const u32 fb = ex.fb, fe = ex.cnt;
     const u32 level_start = fe;
     const u32 next_depth = ex.depth + 1;
+    const u64 *lab64 = reinterpret_cast<const u64 *>(lab);
     u32 cnt = fe;
-    u64 pend = 0;
     contact_n = 0;
     if (tid == 0) {
         st_cg(ex.lvl + next_depth, level_start);
@@ -292,7 +307,6 @@ __device__ bool expand_level(const SamplerParams &p, SideRegs &ex, const SideReg
             deg = __ldg(p.offsets + u + 1) - beg;
             su = ld_cg(ex.sig + i);
         }
-        // inclusive warp scan of deg
         u64 inc = deg;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -300,7 +314,7 @@ __device__ bool expand_level(const SamplerParams &p, SideRegs &ex, const SideReg
             if (lane_id() >= static_cast<u32>(o))
                 inc += t;
         }
-        __syncthreads(); // previous chunk's tiles are done with c_* and red64
+        __syncthreads(); // previous chunk's tiles are done with c_*; their label stores are visible
         if (BLOCK > 32 && lane_id() == 31)
             sh.red64[tid >> 5] = inc;
         sh.c_beg[tid] = beg;
@@ -319,82 +333,194 @@ __device__ bool expand_level(const SamplerParams &p, SideRegs &ex, const SideReg
         if (tid == 0)
             sh.ws[kW_E_bfs] += T;
 
-        // ---- ordered tiles of BLOCK adjacency slots ----
-        for (u64 t0 = 0; t0 < T; t0 += BLOCK) {
-            const u64 j = t0 + tid;
-            const bool active = j < T;
-            u32 v = 0, idx = 0;
-            u64 sig_u = 0;
-            bool candidate = false, at_level = false;
-            if (active) {
-                // owner row: last r with c_scan[r] <= j
-                int lo = 0, hi = BLOCK;
-                while (hi - lo > 1) {
-                    const int mid = (lo + hi) >> 1;
-                    if (sh.c_scan[mid] <= j)
-                        lo = mid;
+        // ---- ordered tiles of TILE adjacency slots ----
+        int prev_row = -1;
+        int row_lo = 0; // owner of the tile's first slot; non-decreasing over the tiles of a chunk
+        for (u64 t0 = 0; t0 < T; t0 += TILE) {
+            const u64 t_last = (t0 + TILE < T ? t0 + TILE : T) - 1;
+            // owner rows of the first and last slot (uniform): last r with c_scan[r] <= j
+            while (sh.c_scan[row_lo + 1] <= t0)
+                ++row_lo;
+            int row_hi = row_lo;
+            {
+                int hi = BLOCK;
+                while (hi - row_hi > 1) {
+                    const int mid = (row_hi + hi) >> 1;
+                    if (sh.c_scan[mid] <= t_last)
+                        row_hi = mid;
                     else
                         hi = mid;
                 }
-                v = __ldg(p.targets + sh.c_beg[lo] + (j - sh.c_scan[lo]));
-                sig_u = sh.c_sig[lo];
-                const u32 rel = ld_cg(ex.lab + v) - ex.base;
-                if (rel < cnt) { // visited (sampler.cpp:92 false)
-                    idx = rel;
-                    at_level = rel >= level_start; // dist[v] == next_depth (sampler.cpp:97)
-                } else {
-                    candidate = true;
-                    atomicMax(ex.lab + v, kClaimTop - tid);
-                }
             }
-            __syncthreads(); // claims visible
-            bool win = false;
-            if (candidate)
-                win = ld_cg(ex.lab + v) == kClaimTop - tid;
-            u32 winners;
-            const u32 rank = block_rank<BLOCK>(win, winners, sh.warp_cnt);
-            const bool overflow = static_cast<u64>(cnt) + winners > p.cap;
-            bool is_contact = false;
-            u32 other_idx = 0;
-            if (win) {
+            u32 v[ITEMS], idx[ITEMS];
+            bool win[ITEMS], at_level[ITEMS], is_contact[ITEMS];
+            u32 other_idx[ITEMS];
+            u32 rank[ITEMS];
+            if (row_lo == row_hi) {
+                // ================= single-row tile: no duplicate targets possible =================
+                if (prev_row != row_lo && prev_row != -1)
+                    __syncthreads(); // label stores of the previous row's tiles must be visible
+                prev_row = row_lo;
+                const u32 *row = p.targets + (sh.c_beg[row_lo] - sh.c_scan[row_lo]);
+                const u64 sig_u = sh.c_sig[row_lo];
+                bool act[ITEMS];
+#pragma unroll
+                for (int k = 0; k < ITEMS; ++k) {
+                    const u64 j = t0 + static_cast<u64>(k) * BLOCK + tid;
+                    act[k] = j <= t_last;
+                    v[k] = act[k] ? __ldg(row + j) : 0u;
+                }
+                u64 both[ITEMS];
+#pragma unroll
+                for (int k = 0; k < ITEMS; ++k)
+                    both[k] = act[k] ? ld_cg(lab64 + v[k]) : 0ull;
+#pragma unroll
+                for (int k = 0; k < ITEMS; ++k) {
+                    const u32 rel = half_of(both[k], e) - ex.base;
+                    const bool visited = rel < cnt;
+                    win[k] = act[k] && !visited;
+                    at_level[k] = act[k] && visited && rel >= level_start; // dist[v] == next_depth (sampler.cpp:97)
+                    idx[k] = rel;
+                    other_idx[k] = half_of(both[k], 1 - e) - ot.base;
+                    is_contact[k] = win[k] && other_idx[k] < ot.cnt; // other.visited(v) (sampler.cpp:107)
+                }
+                const u32 winners = block_ranks<BLOCK, ITEMS>(win, rank, sh.warp_cnt);
+                if (static_cast<u64>(cnt) + winners > p.cap) {
+                    ex.cnt = cnt; // nothing of this tile was written; the caller retires labels < cnt
+                    return false;
+                }
+                bool any_contact_local = false;
+#pragma unroll
+                for (int k = 0; k < ITEMS; ++k) {
+                    if (win[k]) { // settle (sampler.cpp:93-95) and the discovering edge's sigma (sampler.cpp:98)
+                        idx[k] = cnt + rank[k];
+                        st_cg(lab + 2 * static_cast<u64>(v[k]) + e, ex.base + idx[k]);
+                        st_cg(ex.list + idx[k], v[k]);
+                        st_cg(ex.sig + idx[k], sig_u);
+                        if (is_contact[k]) {
+                            atomicMin(&sh.min_contact, other_idx[k]);
+                            any_contact_local = true;
+                        }
+                        wk.e_lvl += 1;
+                    } else if (at_level[k]) {
+                        sat_atomic_add(ex.sig + idx[k], sig_u);
+                        wk.e_lvl += 1;
+                    }
+                }
+                if (__syncthreads_or(any_contact_local ? 1 : 0)) {
+                    u32 crank[ITEMS];
+                    const u32 ctot = block_ranks<BLOCK, ITEMS>(is_contact, crank, sh.warp_cnt2);
+#pragma unroll
+                    for (int k = 0; k < ITEMS; ++k)
+                        if (is_contact[k]) {
+                            st_cg(contact + 2 * static_cast<u64>(contact_n + crank[k]), idx[k]);
+                            st_cg(contact + 2 * static_cast<u64>(contact_n + crank[k]) + 1, other_idx[k]);
+                        }
+                    contact_n += ctot;
+                }
+                cnt += winners;
+            } else {
+                // ================= tile spanning several rows: claim, lowest slot wins =================
+                if (prev_row != -1)
+                    __syncthreads();
+                prev_row = -2;
+                u64 sig_u[ITEMS];
+                bool candidate[ITEMS];
+#pragma unroll
+                for (int k = 0; k < ITEMS; ++k) {
+                    const u64 j = t0 + static_cast<u64>(k) * BLOCK + tid;
+                    const bool act = j <= t_last;
+                    v[k] = 0;
+                    idx[k] = 0;
+                    sig_u[k] = 0;
+                    candidate[k] = false;
+                    at_level[k] = false;
+                    other_idx[k] = 0xffffffffu;
+                    if (act) {
+                        int lo = row_lo, hi = row_hi + 1; // owner row: last r with c_scan[r] <= j
+                        while (hi - lo > 1) {
+                            const int mid = (lo + hi) >> 1;
+                            if (sh.c_scan[mid] <= j)
+                                lo = mid;
+                            else
+                                hi = mid;
+                        }
+                        v[k] = __ldg(p.targets + sh.c_beg[lo] + (j - sh.c_scan[lo]));
+                        sig_u[k] = sh.c_sig[lo];
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < ITEMS; ++k) {
+                    const u64 j = t0 + static_cast<u64>(k) * BLOCK + tid;
+                    if (j <= t_last) {
+                        const u64 both = ld_cg(lab64 + v[k]);
+                        const u32 rel = half_of(both, e) - ex.base;
+                        other_idx[k] = half_of(both, 1 - e) - ot.base;
+                        if (rel < cnt) {
+                            idx[k] = rel;
+                            at_level[k] = rel >= level_start;
+                        } else {
+                            candidate[k] = true;
+                            atomicMax(lab + 2 * static_cast<u64>(v[k]) + e, kClaimTop - (k * BLOCK + tid));
+                        }
+                    }
+                }
+                __syncthreads(); // claims visible
+#pragma unroll
+                for (int k = 0; k < ITEMS; ++k) {
+                    win[k] = candidate[k] &&
+                             ld_cg(lab + 2 * static_cast<u64>(v[k]) + e) == kClaimTop - (k * BLOCK + tid);
+                    is_contact[k] = win[k] && other_idx[k] < ot.cnt;
+                }
+                const u32 winners = block_ranks<BLOCK, ITEMS>(win, rank, sh.warp_cnt);
+                const bool overflow = static_cast<u64>(cnt) + winners > p.cap;
+                bool any_contact_local = false;
+#pragma unroll
+                for (int k = 0; k < ITEMS; ++k) {
+                    if (win[k]) {
+                        if (overflow) {
+                            st_cg(lab + 2 * static_cast<u64>(v[k]) + e, 0u); // undo the claim
+                        } else {
+                            idx[k] = cnt + rank[k];
+                            st_cg(lab + 2 * static_cast<u64>(v[k]) + e, ex.base + idx[k]);
+                            st_cg(ex.list + idx[k], v[k]);
+                            st_cg(ex.sig + idx[k], static_cast<u64>(0));
+                            if (is_contact[k]) {
+                                atomicMin(&sh.min_contact, other_idx[k]);
+                                any_contact_local = true;
+                            }
+                        }
+                    }
+                }
+                const int any_contact = __syncthreads_or(any_contact_local ? 1 : 0); // finals visible
                 if (overflow) {
-                    st_cg(ex.lab + v, 0u); // undo the claim; the sample is abandoned
-                } else {
-                    idx = cnt + rank; // settle (sampler.cpp:93-95, sampler.hpp:49-53)
-                    st_cg(ex.lab + v, ex.base + idx);
-                    st_cg(ex.list + idx, v);
-                    st_cg(ex.sig + idx, static_cast<u64>(0));
-                    pend += __ldg(p.offsets + v + 1) - __ldg(p.offsets + v);
-                    other_idx = ld_cg(ot.lab + v) - ot.base; // other.visited(v) (sampler.cpp:107)
-                    is_contact = other_idx < ot.cnt;
-                    if (is_contact)
-                        atomicMin(&sh.min_contact, other_idx);
+                    ex.cnt = cnt;
+                    return false;
                 }
-            }
-            const int any_contact = __syncthreads_or(is_contact ? 1 : 0); // finals visible
-            if (overflow) {
-                ex.cnt = cnt; // labels up to cnt were handed out; the caller retires them
-                return false;
-            }
-            if (candidate && !win)
-                idx = ld_cg(ex.lab + v) - ex.base;
-            if (active && (candidate || at_level)) {
-                sat_atomic_add(ex.sig + idx, sig_u); // sampler.cpp:97-98
-                wk.e_lvl += 1;
-            }
-            if (any_contact) { // ordered append of (idx, other idx)
-                u32 ctot;
-                const u32 crank = block_rank<BLOCK>(is_contact, ctot, sh.warp_cnt2);
-                if (is_contact) {
-                    st_cg(contact + 2 * (contact_n + crank), idx);
-                    st_cg(contact + 2 * (contact_n + crank) + 1, other_idx);
+#pragma unroll
+                for (int k = 0; k < ITEMS; ++k) {
+                    if (candidate[k] && !win[k])
+                        idx[k] = ld_cg(lab + 2 * static_cast<u64>(v[k]) + e) - ex.base;
+                    if (candidate[k] || at_level[k]) {
+                        sat_atomic_add(ex.sig + idx[k], sig_u[k]); // sampler.cpp:97-98
+                        wk.e_lvl += 1;
+                    }
                 }
-                contact_n += ctot;
+                if (any_contact) {
+                    u32 crank[ITEMS];
+                    const u32 ctot = block_ranks<BLOCK, ITEMS>(is_contact, crank, sh.warp_cnt2);
+#pragma unroll
+                    for (int k = 0; k < ITEMS; ++k)
+                        if (is_contact[k]) {
+                            st_cg(contact + 2 * static_cast<u64>(contact_n + crank[k]), idx[k]);
+                            st_cg(contact + 2 * static_cast<u64>(contact_n + crank[k]) + 1, other_idx[k]);
+                        }
+                    contact_n += ctot;
+                }
+                cnt += winners;
             }
-            cnt += winners;
         }
     }
-    pend = block_sum_u64<BLOCK>(pend, sh.red64);
     __syncthreads();
     if (tid == 0) {
         sh.ws[kW_V_set] += cnt - level_start;
@@ -402,98 +528,152 @@ __device__ bool expand_level(const SamplerParams &p, SideRegs &ex, const SideReg
     }
     ex.fb = level_start; // sampler.cpp:101-103
     ex.cnt = cnt;
-    ex.pending = pend;
     ex.depth = next_depth;
     return true;
 }
 
-// One sigma-weighted step chain from `u` (at depth d on `sd`) to the side's root
-// (sampler.cpp:135-155).  Emits every vertex strictly between into the frame
-// and, optionally, into path_out[pos], pos advancing by pos_step.
+// next_pending (sampler.cpp:95,102): the sum of the degrees of the new frontier.
+// Only needed when the search continues, so it is evaluated after the level,
+// not per settled vertex (the last level of a sample never needs it).
 template <int BLOCK>
-__device__ void walk_side(const SamplerParams &p, const SideRegs &sd, u32 u, u32 d, SampleStream &rng,
-                          u32 *path_out, long long pos, int pos_step, u32 &emitted,
-                          BlockShared<BLOCK> &sh, WorkRegs &wk) {
+__device__ __forceinline__ u64 sum_frontier_degrees(const SamplerParams &p, const SideRegs &sd, u64 *red) {
+    u64 s = 0;
+    for (u32 i = sd.fb + threadIdx.x; i < sd.cnt; i += BLOCK) {
+        const u32 v = ld_cg(sd.list + i);
+        s += __ldg(p.offsets + v + 1) - __ldg(p.offsets + v);
+    }
+    const u64 r = block_sum_u64<BLOCK>(s, red);
+    __syncthreads();
+    return r;
+}
+
+// One sigma-weighted step chain from `u` (at depth d on side `x`) to the side's
+// root (sampler.cpp:135-155).  Emits every vertex strictly between into the
+// frame and, optionally, into path_out[pos], pos advancing by pos_step.
+//
+// predecessors(u) = { w in N(u) : visited(w) && dist[w] + 1 == dist[u] }
+//                 = N(u) ∩ level(d-1), chosen in CSR (= ascending id) order.
+// They are enumerated either by scanning the row of u and testing each label
+// against the idx range of level d-1, or -- when level d-1 is much smaller than
+// the row, the common case for hub vertices -- by binary-searching every vertex
+// of level d-1 in the sorted row.  Both yield the same set with the same row
+// positions, hence the same pick.
+template <int BLOCK, int ITEMS>
+__device__ void walk_side(const SamplerParams &p, const u32 *lab, int x, const SideRegs &sd, u32 u, u32 d,
+                          SampleStream &rng, u32 *path_out, long long pos, int pos_step, u32 &emitted,
+                          BlockShared<BLOCK, ITEMS> &sh, WorkRegs &wk) {
     const u32 tid = threadIdx.x;
     while (d > 0) {
-        // predecessors = neighbours w with visited(w) && dist[w] + 1 == dist[u]
-        //              = label(w) - base in [lvl[d-1], lvl[d])
-        const u32 lo = ld_cg(sd.lvl + (d - 1)), hi = ld_cg(sd.lvl + d);
-        const u32 span = hi - lo;
-        const u32 lab_lo = sd.base + lo;
         const u64 beg = __ldg(p.offsets + u), end = __ldg(p.offsets + u + 1);
         if (tid == 0) {
-            sh.pred_cnt = 0;
             sh.ws[kW_S_walk] += 1;
             sh.ws[kW_E_walk] += end - beg;
         }
-        __syncthreads();
-        // pass 1 (sampler.cpp:138-141): total = sum of sigma over predecessors
-        u128 total_local = 0;
-        for (u64 k = beg + tid; k < end; k += BLOCK) {
-            const u32 w = __ldg(p.targets + k);
-            const u32 rel = ld_cg(sd.lab + w) - lab_lo;
-            if (rel < span) {
-                const u64 sg = ld_cg(sd.sig + lo + rel);
-                total_local += sg;
+        u32 chosen = u;
+        if (d == 1) {
+            // the only vertex at depth 0 is the root and sigma[root] == 1: total = 1, r = 0
+            (void)uniform_below_u128(rng, 1);
+            chosen = ld_cg(sd.list);
+            if (tid == 0)
                 wk.p_walk += 1;
-                const u32 slot = atomicAdd(&sh.pred_cnt, 1u);
-                if (slot < 32) {
-                    sh.pred_pos[slot] = static_cast<u32>(k - beg);
-                    sh.pred_sig[slot] = sg;
-                    sh.pred_vtx[slot] = w;
+        } else {
+            const u32 lo = ld_cg(sd.lvl + (d - 1)), hi = ld_cg(sd.lvl + d);
+            const u32 span = hi - lo;
+            const u32 lab_lo = sd.base + lo;
+            const u64 degu = end - beg;
+            if (tid == 0)
+                sh.pred_cnt = 0;
+            __syncthreads();
+            // pass 1 (sampler.cpp:138-141): total = sum of sigma over predecessors
+            u128 total_local = 0;
+            const bool by_level = static_cast<u64>(span) * (66 - __clzll(degu)) < degu;
+            if (by_level) {
+                for (u32 i = lo + tid; i < hi; i += BLOCK) {
+                    const u32 w = ld_cg(sd.list + i);
+                    u64 a = beg, b = end; // lower_bound of w in the row of u
+                    while (a < b) {
+                        const u64 mid = (a + b) >> 1;
+                        if (__ldg(p.targets + mid) < w)
+                            a = mid + 1;
+                        else
+                            b = mid;
+                    }
+                    if (a < end && __ldg(p.targets + a) == w) {
+                        const u64 sg = ld_cg(sd.sig + i);
+                        total_local += sg;
+                        wk.p_walk += 1;
+                        const u32 slot = atomicAdd(&sh.pred_cnt, 1u);
+                        if (slot < kPredCache) {
+                            sh.pred_pos[slot] = static_cast<u32>(a - beg);
+                            sh.pred_sig[slot] = sg;
+                            sh.pred_vtx[slot] = w;
+                        }
+                    }
+                }
+            } else {
+                for (u64 k = beg + tid; k < end; k += BLOCK) {
+                    const u32 w = __ldg(p.targets + k);
+                    const u32 rel = ld_cg(lab + 2 * static_cast<u64>(w) + x) - lab_lo;
+                    if (rel < span) {
+                        const u64 sg = ld_cg(sd.sig + lo + rel);
+                        total_local += sg;
+                        wk.p_walk += 1;
+                        const u32 slot = atomicAdd(&sh.pred_cnt, 1u);
+                        if (slot < kPredCache) {
+                            sh.pred_pos[slot] = static_cast<u32>(k - beg);
+                            sh.pred_sig[slot] = sg;
+                            sh.pred_vtx[slot] = w;
+                        }
+                    }
                 }
             }
-        }
-        u64 tlo, thi, tov;
-        block_sum_u128<BLOCK>(total_local, tlo, thi, tov, sh.red64);
-        const u128 total = (static_cast<u128>(thi) << 64) | tlo; // < 2^96, cannot overflow
-        __syncthreads();
-        const u32 npred = sh.pred_cnt;
-        u128 r = uniform_below_u128(rng, total); // sampler.cpp:142
-        u32 chosen = u;
-        if (npred <= 32) {
-            // pass 2 on the cached predecessors, in CSR order (sampler.cpp:143-151)
-            if (tid < 32) {
-                const bool have = tid < npred;
-                const u32 mypos = have ? sh.pred_pos[tid] : 0xffffffffu;
-                const u64 mysig = have ? sh.pred_sig[tid] : 0;
-                u128 before = 0;
-                for (u32 q = 0; q < npred; ++q) {
-                    const u32 qpos = sh.pred_pos[q];
-                    if (qpos < mypos)
-                        before += sh.pred_sig[q];
+            u64 tlo, thi, tov;
+            block_sum_u128<BLOCK>(total_local, tlo, thi, tov, sh.red64);
+            const u128 total = (static_cast<u128>(thi) << 64) | tlo; // < 2^96, cannot overflow
+            __syncthreads();
+            const u32 npred = sh.pred_cnt;
+            const u128 r = uniform_below_u128(rng, total); // sampler.cpp:142
+            if (npred <= kPredCache) {
+                // pass 2 on the cached predecessors, in CSR order (sampler.cpp:143-151)
+                if (tid < kPredCache) {
+                    const bool have = tid < npred;
+                    const u32 mypos = have ? sh.pred_pos[tid] : 0xffffffffu;
+                    const u64 mysig = have ? sh.pred_sig[tid] : 0;
+                    u128 before = 0;
+                    for (u32 q = 0; q < npred; ++q)
+                        if (sh.pred_pos[q] < mypos)
+                            before += sh.pred_sig[q];
+                    if (have && before <= r && r - before < mysig)
+                        sh.bcast[0] = sh.pred_vtx[tid];
                 }
-                if (have && before <= r && r - before < mysig)
-                    sh.bcast[0] = sh.pred_vtx[tid];
+                __syncthreads();
+                chosen = sh.bcast[0];
+            } else {
+                // pass 2 by re-scanning the row in order with a block-wide prefix search
+                u128 running = 0;
+                bool running_ovf = false;
+                for (u64 k0 = beg; k0 < end; k0 += BLOCK) {
+                    const u64 k = k0 + tid;
+                    u128 wv = 0;
+                    u32 w = 0;
+                    if (k < end) {
+                        w = __ldg(p.targets + k);
+                        const u32 rel = ld_cg(lab + 2 * static_cast<u64>(w) + x) - lab_lo;
+                        if (rel < span)
+                            wv = ld_cg(sd.sig + lo + rel);
+                    }
+                    const u32 f = block_first_exceeding<BLOCK>(wv, running, running_ovf, r, sh.red64, &sh.found_lane);
+                    if (f != BLOCK) {
+                        if (tid == f)
+                            sh.bcast[0] = w;
+                        __syncthreads();
+                        chosen = sh.bcast[0];
+                        break;
+                    }
+                }
             }
             __syncthreads();
-            chosen = sh.bcast[0];
-        } else {
-            // pass 2 by re-scanning the row in order with a block-wide prefix search
-            u128 running = 0;
-            bool running_ovf = false;
-            for (u64 k0 = beg; k0 < end; k0 += BLOCK) {
-                const u64 k = k0 + tid;
-                u128 wv = 0;
-                u32 w = 0;
-                if (k < end) {
-                    w = __ldg(p.targets + k);
-                    const u32 rel = ld_cg(sd.lab + w) - lab_lo;
-                    if (rel < span)
-                        wv = ld_cg(sd.sig + lo + rel);
-                }
-                const u32 f = block_first_exceeding<BLOCK>(wv, running, running_ovf, r, sh);
-                if (f != BLOCK) {
-                    if (tid == f)
-                        sh.bcast[0] = w;
-                    __syncthreads();
-                    chosen = sh.bcast[0];
-                    break;
-                }
-            }
         }
-        __syncthreads();
         u = chosen;
         d -= 1;
         if (d > 0) { // sampler.cpp:152-153: endpoints are never counted
@@ -508,9 +688,9 @@ __device__ void walk_side(const SamplerParams &p, const SideRegs &sd, u32 u, u32
     }
 }
 
-template <int BLOCK>
+template <int BLOCK, int ITEMS>
 __global__ void __launch_bounds__(BLOCK) sample_kernel(const SamplerParams p) {
-    __shared__ BlockShared<BLOCK> sh;
+    __shared__ BlockShared<BLOCK, ITEMS> sh;
     const u32 tid = threadIdx.x;
     const u64 slot = p.slot_base + blockIdx.x;
     const u64 n = p.n;
@@ -520,9 +700,9 @@ __global__ void __launch_bounds__(BLOCK) sample_kernel(const SamplerParams p) {
         ticket_count = listed < ticket_count ? listed : ticket_count;
     }
 
+    u32 *lab = p.lab + slot * 2 * n; // lab[2v + side]
     SideRegs side[2];
     for (int k = 0; k < 2; ++k) {
-        side[k].lab = p.lab + (slot * 2 + k) * n;
         side[k].list = p.list + (slot * 2 + k) * p.cap;
         side[k].sig = p.sig + (slot * 2 + k) * p.cap;
         side[k].lvl = p.lvl + (slot * 2 + k) * (p.cap + 2);
@@ -547,13 +727,22 @@ __global__ void __launch_bounds__(BLOCK) sample_kernel(const SamplerParams p) {
         const u64 local = p.relist ? p.relist[ticket] : ticket;
         const u64 index = p.first + local;
 
-        // ---- label-space housekeeping: a side's labels must stay below the claim range ----
-        for (int k = 0; k < 2; ++k) {
-            const u64 limit = static_cast<u64>(kClaimTop) - kMaxBlockThreads - 2;
-            if (static_cast<u64>(side[k].base) + p.cap + 1 >= limit) {
-                for (u64 i = tid; i < n; i += BLOCK)
-                    st_cg(side[k].lab + i, 0u);
-                side[k].base = 1;
+        // ---- label-space housekeeping: labels must stay below the claim range ----
+        {
+            const u64 limit = static_cast<u64>(kClaimTop) - kMaxTileSlots - 2;
+            const bool r0 = static_cast<u64>(side[0].base) + p.cap + 1 >= limit;
+            const bool r1 = static_cast<u64>(side[1].base) + p.cap + 1 >= limit;
+            if (r0 || r1) {
+                for (u64 i = tid; i < n; i += BLOCK) {
+                    if (r0)
+                        st_cg(lab + 2 * i, 0u);
+                    if (r1)
+                        st_cg(lab + 2 * i + 1, 0u);
+                }
+                if (r0)
+                    side[0].base = 1;
+                if (r1)
+                    side[1].base = 1;
                 __syncthreads();
             }
         }
@@ -581,7 +770,7 @@ __global__ void __launch_bounds__(BLOCK) sample_kernel(const SamplerParams p) {
             side[k].depth = 0;
             side[k].pending = __ldg(p.offsets + root + 1) - __ldg(p.offsets + root);
             if (tid == 0) {
-                st_cg(side[k].lab + root, side[k].base);
+                st_cg(lab + 2 * static_cast<u64>(root) + k, side[k].base);
                 st_cg(side[k].list, root);
                 st_cg(side[k].sig, static_cast<u64>(1));
                 st_cg(side[k].lvl, 0u);
@@ -616,12 +805,15 @@ __global__ void __launch_bounds__(BLOCK) sample_kernel(const SamplerParams p) {
             if (side[0].cnt == side[0].fb || side[1].cnt == side[1].fb)
                 break; // a frontier ran empty: t unreachable, empty sample (sampler.cpp:82-83)
             e = side[0].pending <= side[1].pending ? 0 : 1; // tie -> forward (sampler.cpp:84)
-            if (!expand_level<BLOCK>(p, side[e], side[1 - e], contact, contact_n, sh, wk)) {
+            if (!expand_level<BLOCK, ITEMS>(p, lab, e, side[e], side[1 - e], contact, contact_n, sh, wk)) {
                 aborted = true;
                 break;
             }
             found = sh.min_contact != 0xffffffffu;
-            __syncthreads();
+            if (!found)
+                side[e].pending = sum_frontier_degrees<BLOCK>(p, side[e], sh.red64);
+            else
+                __syncthreads();
         }
 
         if (aborted) {
@@ -648,11 +840,10 @@ __global__ void __launch_bounds__(BLOCK) sample_kernel(const SamplerParams p) {
             u128 wsum = 0;
             u32 mcount = 0;
             for (u32 c = tid; c < contact_n; c += BLOCK) {
-                const u32 oi = ld_cg(contact + 2 * c + 1);
+                const u32 oi = ld_cg(contact + 2 * static_cast<u64>(c) + 1);
                 if (oi - olo < ohi - olo) {
-                    const u32 ei = ld_cg(contact + 2 * c);
+                    const u32 ei = ld_cg(contact + 2 * static_cast<u64>(c));
                     wsum += static_cast<u128>(ld_cg(ex.sig + ei)) * ld_cg(ot.sig + oi);
-                    // a single thread's partial sum can itself wrap only beyond 2^64 terms
                     ++mcount;
                 }
             }
@@ -680,13 +871,13 @@ __global__ void __launch_bounds__(BLOCK) sample_kernel(const SamplerParams p) {
                     u128 wv = 0;
                     u32 ei = 0;
                     if (c < contact_n) {
-                        const u32 oi = ld_cg(contact + 2 * c + 1);
+                        const u32 oi = ld_cg(contact + 2 * static_cast<u64>(c) + 1);
                         if (oi - olo < ohi - olo) {
-                            ei = ld_cg(contact + 2 * c);
+                            ei = ld_cg(contact + 2 * static_cast<u64>(c));
                             wv = static_cast<u128>(ld_cg(ex.sig + ei)) * ld_cg(ot.sig + oi);
                         }
                     }
-                    const u32 f = block_first_exceeding<BLOCK>(wv, running, running_ovf, pick, sh);
+                    const u32 f = block_first_exceeding<BLOCK>(wv, running, running_ovf, pick, sh.red64, &sh.found_lane);
                     if (f != BLOCK) {
                         if (tid == f)
                             sh.bcast[0] = ei;
@@ -697,9 +888,9 @@ __global__ void __launch_bounds__(BLOCK) sample_kernel(const SamplerParams p) {
                 }
                 if (meet_e == 0xffffffffu) {
                     for (u32 c = contact_n; c-- > 0;) {
-                        const u32 oi = ld_cg(contact + 2 * c + 1);
+                        const u32 oi = ld_cg(contact + 2 * static_cast<u64>(c) + 1);
                         if (oi - olo < ohi - olo) {
-                            meet_e = ld_cg(contact + 2 * c);
+                            meet_e = ld_cg(contact + 2 * static_cast<u64>(c));
                             break;
                         }
                     }
@@ -714,8 +905,8 @@ __global__ void __launch_bounds__(BLOCK) sample_kernel(const SamplerParams p) {
             const u32 dist_b = e == 0 ? d_ot : d_ex;
             u32 emitted = 0;
             // forward side: vertices at forward depth d sit at internal position d-1
-            walk_side<BLOCK>(p, side[0], meet, dist_f, rng, path_out, static_cast<long long>(dist_f) - 2, -1,
-                             emitted, sh, wk);
+            walk_side<BLOCK, ITEMS>(p, lab, 0, side[0], meet, dist_f, rng, path_out,
+                                    static_cast<long long>(dist_f) - 2, -1, emitted, sh, wk);
             if (meet != s && meet != t) {
                 if (tid == 0) {
                     atomicAdd(p.frame + 1 + meet, 1u);
@@ -724,8 +915,8 @@ __global__ void __launch_bounds__(BLOCK) sample_kernel(const SamplerParams p) {
                 }
                 emitted += 1;
             }
-            walk_side<BLOCK>(p, side[1], meet, dist_b, rng, path_out, static_cast<long long>(dist_f), +1,
-                             emitted, sh, wk);
+            walk_side<BLOCK, ITEMS>(p, lab, 1, side[1], meet, dist_b, rng, path_out,
+                                    static_cast<long long>(dist_f), +1, emitted, sh, wk);
             rec.path_len = emitted;
             if (tid == 0)
                 sh.ws[kW_L] += emitted;
