@@ -146,6 +146,12 @@ typedef struct ebc_run_config {
     uint64_t slot_capacity;    /* settled vertices per side per slot: 0 = auto             */
     int overlap;               /* 1 = sample epoch e+1 while epoch e is reduced/checked    */
     uint32_t items_per_thread; /* adjacency slots per thread per tile (1|2|4): 0 = auto    */
+    int materialize_final_level; /* 1 = also settle (label, sigma) every vertex of a sample's LAST level.
+                                  * By default a large last level is only scanned: its contact edges give
+                                  * the meet set, sigma and order the reference derives (bit-identical
+                                  * paths, counters, tau), but vertices that cannot lie on the sampled path
+                                  * are not labelled.  Needed for ebc_sampler_last_state and for work
+                                  * counters V_set / F_chk / E_lvl that equal the reference algorithm's. */
 } ebc_run_config;
 
 EBC_API void ebc_run_config_default(ebc_run_config *cfg);

@@ -228,6 +228,7 @@ class RunConfig:
     slot_capacity: int = 0
     overlap: bool = True
     items_per_thread: int = 0
+    materialize_final_level: bool = False
 
     def to_c(self) -> _CRunConfig:
         c = _CRunConfig()
@@ -237,6 +238,7 @@ class RunConfig:
                   "rank", "world_size", "block_threads", "slots", "slot_capacity", "items_per_thread"):
             setattr(c, f, getattr(self, f))
         c.overlap = int(self.overlap)
+        c.materialize_final_level = int(self.materialize_final_level)
         if self.allreduce is not None:
             c.allreduce = self.allreduce
         return c

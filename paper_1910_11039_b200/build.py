@@ -42,6 +42,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "-gencode", "arch=compute_100a,code=sm_100a",
            "-Xcompiler", "-fPIC,-fvisibility=hidden,-Wall,-Wextra,-Wno-unknown-pragmas",
            "-shared", "-o", LIB] + [os.path.join(CSRC, s) for s in SOURCES] + ["-lpthread"]
+    cmd[1:1] = os.environ.get("EBC_NVCC_FLAGS", "").split()
     if verbose:
         cmd.insert(1, "-Xptxas")
         cmd.insert(2, "-v")

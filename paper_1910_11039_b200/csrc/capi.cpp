@@ -74,6 +74,7 @@ SamplerOptions sampler_options(const ebc_run_config *cfg) {
         o.slots = cfg->slots;
         o.slot_capacity = cfg->slot_capacity;
         o.items_per_thread = cfg->items_per_thread;
+        o.materialize_final_level = cfg->materialize_final_level != 0;
     }
     return o;
 }

@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -187,9 +188,13 @@ __global__ void flush_kernel(u32 *buf, u64 count, u32 salt) {
 }
 
 // (BLOCK, ITEMS) instantiations of the sampling kernel.
+#ifdef EBC_FEW_SHAPES // faster experimental builds
+#define EBC_FOR_EACH_SHAPE(X) X(32, 1) X(64, 2) X(64, 4) X(128, 2) X(128, 4) X(256, 4)
+#else
 #define EBC_FOR_EACH_SHAPE(X) \
     X(32, 1) X(32, 2) X(32, 4) X(64, 1) X(64, 2) X(64, 4) X(128, 1) X(128, 2) X(128, 4) X(256, 1) X(256, 2) \
     X(256, 4) X(512, 1) X(512, 2) X(512, 4)
+#endif
 
 void launch_sample_dispatch(u32 block, u32 items, const SamplerParams &p, u32 grid, cudaStream_t stream) {
     bool done = false;
@@ -230,9 +235,9 @@ struct SlotArrays {
         list = dev_alloc<u32>(slots * 2 * cap);
         sig = dev_alloc<u64>(slots * 2 * cap);
         lvl = dev_alloc<u32>(slots * 2 * (cap + 2));
-        contact = dev_alloc<u32>(slots * 2 * cap);
+        contact = dev_alloc<u32>(slots * 6 * cap);
         hdr = dev_alloc<u32>(slots * kHdrWords);
-        bytes = slots * (2 * n * 4 + 2 * cap * (4 + 8 + 4) + 2 * (cap + 2) * 4 + kHdrWords * 4);
+        bytes = slots * bytes_per_slot(n, cap);
         EBC_CUDA(cudaMemsetAsync(lab, 0, slots * 2 * n * 4, stream));
         std::vector<u32> h(slots * kHdrWords, 0);
         for (u64 s = 0; s < slots; ++s)
@@ -248,7 +253,9 @@ struct SlotArrays {
         cudaFree(contact);
         cudaFree(hdr);
     }
-    static u64 bytes_per_slot(u64 n, u64 cap) { return 2 * n * 4 + 2 * cap * 16 + 2 * (cap + 2) * 4 + kHdrWords * 4; }
+    static u64 bytes_per_slot(u64 n, u64 cap) {
+        return 2 * n * 4 + 2 * cap * (4 + 8) + 2 * (cap + 2) * 4 + 6 * cap * 4 + kHdrWords * 4;
+    }
 };
 
 constexpr u32 kOverflowCap = 1u << 20; // also the largest number of samples per launch
@@ -264,6 +271,7 @@ struct CudaSampler::Impl {
     u32 *d_targets = nullptr;
     u32 block = 128;
     u32 items = 4;
+    u32 flags = 0;
     SlotArrays small, big;
     u32 *d_frame[2] = {nullptr, nullptr};
     u64 *d_S = nullptr;
@@ -305,6 +313,7 @@ struct CudaSampler::Impl {
         p.work = d_work;
         p.overflow_list = d_overflow_list;
         p.overflow_cap = kOverflowCap;
+        p.flags = flags;
         return p;
     }
 
@@ -378,6 +387,17 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
         throw CudaError("this build targets sm_100a (B200); found compute capability " +
                         std::to_string(prop.major) + "." + std::to_string(prop.minor));
     m.sm_count = prop.multiProcessorCount;
+    {
+        // The path is dominated by random 4..8-byte probes of per-vertex labels.  With the default
+        // L2 fetch granularity every such probe pulls a whole 128-byte line from HBM (measured with
+        // ncu: 4 sectors per request); 32 bytes makes DRAM traffic match the sectors actually used.
+        size_t granularity = 32;
+        if (const char *env = std::getenv("EBC_L2_FETCH_GRANULARITY"))
+            granularity = static_cast<size_t>(std::atoi(env));
+        if (granularity == 32 || granularity == 64 || granularity == 128)
+            cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, granularity); // a hint; failure is harmless
+        cudaGetLastError();
+    }
     require(g.n >= 2, "sampler: need at least two vertices");
     m.n = g.n;
     m.arcs = g.targets.size();
@@ -402,6 +422,7 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
     // ---- launch shape ----
     m.block = opt.block_threads ? opt.block_threads : 128;
     m.items = opt.items_per_thread ? opt.items_per_thread : 4;
+    m.flags = opt.materialize_final_level ? kFlagMaterializeFinal : 0u;
     const int per_sm = occupancy_for(m.block, m.items);
     if (per_sm < 1)
         throw CudaError("sampling kernel does not fit on an SM");

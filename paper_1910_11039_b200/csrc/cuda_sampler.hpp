@@ -19,6 +19,7 @@ struct SamplerOptions {
     std::uint32_t slots = 0;         // 0 = auto
     std::uint64_t slot_capacity = 0; // 0 = auto
     std::uint32_t items_per_thread = 0; // 0 = auto
+    bool materialize_final_level = false; // settle the final level of every sample (see ebc_b200.h)
 };
 
 struct SampleRecordHost { // == ebc_sample_record

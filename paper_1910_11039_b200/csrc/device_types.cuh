@@ -37,6 +37,7 @@ enum WorkCounter : int {
 constexpr u32 kClaimTop = 0xffffffffu;     // transient claim values: kClaimTop - slot_in_tile
 constexpr u32 kMaxBlockThreads = 1024;
 constexpr u32 kMaxTileSlots = 4096;        // BLOCK * ITEMS never exceeds this
+constexpr u32 kFlagMaterializeFinal = 1u; // always settle the final level (state dumps, exact V_set / F_chk)
 constexpr u32 kHdrWords = 16;              // per-slot header (u32)
 // header word indices
 enum : int { kHdrBase0 = 0, kHdrBase1 = 1, kHdrLastBase0 = 2, kHdrLastBase1 = 3, kHdrLastCnt0 = 4,
@@ -81,6 +82,7 @@ struct SamplerParams {
     const u32 *count_ptr;
     u64 slot_base;              // first slot used by this launch
     unsigned long long *overflow_total; // persistent count of abandoned samples of this pass
+    u32 flags;                  // kFlag*
 };
 
 } // namespace ebc

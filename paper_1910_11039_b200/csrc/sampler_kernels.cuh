@@ -77,8 +77,21 @@ __device__ __forceinline__ u128 uniform_below_u128(SampleStream &rng, u128 bound
 
 constexpr int kPredCache = 32;
 
+// Final-level probe (see probe_level): a level with at least kProbeMinSlots adjacency slots is first
+// scanned read-only; if it touches the other side, the meet set is resolved from at most
+// FinalEdgeCap<BLOCK>::value contact edges and the level is never settled.
+constexpr u64 kProbeMinSlots = 2048;
+template <int BLOCK> struct FinalEdgeCap {
+    static constexpr int value = 4 * BLOCK < 512 ? 4 * BLOCK : 512;
+};
+
 template <int BLOCK, int ITEMS> struct BlockShared {
     static constexpr int WARPS = BLOCK / 32;
+    u64 f_key[FinalEdgeCap<BLOCK>::value]; // contact edges of a probed final level: discovery key,
+    u64 f_s[FinalEdgeCap<BLOCK>::value];   //   sigma of the parent,
+    u32 f_v[FinalEdgeCap<BLOCK>::value];   //   target vertex,
+    u32 f_o[FinalEdgeCap<BLOCK>::value];   //   its idx on the other side
+    u32 edge_cnt;
     u64 c_beg[BLOCK];      // row start of each frontier-chunk vertex
     u64 c_scan[BLOCK + 1]; // exclusive prefix of the chunk's degrees
     u64 c_sig[BLOCK];      // sigma of each chunk vertex
@@ -547,6 +560,249 @@ __device__ __forceinline__ u64 sum_frontier_degrees(const SamplerParams &p, cons
     return r;
 }
 
+// Read-only scan of the level that is about to be expanded on side `e`: every
+// adjacency slot is visited (its target's label is probed exactly as in
+// expand_level) but nothing is written.  Each slot whose target is unvisited on
+// this side and visited on the other side is a CONTACT EDGE; it is appended
+// (unordered) to `edges` as 6 words {frontier position, index in row, target,
+// other-side idx, sigma[u] lo, hi}.  If the level has at least one contact edge
+// the search ends with this level (sampler.cpp:105-115), and everything the
+// reference derives from it -- the meet set in discovery order and
+// sigma_ex[v] = sat-sum of sigma[u] over the parents u of v (sampler.cpp:97-98)
+// -- can be recomputed from the contact edges alone (meet_from_edges), so the
+// ~10^4 label / list / sigma writes of settling a level whose other vertices
+// are never looked at again are skipped.  Returns the number of contact edges
+// (possibly > edge_cap, in which case the caller falls back to expand_level).
+// new_slots counts (per thread) the slots whose target is unvisited on this
+// side (= the level's E_lvl, sampler.cpp:97).
+template <int BLOCK, int ITEMS>
+__device__ u32 probe_level(const SamplerParams &p, const u32 *lab, int e, const SideRegs &ex, const SideRegs &ot,
+                           u32 *edges, u32 edge_cap, BlockShared<BLOCK, ITEMS> &sh, u64 &new_slots,
+                           u64 &total_slots) {
+    constexpr int TILE = BLOCK * ITEMS;
+    const u32 tid = threadIdx.x;
+    const u32 fb = ex.fb, fe = ex.cnt;
+    const u64 *lab64 = reinterpret_cast<const u64 *>(lab);
+    if (tid == 0) {
+        sh.edge_cnt = 0;
+        sh.min_contact = 0xffffffffu;
+    }
+    u64 t_total = 0;
+    for (u32 c0 = fb; c0 < fe; c0 += BLOCK) {
+        const u32 i = c0 + tid;
+        u64 beg = 0, deg = 0, su = 0;
+        if (i < fe) {
+            const u32 u = ld_cg(ex.list + i);
+            beg = __ldg(p.offsets + u);
+            deg = __ldg(p.offsets + u + 1) - beg;
+            su = ld_cg(ex.sig + i);
+        }
+        u64 inc = deg;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u64 t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane_id() >= static_cast<u32>(o))
+                inc += t;
+        }
+        __syncthreads();
+        if (BLOCK > 32 && lane_id() == 31)
+            sh.red64[tid >> 5] = inc;
+        sh.c_beg[tid] = beg;
+        sh.c_sig[tid] = su;
+        if (BLOCK > 32)
+            __syncthreads();
+        u64 before = 0;
+        if (BLOCK > 32)
+            for (u32 w = 0; w < (tid >> 5); ++w)
+                before += sh.red64[w];
+        sh.c_scan[tid + 1] = before + inc;
+        if (tid == 0)
+            sh.c_scan[0] = 0;
+        __syncthreads();
+        const u64 T = sh.c_scan[BLOCK];
+        t_total += T;
+        int row_lo = 0;
+        for (u64 t0 = 0; t0 < T; t0 += TILE) {
+            const u64 t_last = (t0 + TILE < T ? t0 + TILE : T) - 1;
+            while (sh.c_scan[row_lo + 1] <= t0)
+                ++row_lo;
+            int row_hi = row_lo;
+            {
+                int hi = BLOCK;
+                while (hi - row_hi > 1) {
+                    const int mid = (row_hi + hi) >> 1;
+                    if (sh.c_scan[mid] <= t_last)
+                        row_hi = mid;
+                    else
+                        hi = mid;
+                }
+            }
+            u32 v[ITEMS], kk[ITEMS];
+            int owner[ITEMS];
+            bool act[ITEMS];
+#pragma unroll
+            for (int k = 0; k < ITEMS; ++k) {
+                const u64 j = t0 + static_cast<u64>(k) * BLOCK + tid;
+                act[k] = j <= t_last;
+                v[k] = 0;
+                kk[k] = 0;
+                owner[k] = row_lo;
+                if (act[k]) {
+                    int lo = row_lo, hi = row_hi + 1;
+                    while (hi - lo > 1) {
+                        const int mid = (lo + hi) >> 1;
+                        if (sh.c_scan[mid] <= j)
+                            lo = mid;
+                        else
+                            hi = mid;
+                    }
+                    owner[k] = lo;
+                    kk[k] = static_cast<u32>(j - sh.c_scan[lo]);
+                    v[k] = __ldg(p.targets + sh.c_beg[lo] + kk[k]);
+                }
+            }
+            u64 both[ITEMS];
+#pragma unroll
+            for (int k = 0; k < ITEMS; ++k)
+                both[k] = act[k] ? ld_cg(lab64 + v[k]) : 0ull;
+#pragma unroll
+            for (int k = 0; k < ITEMS; ++k) {
+                if (!act[k])
+                    continue;
+                const u32 rel = half_of(both[k], e) - ex.base;
+                if (rel < ex.cnt)
+                    continue; // visited before this level
+                new_slots += 1;
+                const u32 oi = half_of(both[k], 1 - e) - ot.base;
+                if (oi < ot.cnt) {
+                    atomicMin(&sh.min_contact, oi);
+                    const u32 pos = atomicAdd(&sh.edge_cnt, 1u);
+                    if (pos < edge_cap) {
+                        u32 *w = edges + 6 * static_cast<u64>(pos);
+                        const u64 sg = sh.c_sig[owner[k]];
+                        st_cg(w + 0, (c0 - fb) + static_cast<u32>(owner[k]));
+                        st_cg(w + 1, kk[k]);
+                        st_cg(w + 2, v[k]);
+                        st_cg(w + 3, oi);
+                        st_cg(w + 4, static_cast<u32>(sg));
+                        st_cg(w + 5, static_cast<u32>(sg >> 32));
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();
+    total_slots = t_total;
+    return sh.edge_cnt;
+}
+
+// Meet set of a probed final level from its m <= final_edge_cap contact edges:
+// groups the edges by target, sigma_ex[v] = saturating sum of the parents' sigma
+// (order independent), discovery key of v = smallest (frontier position, index
+// in row) among its edges -- exactly the order in which the reference would
+// have appended v to `next` -- and writes the members whose other-side idx lies
+// in [olo, ohi) to meetbuf in that order as {v, other idx, sigma lo, sigma hi}.
+template <int BLOCK, int ITEMS>
+__device__ u32 meet_from_edges(const u32 *edges, u32 m, u32 olo, u32 ohi, u32 *meetbuf,
+                               BlockShared<BLOCK, ITEMS> &sh) {
+    constexpr int PER = FinalEdgeCap<BLOCK>::value / BLOCK > 0 ? FinalEdgeCap<BLOCK>::value / BLOCK : 1;
+    const u32 tid = threadIdx.x;
+    for (u32 i = tid; i < m; i += BLOCK) {
+        const u32 *w = edges + 6 * static_cast<u64>(i);
+        sh.f_key[i] = (static_cast<u64>(ld_cg(w)) << 32) | ld_cg(w + 1);
+        sh.f_v[i] = ld_cg(w + 2);
+        sh.f_o[i] = ld_cg(w + 3);
+        sh.f_s[i] = static_cast<u64>(ld_cg(w + 4)) | (static_cast<u64>(ld_cg(w + 5)) << 32);
+    }
+    __syncthreads();
+    u64 sum[PER];
+    bool first[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const u32 i = tid + q * BLOCK;
+        sum[q] = 0;
+        first[q] = i < m;
+        if (i < m) {
+            const u32 vi = sh.f_v[i];
+            const u64 ki = sh.f_key[i];
+            for (u32 j = 0; j < m; ++j)
+                if (sh.f_v[j] == vi) {
+                    const u64 sj = sh.f_s[j];
+                    sum[q] = sum[q] > ~0ull - sj ? ~0ull : sum[q] + sj; // sat_add_u64 (sampler.cpp:11-13)
+                    if (sh.f_key[j] < ki)
+                        first[q] = false;
+                }
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const u32 i = tid + q * BLOCK;
+        if (i < m) {
+            if (first[q])
+                sh.f_s[i] = sum[q];
+            else
+                sh.f_o[i] = 0xffffffffu; // a later edge of an already listed vertex
+        }
+    }
+    __syncthreads();
+    u32 members = 0;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const u32 i = tid + q * BLOCK;
+        if (i < m && sh.f_o[i] - olo < ohi - olo) {
+            const u64 ki = sh.f_key[i];
+            u32 rank = 0;
+            for (u32 j = 0; j < m; ++j)
+                if (sh.f_o[j] - olo < ohi - olo && sh.f_key[j] < ki)
+                    ++rank;
+            u32 *w = meetbuf + 4 * static_cast<u64>(rank);
+            st_cg(w + 0, sh.f_v[i]);
+            st_cg(w + 1, sh.f_o[i]);
+            st_cg(w + 2, static_cast<u32>(sh.f_s[i]));
+            st_cg(w + 3, static_cast<u32>(sh.f_s[i] >> 32));
+            ++members;
+        }
+    }
+    const u32 total = static_cast<u32>(block_sum_u64<BLOCK>(members, sh.red64));
+    __syncthreads();
+    return total;
+}
+
+// Meet set of a normally expanded final level: the contacts (in discovery order)
+// whose other-side idx lies in [olo, ohi), written to meetbuf like meet_from_edges.
+template <int BLOCK, int ITEMS>
+__device__ u32 meet_from_contacts(const u32 *contact, u32 contact_n, const SideRegs &ex, u32 olo, u32 ohi,
+                                  u32 *meetbuf, BlockShared<BLOCK, ITEMS> &sh) {
+    const u32 tid = threadIdx.x;
+    u32 count = 0;
+    for (u32 c0 = 0; c0 < contact_n; c0 += BLOCK) {
+        const u32 c = c0 + tid;
+        bool in[1] = {false};
+        u32 ei = 0, oi = 0;
+        if (c < contact_n) {
+            oi = ld_cg(contact + 2 * static_cast<u64>(c) + 1);
+            in[0] = oi - olo < ohi - olo;
+            if (in[0])
+                ei = ld_cg(contact + 2 * static_cast<u64>(c));
+        }
+        u32 rank[1];
+        const u32 tot = block_ranks<BLOCK, 1>(in, rank, sh.warp_cnt);
+        if (in[0]) {
+            const u64 sg = ld_cg(ex.sig + ei);
+            u32 *w = meetbuf + 4 * static_cast<u64>(count + rank[0]);
+            st_cg(w + 0, ld_cg(ex.list + ei));
+            st_cg(w + 1, oi);
+            st_cg(w + 2, static_cast<u32>(sg));
+            st_cg(w + 3, static_cast<u32>(sg >> 32));
+        }
+        count += tot;
+        __syncthreads();
+    }
+    __syncthreads();
+    return count;
+}
+
 // One sigma-weighted step chain from `u` (at depth d on side `x`) to the side's
 // root (sampler.cpp:135-155).  Emits every vertex strictly between into the
 // frame and, optionally, into path_out[pos], pos advancing by pos_step.
@@ -688,8 +944,16 @@ __device__ void walk_side(const SamplerParams &p, const u32 *lab, int x, const S
     }
 }
 
+// Resident CTAs per SM the kernel is compiled for (register budget = 65536 / (BLOCK * this)).
+#ifndef EBC_WARPS_PER_SM
+#define EBC_WARPS_PER_SM 16
+#endif
+template <int BLOCK> constexpr int min_blocks_per_sm() {
+    return (EBC_WARPS_PER_SM * 32) / BLOCK > 0 ? (EBC_WARPS_PER_SM * 32) / BLOCK : 1;
+}
+
 template <int BLOCK, int ITEMS>
-__global__ void __launch_bounds__(BLOCK) sample_kernel(const SamplerParams p) {
+__global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kernel(const SamplerParams p) {
     __shared__ BlockShared<BLOCK, ITEMS> sh;
     const u32 tid = threadIdx.x;
     const u64 slot = p.slot_base + blockIdx.x;
@@ -708,7 +972,11 @@ __global__ void __launch_bounds__(BLOCK) sample_kernel(const SamplerParams p) {
         side[k].lvl = p.lvl + (slot * 2 + k) * (p.cap + 2);
         side[k].base = p.hdr[slot * kHdrWords + kHdrBase0 + k];
     }
-    u32 *contact = p.contact + slot * 2 * p.cap;
+    u32 *contact = p.contact + slot * 6 * p.cap; // 2*cap words: contacts / contact edges
+    u32 *meetbuf = contact + 2 * p.cap;          // 4*cap words: ordered meet set
+    const u32 edge_cap = static_cast<u32>((2 * p.cap) / 6 < static_cast<u64>(FinalEdgeCap<BLOCK>::value)
+                                              ? (2 * p.cap) / 6
+                                              : static_cast<u64>(FinalEdgeCap<BLOCK>::value));
     WorkRegs wk;
     u64 tot_e_lvl = 0, tot_p_walk = 0;
     if (tid == 0)
@@ -798,13 +1066,33 @@ __global__ void __launch_bounds__(BLOCK) sample_kernel(const SamplerParams p) {
         rec.weight_lo = rec.weight_hi = 0;
 
         // ---- level loop (sampler.cpp:81-116) ----
-        bool found = false, aborted = false;
+        bool found = false, aborted = false, probed = false;
         int e = 0;
-        u32 contact_n = 0;
+        u32 contact_n = 0, edge_n = 0;
         while (!found) {
             if (side[0].cnt == side[0].fb || side[1].cnt == side[1].fb)
                 break; // a frontier ran empty: t unreachable, empty sample (sampler.cpp:82-83)
             e = side[0].pending <= side[1].pending ? 0 : 1; // tie -> forward (sampler.cpp:84)
+            if (!(p.flags & kFlagMaterializeFinal) && edge_cap > 0 && side[e].pending >= kProbeMinSlots) {
+                u64 new_slots = 0, total_slots = 0;
+                edge_n = probe_level<BLOCK, ITEMS>(p, lab, e, side[e], side[1 - e], contact, edge_cap, sh, new_slots,
+                                                   total_slots);
+                if (edge_n > 0 && edge_n <= edge_cap) {
+                    // final level: account its scan, open the (virtual) level for the walk, stop
+                    wk.e_lvl += new_slots;
+                    if (tid == 0) {
+                        sh.ws[kW_E_bfs] += total_slots;
+                        sh.ws[kW_V_exp] += side[e].cnt - side[e].fb;
+                        sh.ws[kW_levels] += 1;
+                        st_cg(side[e].lvl + side[e].depth + 1, side[e].cnt);
+                    }
+                    __syncthreads();
+                    probed = true;
+                    found = true;
+                    break;
+                }
+                __syncthreads(); // no contact (or too many contact edges): expand normally
+            }
             if (!expand_level<BLOCK, ITEMS>(p, lab, e, side[e], side[1 - e], contact, contact_n, sh, wk)) {
                 aborted = true;
                 break;
@@ -827,6 +1115,7 @@ __global__ void __launch_bounds__(BLOCK) sample_kernel(const SamplerParams p) {
         } else if (found) {
             SideRegs &ex = side[e];
             SideRegs &ot = side[1 - e];
+            const u32 d_ex = probed ? ex.depth + 1 : ex.depth; // depth of the level that touched the other side
             // best = min other.dist over contacts = level of the smallest other-side idx
             const u32 min_idx = sh.min_contact;
             u32 best = ot.depth;
@@ -834,22 +1123,24 @@ __global__ void __launch_bounds__(BLOCK) sample_kernel(const SamplerParams p) {
                 --best;
             const u32 olo = ld_cg(ot.lvl + best);
             const u32 ohi = best == ot.depth ? ot.cnt : ld_cg(ot.lvl + best + 1);
-            rec.dist = ex.depth + best;
+            rec.dist = d_ex + best;
+            if (probed)
+                rec.flags |= 2u;
+            __syncthreads();
+
+            // meet set in discovery order (sampler.cpp:109-113) -> meetbuf
+            const u32 meet_count = probed ? meet_from_edges<BLOCK, ITEMS>(contact, edge_n, olo, ohi, meetbuf, sh)
+                                          : meet_from_contacts<BLOCK, ITEMS>(contact, contact_n, ex, olo, ohi, meetbuf, sh);
 
             // total weight over the meet set (sampler.cpp:121-123), saturating at 2^128-1
             u128 wsum = 0;
-            u32 mcount = 0;
-            for (u32 c = tid; c < contact_n; c += BLOCK) {
-                const u32 oi = ld_cg(contact + 2 * static_cast<u64>(c) + 1);
-                if (oi - olo < ohi - olo) {
-                    const u32 ei = ld_cg(contact + 2 * static_cast<u64>(c));
-                    wsum += static_cast<u128>(ld_cg(ex.sig + ei)) * ld_cg(ot.sig + oi);
-                    ++mcount;
-                }
+            for (u32 c = tid; c < meet_count; c += BLOCK) {
+                const u32 *w = meetbuf + 4 * static_cast<u64>(c);
+                const u64 sg = static_cast<u64>(ld_cg(w + 2)) | (static_cast<u64>(ld_cg(w + 3)) << 32);
+                wsum += static_cast<u128>(sg) * ld_cg(ot.sig + ld_cg(w + 1));
             }
             u64 wlo, whi, wov;
             block_sum_u128<BLOCK>(wsum, wlo, whi, wov, sh.red64);
-            const u32 meet_count = static_cast<u32>(block_sum_u64<BLOCK>(mcount, sh.red64));
             __syncthreads();
             const u128 total_weight = wov ? ~static_cast<u128>(0) : ((static_cast<u128>(whi) << 64) | wlo);
             rec.weight_lo = static_cast<u64>(total_weight);
@@ -862,45 +1153,36 @@ __global__ void __launch_bounds__(BLOCK) sample_kernel(const SamplerParams p) {
             // sum of the weights, so a hit always exists; the reference's fall-through
             // default (last meet vertex, sampler.cpp:125) is kept for completeness.
             const u128 pick = uniform_below_u128(rng, total_weight);
-            u32 meet_e = 0xffffffffu;
+            u32 meet = 0xffffffffu;
             {
                 u128 running = 0;
                 bool running_ovf = false;
-                for (u32 c0 = 0; c0 < contact_n && meet_e == 0xffffffffu; c0 += BLOCK) {
+                for (u32 c0 = 0; c0 < meet_count && meet == 0xffffffffu; c0 += BLOCK) {
                     const u32 c = c0 + tid;
                     u128 wv = 0;
-                    u32 ei = 0;
-                    if (c < contact_n) {
-                        const u32 oi = ld_cg(contact + 2 * static_cast<u64>(c) + 1);
-                        if (oi - olo < ohi - olo) {
-                            ei = ld_cg(contact + 2 * static_cast<u64>(c));
-                            wv = static_cast<u128>(ld_cg(ex.sig + ei)) * ld_cg(ot.sig + oi);
-                        }
+                    u32 mv = 0;
+                    if (c < meet_count) {
+                        const u32 *w = meetbuf + 4 * static_cast<u64>(c);
+                        const u64 sg = static_cast<u64>(ld_cg(w + 2)) | (static_cast<u64>(ld_cg(w + 3)) << 32);
+                        wv = static_cast<u128>(sg) * ld_cg(ot.sig + ld_cg(w + 1));
+                        mv = ld_cg(w);
                     }
                     const u32 f = block_first_exceeding<BLOCK>(wv, running, running_ovf, pick, sh.red64, &sh.found_lane);
                     if (f != BLOCK) {
                         if (tid == f)
-                            sh.bcast[0] = ei;
+                            sh.bcast[0] = mv;
                         __syncthreads();
-                        meet_e = sh.bcast[0];
+                        meet = sh.bcast[0];
                         __syncthreads();
                     }
                 }
-                if (meet_e == 0xffffffffu) {
-                    for (u32 c = contact_n; c-- > 0;) {
-                        const u32 oi = ld_cg(contact + 2 * static_cast<u64>(c) + 1);
-                        if (oi - olo < ohi - olo) {
-                            meet_e = ld_cg(contact + 2 * static_cast<u64>(c));
-                            break;
-                        }
-                    }
-                }
+                if (meet == 0xffffffffu)
+                    meet = ld_cg(meetbuf + 4 * static_cast<u64>(meet_count - 1));
             }
-            const u32 meet = ld_cg(ex.list + meet_e);
             rec.meet = meet;
 
             // walks (sampler.cpp:157-163): path order s .. meet .. t
-            const u32 d_ex = ex.depth, d_ot = best;
+            const u32 d_ot = best;
             const u32 dist_f = e == 0 ? d_ex : d_ot; // depth of meet on the forward side
             const u32 dist_b = e == 0 ? d_ot : d_ex;
             u32 emitted = 0;

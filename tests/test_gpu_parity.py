@@ -70,7 +70,7 @@ def test_search_state_matches_oracle(block):
         off, tg = small_graphs()[name]
         g = ebc.Graph.from_csr(off, tg)
         o = Oracle(off, tg)
-        s = ebc.Sampler(g, ebc.RunConfig(block_threads=block, slots=1))
+        s = ebc.Sampler(g, ebc.RunConfig(block_threads=block, slots=1, materialize_final_level=True))
         for i in range(25):
             rec, _ = s.sample_debug(SEED, i, 1)
             want = o.sample(SEED, i)
@@ -122,7 +122,7 @@ def test_frames_accumulate_and_epochs_fold():
     (off, tg), _ = largest_component(off, tg)
     g = ebc.Graph.from_csr(off, tg)
     o = Oracle(off, tg)
-    s = ebc.Sampler(g, ebc.RunConfig())
+    s = ebc.Sampler(g, ebc.RunConfig(materialize_final_level=True))
     n = g.num_vertices
     dl, du = ebc.calibrate(np.zeros(n + 1, dtype=np.uint64), n, 0.1)
     s.set_stopping(0.005, 10 ** 9, dl, du)  # Hoeffding width at tau=12000 is ~0.021: never stops here
@@ -159,3 +159,46 @@ def test_rmat14_counters_bit_exact():
         want = o.sample(SEED, i)
         assert int(rec[i]["meet"]) == want["meet"] and int(rec[i]["dist"]) == want["dist"]
         assert np.array_equal(paths[i, :len(want["path"])], want["path"])
+
+
+@pytest.mark.parametrize("block,items", [(32, 1), (64, 2), (128, 4), (256, 4)])
+def test_final_level_probe_is_result_identical(block, items):
+    """Large last levels are only scanned (contact edges -> meet set); paths, counters and the work the
+    reference algorithm defines must not change.  R-MAT-15 has levels far above the probe threshold."""
+    g = ebc.gen_rmat(15, 16, seed=5).largest_connected_component()
+    o = Oracle(g.offsets, g.targets)
+    fast = ebc.Sampler(g, ebc.RunConfig(block_threads=block, items_per_thread=items))
+    full = ebc.Sampler(g, ebc.RunConfig(block_threads=block, items_per_thread=items, materialize_final_level=True))
+    rec, paths = fast.sample_debug(SEED, 0, 3000, path_stride=12)
+    rec2, paths2 = full.sample_debug(SEED, 0, 3000, path_stride=12)
+    assert (rec["flags"] & 2).sum() > 1000          # the probe path really ran
+    assert (rec2["flags"] & 2).sum() == 0
+    for k in ("s", "t", "dist", "meet", "meet_count", "draws", "path_len", "weight_lo", "weight_hi"):
+        assert np.array_equal(rec[k], rec2[k]), k
+    assert np.array_equal(paths, paths2)
+    want = o.accumulate(SEED, 0, 3000)
+    assert np.array_equal(fast.read_frame(0), want) and np.array_equal(full.read_frame(0), want)
+    for i in range(0, 3000, 37):
+        w = o.sample(SEED, i)
+        assert (int(rec[i]["dist"]), int(rec[i]["meet"]), int(rec[i]["draws"])) == (w["dist"], w["meet"], w["draws"])
+        assert int(rec[i]["meet_count"]) == len(o.last_meet_set())
+        assert np.array_equal(paths[i, :len(w["path"])], w["path"])
+    ow = dict(zip(ebc.WORK_NAMES[:11], (int(x) for x in o.work())))   # 3000 + 82 samples
+    o2 = Oracle(g.offsets, g.targets)
+    o2.accumulate(SEED, 0, 3000)
+    ow = dict(zip(ebc.WORK_NAMES[:11], (int(x) for x in o2.work())))
+    wf, wm = fast.work(), full.work()
+    for k in ebc.WORK_NAMES[:11]:
+        assert wm[k] == ow[k], k                      # materialised: every counter equals the reference algorithm's
+    for k in ("E_bfs", "E_lvl", "V_exp", "M", "S_walk", "E_walk", "P_walk", "L", "levels"):
+        assert wf[k] == ow[k], k                      # scanned edges, levels, walks: unchanged
+    assert wf["V_set"] < ow["V_set"] and wf["F_chk"] < ow["F_chk"]   # last-level vertices are not settled
+
+
+def test_final_level_probe_with_tiny_edge_buffer_falls_back():
+    """slot_capacity so small that the contact-edge buffer overflows: expand_level / large-slot fallbacks."""
+    g = ebc.gen_rmat(13, 16, seed=9).largest_connected_component()
+    o = Oracle(g.offsets, g.targets)
+    s = ebc.Sampler(g, ebc.RunConfig(block_threads=64, items_per_thread=2, slots=16, slot_capacity=64))
+    s.sample(SEED, 0, 1500)
+    assert np.array_equal(s.read_frame(0), o.accumulate(SEED, 0, 1500))
