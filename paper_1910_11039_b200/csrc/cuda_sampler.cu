@@ -223,7 +223,7 @@ int occupancy_for(u32 block, u32 items) {
 }
 
 struct SlotArrays {
-    u32 *lab = nullptr, *list = nullptr, *lvl = nullptr, *contact = nullptr, *hdr = nullptr;
+    u32 *lab = nullptr, *list = nullptr, *lvl = nullptr, *contact = nullptr, *hdr = nullptr, *bits = nullptr;
     u64 *sig = nullptr;
     u64 slots = 0, cap = 0;
     u64 bytes = 0;
@@ -236,6 +236,8 @@ struct SlotArrays {
         sig = dev_alloc<u64>(slots * 2 * cap);
         lvl = dev_alloc<u32>(slots * 2 * (cap + 2));
         contact = dev_alloc<u32>(slots * 6 * cap);
+        bits = dev_alloc<u32>(slots * 2 * ((n + 31) / 32));
+        EBC_CUDA(cudaMemsetAsync(bits, 0, slots * 2 * ((n + 31) / 32) * 4, stream));
         hdr = dev_alloc<u32>(slots * kHdrWords);
         bytes = slots * bytes_per_slot(n, cap);
         EBC_CUDA(cudaMemsetAsync(lab, 0, slots * 2 * n * 4, stream));
@@ -251,10 +253,11 @@ struct SlotArrays {
         cudaFree(sig);
         cudaFree(lvl);
         cudaFree(contact);
+        cudaFree(bits);
         cudaFree(hdr);
     }
     static u64 bytes_per_slot(u64 n, u64 cap) {
-        return 2 * n * 4 + 2 * cap * (4 + 8) + 2 * (cap + 2) * 4 + 6 * cap * 4 + kHdrWords * 4;
+        return 2 * n * 4 + 2 * ((n + 31) / 32) * 4 + 2 * cap * (4 + 8) + 2 * (cap + 2) * 4 + 6 * cap * 4 + kHdrWords * 4;
     }
 };
 
@@ -309,6 +312,8 @@ struct CudaSampler::Impl {
         p.lvl = a.lvl;
         p.contact = a.contact;
         p.hdr = a.hdr;
+        p.bits = a.bits;
+        p.bit_words = (n + 31) / 32;
         p.cap = a.cap;
         p.work = d_work;
         p.overflow_list = d_overflow_list;
@@ -423,6 +428,17 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
     m.block = opt.block_threads ? opt.block_threads : 128;
     m.items = opt.items_per_thread ? opt.items_per_thread : 4;
     m.flags = opt.materialize_final_level ? kFlagMaterializeFinal : 0u;
+    {
+        // Visited bitmaps pay off when single rows are long enough to be probed (hub graphs); on
+        // low-degree graphs they would only add an atomic per settled vertex.
+        std::uint64_t max_degree = 0;
+        for (std::uint64_t v = 0; v < g.n; ++v)
+            max_degree = std::max<std::uint64_t>(max_degree, g.degree(v));
+        const char *env = std::getenv("EBC_BITMAP");
+        const bool want = env ? std::atoi(env) != 0 : max_degree >= 1024;
+        if (want && !opt.materialize_final_level)
+            m.flags |= kFlagUseBitmap;
+    }
     const int per_sm = occupancy_for(m.block, m.items);
     if (per_sm < 1)
         throw CudaError("sampling kernel does not fit on an SM");

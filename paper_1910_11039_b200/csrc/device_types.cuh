@@ -37,6 +37,7 @@ enum WorkCounter : int {
 constexpr u32 kClaimTop = 0xffffffffu;     // transient claim values: kClaimTop - slot_in_tile
 constexpr u32 kMaxBlockThreads = 1024;
 constexpr u32 kMaxTileSlots = 4096;        // BLOCK * ITEMS never exceeds this
+constexpr u32 kFlagUseBitmap = 2u;        // per-slot visited bitmaps are maintained and used by probe_level
 constexpr u32 kFlagMaterializeFinal = 1u; // always settle the final level (state dumps, exact V_set / F_chk)
 constexpr u32 kHdrWords = 16;              // per-slot header (u32)
 // header word indices
@@ -83,6 +84,8 @@ struct SamplerParams {
     u64 slot_base;              // first slot used by this launch
     unsigned long long *overflow_total; // persistent count of abandoned samples of this pass
     u32 flags;                  // kFlag*
+    u32 *bits;                  // [slots][2 * bit_words] visited bitmaps, bits[2*(v>>5) + side]
+    u64 bit_words;              // ceil(n / 32)
 };
 
 } // namespace ebc

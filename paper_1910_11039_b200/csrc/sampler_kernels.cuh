@@ -294,7 +294,7 @@ __device__ __forceinline__ u32 half_of(u64 both, int side) { return static_cast<
 // contact_n returns the number of contact vertices appended to `contact`.
 // ex.pending is NOT updated here (see sum_frontier_degrees).
 template <int BLOCK, int ITEMS>
-__device__ bool expand_level(const SamplerParams &p, u32 *lab, int e, SideRegs &ex, const SideRegs &ot,
+__device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e, SideRegs &ex, const SideRegs &ot,
                              u32 *contact, u32 &contact_n, BlockShared<BLOCK, ITEMS> &sh, WorkRegs &wk) {
     constexpr int TILE = BLOCK * ITEMS;
     const u32 tid = threadIdx.x;
@@ -410,6 +410,8 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, int e, SideRegs &
                         st_cg(lab + 2 * static_cast<u64>(v[k]) + e, ex.base + idx[k]);
                         st_cg(ex.list + idx[k], v[k]);
                         st_cg(ex.sig + idx[k], sig_u);
+                        if (bits)
+                            atomicOr(bits + 2 * static_cast<u64>(v[k] >> 5) + e, 1u << (v[k] & 31));
                         if (is_contact[k]) {
                             atomicMin(&sh.min_contact, other_idx[k]);
                             any_contact_local = true;
@@ -498,6 +500,8 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, int e, SideRegs &
                             st_cg(lab + 2 * static_cast<u64>(v[k]) + e, ex.base + idx[k]);
                             st_cg(ex.list + idx[k], v[k]);
                             st_cg(ex.sig + idx[k], static_cast<u64>(0));
+                            if (bits)
+                                atomicOr(bits + 2 * static_cast<u64>(v[k] >> 5) + e, 1u << (v[k] & 31));
                             if (is_contact[k]) {
                                 atomicMin(&sh.min_contact, other_idx[k]);
                                 any_contact_local = true;
@@ -576,7 +580,7 @@ __device__ __forceinline__ u64 sum_frontier_degrees(const SamplerParams &p, cons
 // new_slots counts (per thread) the slots whose target is unvisited on this
 // side (= the level's E_lvl, sampler.cpp:97).
 template <int BLOCK, int ITEMS>
-__device__ u32 probe_level(const SamplerParams &p, const u32 *lab, int e, const SideRegs &ex, const SideRegs &ot,
+__device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bits, int e, const SideRegs &ex, const SideRegs &ot,
                            u32 *edges, u32 edge_cap, BlockShared<BLOCK, ITEMS> &sh, u64 &new_slots,
                            u64 &total_slots) {
     constexpr int TILE = BLOCK * ITEMS;
@@ -661,19 +665,39 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, int e, const 
                     v[k] = __ldg(p.targets + sh.c_beg[lo] + kk[k]);
                 }
             }
+            // Visit test.  With bitmaps one 8-byte word holds the visited bits of 32 consecutive vertices
+            // for both sides; rows are ascending, so a hub row streams through the bitmap instead of
+            // touching one 128-byte label line per target.
             u64 both[ITEMS];
+            if (bits) {
+                const u64 *bits64 = reinterpret_cast<const u64 *>(bits);
 #pragma unroll
-            for (int k = 0; k < ITEMS; ++k)
-                both[k] = act[k] ? ld_cg(lab64 + v[k]) : 0ull;
+                for (int k = 0; k < ITEMS; ++k)
+                    both[k] = act[k] ? ld_cg(bits64 + (v[k] >> 5)) : 0ull;
+            } else {
+#pragma unroll
+                for (int k = 0; k < ITEMS; ++k)
+                    both[k] = act[k] ? ld_cg(lab64 + v[k]) : 0ull;
+            }
 #pragma unroll
             for (int k = 0; k < ITEMS; ++k) {
                 if (!act[k])
                     continue;
-                const u32 rel = half_of(both[k], e) - ex.base;
-                if (rel < ex.cnt)
-                    continue; // visited before this level
-                new_slots += 1;
-                const u32 oi = half_of(both[k], 1 - e) - ot.base;
+                u32 oi;
+                if (bits) {
+                    if ((half_of(both[k], e) >> (v[k] & 31)) & 1u)
+                        continue; // visited before this level
+                    new_slots += 1;
+                    if (!((half_of(both[k], 1 - e) >> (v[k] & 31)) & 1u))
+                        continue; // not a contact
+                    oi = ld_cg(lab + 2 * static_cast<u64>(v[k]) + (1 - e)) - ot.base;
+                } else {
+                    const u32 rel = half_of(both[k], e) - ex.base;
+                    if (rel < ex.cnt)
+                        continue; // visited before this level
+                    new_slots += 1;
+                    oi = half_of(both[k], 1 - e) - ot.base;
+                }
                 if (oi < ot.cnt) {
                     atomicMin(&sh.min_contact, oi);
                     const u32 pos = atomicAdd(&sh.edge_cnt, 1u);
@@ -965,6 +989,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
     }
 
     u32 *lab = p.lab + slot * 2 * n; // lab[2v + side]
+    u32 *bits = (p.flags & kFlagUseBitmap) ? p.bits + slot * 2 * p.bit_words : nullptr;
     SideRegs side[2];
     for (int k = 0; k < 2; ++k) {
         side[k].list = p.list + (slot * 2 + k) * p.cap;
@@ -1039,6 +1064,8 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             side[k].pending = __ldg(p.offsets + root + 1) - __ldg(p.offsets + root);
             if (tid == 0) {
                 st_cg(lab + 2 * static_cast<u64>(root) + k, side[k].base);
+                if (bits)
+                    atomicOr(bits + 2 * static_cast<u64>(root >> 5) + k, 1u << (root & 31));
                 st_cg(side[k].list, root);
                 st_cg(side[k].sig, static_cast<u64>(1));
                 st_cg(side[k].lvl, 0u);
@@ -1075,7 +1102,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             e = side[0].pending <= side[1].pending ? 0 : 1; // tie -> forward (sampler.cpp:84)
             if (!(p.flags & kFlagMaterializeFinal) && edge_cap > 0 && side[e].pending >= kProbeMinSlots) {
                 u64 new_slots = 0, total_slots = 0;
-                edge_n = probe_level<BLOCK, ITEMS>(p, lab, e, side[e], side[1 - e], contact, edge_cap, sh, new_slots,
+                edge_n = probe_level<BLOCK, ITEMS>(p, lab, bits, e, side[e], side[1 - e], contact, edge_cap, sh, new_slots,
                                                    total_slots);
                 if (edge_n > 0 && edge_n <= edge_cap) {
                     // final level: account its scan, open the (virtual) level for the walk, stop
@@ -1093,7 +1120,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
                 }
                 __syncthreads(); // no contact (or too many contact edges): expand normally
             }
-            if (!expand_level<BLOCK, ITEMS>(p, lab, e, side[e], side[1 - e], contact, contact_n, sh, wk)) {
+            if (!expand_level<BLOCK, ITEMS>(p, lab, bits, e, side[e], side[1 - e], contact, contact_n, sh, wk)) {
                 aborted = true;
                 break;
             }
@@ -1217,6 +1244,12 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
         }
         if (p.records && tid == 0)
             p.records[local] = rec;
+        if (bits) { // clear the bitmap words of every settled vertex (both sides share the 8-byte word)
+            u64 *bits64 = reinterpret_cast<u64 *>(bits);
+            for (int k = 0; k < 2; ++k)
+                for (u32 i = tid; i < side[k].cnt; i += BLOCK)
+                    st_cg(bits64 + (ld_cg(side[k].list + i) >> 5), static_cast<u64>(0));
+        }
         for (int k = 0; k < 2; ++k) {
             last_base[k] = side[k].base;
             last_cnt[k] = side[k].cnt;
