@@ -270,6 +270,10 @@ EBC_API ebc_status ebc_sampler_frame_ptr(ebc_sampler *s, int frame, void **dev_p
 EBC_API ebc_status ebc_sampler_bfs(ebc_sampler *s, uint32_t source, uint32_t *dist_out,
                                    uint64_t out[3]);
 
+/* Device buffers of destroyed samplers / finished runs are cached per process and reused by the next
+ * run (cudaMalloc/cudaFree of ~10 GB costs more than sampling a small input); this releases them. */
+EBC_API void ebc_release_device_cache(void);
+
 /* L2 flush helper for benchmarks: writes a buffer larger than L2 on the sampler's stream. */
 EBC_API ebc_status ebc_sampler_flush_l2(ebc_sampler *s);
 

@@ -102,6 +102,7 @@ SIGNATURES = {
     "ebc_sampler_frame_ptr": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_void_p), u64p]),
     "ebc_sampler_bfs": (C.c_int, [C.c_void_p, C.c_uint32, u32p, u64p]),
     "ebc_sampler_flush_l2": (C.c_int, [C.c_void_p]),
+    "ebc_release_device_cache": (None, []),
 }
 
 _lib = None

@@ -380,9 +380,9 @@ ebc_status ebc_sampler_create(const ebc_graph *g, const ebc_run_config *cfg, ebc
         need(out, "ebc_sampler_create: null out");
         auto h = std::make_unique<ebc_sampler>();
         h->s = std::make_unique<CudaSampler>(g->g, sampler_options(cfg));
-        if (cfg && cfg->world_size > 1) {
-            if (!cfg->allreduce)
-                throw ConfigError("run config: world_size > 1 needs an allreduce hook");
+        if (cfg && cfg->world_size > 1 && !cfg->allreduce)
+            throw ConfigError("run config: world_size > 1 needs an allreduce hook");
+        if (cfg && cfg->allreduce) { // also honoured for world_size == 1 (a 1-rank communicator)
             h->allreduce = cfg->allreduce;
             h->allreduce_user = cfg->allreduce_user;
         }
@@ -538,6 +538,13 @@ ebc_status ebc_sampler_bfs(ebc_sampler *s, uint32_t source, uint32_t *dist_out, 
         out[1] = r.eccentricity;
         out[2] = r.reached;
     });
+}
+
+void ebc_release_device_cache(void) {
+    try {
+        release_device_cache();
+    } catch (...) {
+    }
 }
 
 ebc_status ebc_sampler_flush_l2(ebc_sampler *s) {

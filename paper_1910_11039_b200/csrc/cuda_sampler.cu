@@ -9,6 +9,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 
 #include "sampler_kernels.cuh"
@@ -26,11 +28,81 @@ void cuda_check(cudaError_t e, const char *what, const char *file, int line) {
 }
 #define EBC_CUDA(expr) cuda_check((expr), #expr, __FILE__, __LINE__)
 
-template <typename T> T *dev_alloc(std::uint64_t count) {
-    void *p = nullptr;
-    EBC_CUDA(cudaMalloc(&p, std::max<std::uint64_t>(count, 1) * sizeof(T)));
-    return static_cast<T *>(p);
+// Process-wide cache of device allocations.  A run allocates ~10 GB of slot state; cudaMalloc/cudaFree of
+// that size costs far more than the sampling itself on small inputs, so buffers released by one sampler
+// are kept (per device, keyed by size) and handed to the next one.  ebc_release_device_cache() frees them.
+class DevicePool {
+public:
+    void *alloc(std::size_t bytes) {
+        bytes = std::max<std::size_t>(bytes, 256);
+        int dev = 0;
+        EBC_CUDA(cudaGetDevice(&dev));
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            auto it = idle_.find({dev, bytes});
+            if (it != idle_.end()) {
+                void *p = it->second;
+                idle_.erase(it);
+                idle_bytes_ -= bytes;
+                live_[p] = {dev, bytes};
+                return p;
+            }
+        }
+        void *p = nullptr;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e == cudaErrorMemoryAllocation) { // make room and retry once
+            cudaGetLastError();
+            release_idle();
+            e = cudaMalloc(&p, bytes);
+        }
+        cuda_check(e, "cudaMalloc", __FILE__, __LINE__);
+        std::lock_guard<std::mutex> lk(mu_);
+        live_[p] = {dev, bytes};
+        return p;
+    }
+    void free(void *p) {
+        if (!p)
+            return;
+        std::lock_guard<std::mutex> lk(mu_);
+        auto it = live_.find(p);
+        if (it == live_.end()) {
+            cudaFree(p);
+            return;
+        }
+        const auto key = it->second;
+        live_.erase(it);
+        if (idle_bytes_ + key.second > kMaxIdleBytes) {
+            cudaFree(p);
+            return;
+        }
+        idle_.emplace(key, p);
+        idle_bytes_ += key.second;
+    }
+    void release_idle() {
+        std::lock_guard<std::mutex> lk(mu_);
+        for (auto &kv : idle_)
+            cudaFree(kv.second);
+        idle_.clear();
+        idle_bytes_ = 0;
+    }
+
+private:
+    static constexpr std::size_t kMaxIdleBytes = std::size_t{96} << 30;
+    std::mutex mu_;
+    std::map<void *, std::pair<int, std::size_t>> live_;
+    std::multimap<std::pair<int, std::size_t>, void *> idle_;
+    std::size_t idle_bytes_ = 0;
+};
+
+DevicePool &pool() {
+    static DevicePool *p = new DevicePool; // intentionally leaked: must outlive every sampler at exit
+    return *p;
 }
+
+template <typename T> T *dev_alloc(std::uint64_t count) {
+    return static_cast<T *>(pool().alloc(std::max<std::uint64_t>(count, 1) * sizeof(T)));
+}
+void dev_free(void *p) { pool().free(p); }
 
 // ------------------------------------------------------------------------------------
 // Frame fold + stopping check.
@@ -248,13 +320,13 @@ struct SlotArrays {
         EBC_CUDA(cudaStreamSynchronize(stream));
     }
     void release() {
-        cudaFree(lab);
-        cudaFree(list);
-        cudaFree(sig);
-        cudaFree(lvl);
-        cudaFree(contact);
-        cudaFree(bits);
-        cudaFree(hdr);
+        dev_free(lab);
+        dev_free(list);
+        dev_free(sig);
+        dev_free(lvl);
+        dev_free(contact);
+        dev_free(bits);
+        dev_free(hdr);
     }
     static u64 bytes_per_slot(u64 n, u64 cap) {
         return 2 * n * 4 + 2 * ((n + 31) / 32) * 4 + 2 * cap * (4 + 8) + 2 * (cap + 2) * 4 + 6 * cap * 4 + kHdrWords * 4;
@@ -265,6 +337,8 @@ constexpr u32 kOverflowCap = 1u << 20; // also the largest number of samples per
 constexpr int kEvents = 8;
 
 } // namespace
+
+void release_device_cache() { pool().release_idle(); }
 
 struct CudaSampler::Impl {
     int device = 0;
@@ -490,32 +564,32 @@ CudaSampler::~CudaSampler() {
     cudaDeviceSynchronize();
     m.small.release();
     m.big.release();
-    cudaFree(m.d_offsets);
-    cudaFree(m.d_targets);
+    dev_free(m.d_offsets);
+    dev_free(m.d_targets);
     for (int i = 0; i < 2; ++i) {
-        cudaFree(m.d_frame[i]);
+        dev_free(m.d_frame[i]);
         cudaFreeHost(m.h_result[i]);
         cudaEventDestroy(m.ev_sampled[i]);
         cudaEventDestroy(m.ev_folded[i]);
     }
     for (int i = 0; i < kEvents; ++i)
         cudaEventDestroy(m.ev_user[i]);
-    cudaFree(m.d_ovf_total);
-    cudaFree(m.d_S);
-    cudaFree(m.d_wide);
-    cudaFree(m.d_ticket);
-    cudaFree(m.d_work);
-    cudaFree(m.d_overflow_list);
-    cudaFree(m.d_overflow_count);
-    cudaFree(m.d_fail);
-    cudaFree(m.d_log_lower);
-    cudaFree(m.d_log_upper);
-    cudaFree(m.d_dist);
-    cudaFree(m.d_queue[0]);
-    cudaFree(m.d_queue[1]);
-    cudaFree(m.d_bfs);
-    cudaFree(m.d_best);
-    cudaFree(m.d_flush);
+    dev_free(m.d_ovf_total);
+    dev_free(m.d_S);
+    dev_free(m.d_wide);
+    dev_free(m.d_ticket);
+    dev_free(m.d_work);
+    dev_free(m.d_overflow_list);
+    dev_free(m.d_overflow_count);
+    dev_free(m.d_fail);
+    dev_free(m.d_log_lower);
+    dev_free(m.d_log_upper);
+    dev_free(m.d_dist);
+    dev_free(m.d_queue[0]);
+    dev_free(m.d_queue[1]);
+    dev_free(m.d_bfs);
+    dev_free(m.d_best);
+    dev_free(m.d_flush);
     cudaStreamDestroy(m.s_sample);
     cudaStreamDestroy(m.s_agg);
 }
@@ -572,14 +646,14 @@ void CudaSampler::sample_debug(std::uint64_t seed, std::uint32_t tag, std::uint6
         unsigned long long ovf[2];
         m.read_overflow(ovf);
     } catch (...) {
-        cudaFree(d_pairs);
-        cudaFree(d_rec);
-        cudaFree(d_paths);
+        dev_free(d_pairs);
+        dev_free(d_rec);
+        dev_free(d_paths);
         throw;
     }
-    cudaFree(d_pairs);
-    cudaFree(d_rec);
-    cudaFree(d_paths);
+    dev_free(d_pairs);
+    dev_free(d_rec);
+    dev_free(d_paths);
 }
 
 // Decodes the label / list / sigma / level arrays of the slot that ran the last

@@ -29,6 +29,9 @@ struct SampleRecordHost { // == ebc_sample_record
 
 using AllreduceFn = int (*)(void *user, void *buf, std::uint64_t count, void *cuda_stream);
 
+// Frees the device buffers cached from destroyed samplers (see DevicePool in cuda_sampler.cu).
+void release_device_cache();
+
 class CudaSampler {
 public:
     CudaSampler(const HostGraph &g, const SamplerOptions &opt);

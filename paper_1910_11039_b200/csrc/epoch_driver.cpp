@@ -33,7 +33,13 @@ void RunConfig::validate() const {
 }
 
 std::uint64_t default_epoch_samples(std::uint64_t omega) {
-    std::uint64_t b = (omega + 15) / 16;
+    // k epochs of equal size, k = clamp(round(omega / 32768), 2, 16): an epoch keeps every resident CTA
+    // busy for many samples (the tail of a launch costs about one sample time) while the adaptive rule
+    // still gets at least two chances to stop before the static budget; B is rounded up to 1024 so that
+    // k * B overshoots omega by less than k * 1024 samples.
+    std::uint64_t k = (omega + 16384) / 32768;
+    k = k < 2 ? 2 : (k > 16 ? 16 : k);
+    std::uint64_t b = (omega + k - 1) / k;
     b = (b + 1023) / 1024 * 1024;
     if (b < 1024)
         b = 1024;
@@ -51,7 +57,7 @@ RunOutput run_pipeline(const HostGraph &g, const RunConfig &cfg, SamplerBackend 
     st.n = n;
     st.m = g.m;
     const double run_start = now_s();
-    const AllreduceHook hook = cfg.world_size > 1 ? cfg.allreduce : nullptr;
+    const AllreduceHook hook = cfg.allreduce; // also honoured for world_size == 1 (a 1-rank communicator)
 
     // Phase 1: vertex-diameter bound (engine.cpp:298-311).  Deterministic, so
     // every rank computes it locally instead of receiving a broadcast.
@@ -85,7 +91,10 @@ RunOutput run_pipeline(const HostGraph &g, const RunConfig &cfg, SamplerBackend 
             be.fold_async(0, hook, cfg.allreduce_user);
             std::uint64_t tau = 0;
             be.wait_fold(0, &tau);
-            be.read_state(calib.data());
+            if (cfg.allocator == 0)
+                calib[0] = tau; // the uniform allocator uses no calibration counts (stopping.cpp:50,72-78)
+            else
+                be.read_state(calib.data());
             be.clear();
         }
         st.calibration_samples = calib[0];
@@ -150,7 +159,7 @@ RunOutput run_pipeline(const HostGraph &g, const RunConfig &cfg, SamplerBackend 
     be.read_state(words.data());
     require(words[0] == tau, "sample conservation violated: tau of S differs from the checked tau");
     out.tau_total = tau;
-    out.original_ids = g.original_ids;
+    out.original_ids.assign(g.original_ids.begin(), g.original_ids.end());
     out.counts.assign(words.begin() + 1, words.end());
     out.scores.assign(n, 0.0);
     if (tau > 0)

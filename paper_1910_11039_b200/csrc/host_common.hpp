@@ -6,7 +6,9 @@
 #include <algorithm>
 #include <cstdint>
 #include <stdexcept>
+#include <memory>
 #include <string>
+#include <utility>
 #include <vector>
 
 namespace ebc {
@@ -35,12 +37,25 @@ inline void require(bool cond, const char *what) {
 
 // Immutable undirected CSR; rows sorted ascending, symmetric, no loops or
 // duplicates (the invariants of epochbc::Graph, graph.hpp:14-20).
+// std::vector whose resize() leaves trivially constructible elements uninitialised, so large arrays
+// can be filled (and their pages first touched) by several threads instead of being zeroed by one.
+template <class T> struct DefaultInitAllocator : std::allocator<T> {
+    template <class U> struct rebind {
+        using other = DefaultInitAllocator<U>;
+    };
+    template <class U> void construct(U *p) noexcept { ::new (static_cast<void *>(p)) U; }
+    template <class U, class... Args> void construct(U *p, Args &&...args) {
+        ::new (static_cast<void *>(p)) U(std::forward<Args>(args)...);
+    }
+};
+template <class T> using RawVector = std::vector<T, DefaultInitAllocator<T>>;
+
 struct HostGraph {
     std::uint64_t n = 0;
     std::uint64_t m = 0; // undirected edges
-    std::vector<std::uint64_t> offsets; // n+1
-    std::vector<std::uint32_t> targets; // 2m
-    std::vector<std::uint64_t> original_ids; // n
+    RawVector<std::uint64_t> offsets; // n+1
+    RawVector<std::uint32_t> targets; // 2m
+    RawVector<std::uint64_t> original_ids; // n
 
     std::uint64_t degree(std::uint64_t v) const { return offsets[v + 1] - offsets[v]; }
 };

@@ -153,19 +153,27 @@ HostGraph graph_from_csr(std::uint64_t n, const std::uint64_t *offsets, const st
     require(offsets[0] == 0, "graph_from_csr: offsets[0] must be 0");
     HostGraph g;
     g.n = n;
-    g.offsets.assign(offsets, offsets + n + 1);
     const std::uint64_t arcs = offsets[n];
     require(arcs % 2 == 0, "graph_from_csr: odd arc count (graph not symmetric)");
     require(arcs == 0 || targets != nullptr, "graph_from_csr: null targets");
     g.m = arcs / 2;
-    g.targets.assign(targets, targets + arcs);
-    if (original_ids) {
-        g.original_ids.assign(original_ids, original_ids + n);
-    } else {
-        g.original_ids.resize(n);
-        for (std::uint64_t v = 0; v < n; ++v)
-            g.original_ids[v] = v;
-    }
+    // Copies run in parallel: for ~100 MB inputs the first-touch page faults of the destination dominate.
+    g.offsets.resize(n + 1);
+    g.targets.resize(arcs);
+    g.original_ids.resize(n);
+    parallel_blocks(n + 1, worker_count(n + 1, 1u << 18), [&](unsigned, std::uint64_t b, std::uint64_t e) {
+        std::memcpy(g.offsets.data() + b, offsets + b, (e - b) * 8);
+    });
+    parallel_blocks(arcs, worker_count(arcs, 1u << 19), [&](unsigned, std::uint64_t b, std::uint64_t e) {
+        std::memcpy(g.targets.data() + b, targets + b, (e - b) * 4);
+    });
+    parallel_blocks(n, worker_count(n, 1u << 18), [&](unsigned, std::uint64_t b, std::uint64_t e) {
+        if (original_ids)
+            std::memcpy(g.original_ids.data() + b, original_ids + b, (e - b) * 8);
+        else
+            for (std::uint64_t v = b; v < e; ++v)
+                g.original_ids[v] = v;
+    });
     if (validate) {
         for (std::uint64_t u = 0; u < n; ++u) {
             if (g.offsets[u + 1] < g.offsets[u])
@@ -316,7 +324,7 @@ HostGraph load_text(std::istream &in) {
     HostGraph g = graph_from_edges(ids.size(), a.data(), b.data(), a.size());
     if (g.m == 0)
         throw ParseError("edge list: graph has no edges after removing self-loops");
-    g.original_ids = std::move(ids);
+    g.original_ids.assign(ids.begin(), ids.end());
     return g;
 }
 
@@ -373,7 +381,7 @@ HostGraph load_ebcg(std::istream &in) {
         }
     }
     HostGraph g = graph_from_arc_keys(n, std::move(keys));
-    g.original_ids = std::move(ids);
+    g.original_ids.assign(ids.begin(), ids.end());
     return g;
 }
 

@@ -72,10 +72,18 @@ void calibrate(const std::uint64_t *calib, std::uint64_t n, double delta, int al
 }
 
 void bound_log_terms(const double *delta_v, std::uint64_t n, int bound, double *out) {
+    // Equal inputs give equal outputs, so the last (input, output) pair is reused: under the uniform
+    // allocator all n values are identical and this is one log() instead of n.
+    double last_in = -1.0, last_out = 0.0;
     for (std::uint64_t v = 0; v < n; ++v) {
-        if (!(delta_v[v] > 0.0 && delta_v[v] < 1.0))
-            throw ContractViolation("bound: bad per-vertex delta");
-        out[v] = bound == 0 ? std::log(1.0 / delta_v[v]) : std::log(2.0 / delta_v[v]);
+        const double d = delta_v[v];
+        if (d != last_in) {
+            if (!(d > 0.0 && d < 1.0))
+                throw ContractViolation("bound: bad per-vertex delta");
+            last_in = d;
+            last_out = bound == 0 ? std::log(1.0 / d) : std::log(2.0 / d);
+        }
+        out[v] = last_out;
     }
 }
 

