@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -561,7 +562,12 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
 
 CudaSampler::~CudaSampler() {
     Impl &m = *impl_;
+    const bool trace = std::getenv("EBC_TRACE") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     cudaDeviceSynchronize();
+    if (trace)
+        std::fprintf(stderr, "[ebc] ~CudaSampler: device sync %.3f ms\n",
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
     m.small.release();
     m.big.release();
     dev_free(m.d_offsets);
@@ -592,6 +598,9 @@ CudaSampler::~CudaSampler() {
     dev_free(m.d_flush);
     cudaStreamDestroy(m.s_sample);
     cudaStreamDestroy(m.s_agg);
+    if (trace)
+        std::fprintf(stderr, "[ebc] ~CudaSampler: total %.3f ms\n",
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
 }
 
 std::uint64_t CudaSampler::n() const { return impl_->n; }
