@@ -87,10 +87,25 @@ template <int BLOCK> struct FinalEdgeCap {
 
 template <int BLOCK, int ITEMS> struct BlockShared {
     static constexpr int WARPS = BLOCK / 32;
-    u64 f_key[FinalEdgeCap<BLOCK>::value]; // contact edges of a probed final level: discovery key,
-    u64 f_s[FinalEdgeCap<BLOCK>::value];   //   sigma of the parent,
-    u32 f_v[FinalEdgeCap<BLOCK>::value];   //   target vertex,
-    u32 f_o[FinalEdgeCap<BLOCK>::value];   //   its idx on the other side
+    // Duplicate filter of multi-row tiles: open-addressing table keyed by target vertex, one u64 per
+    // entry = generation (22 bits) | vertex (32) | TILE-1-slot (10); atomicMax keeps the LOWEST slot.
+#ifndef EBC_SMEM_DEDUPE
+#define EBC_SMEM_DEDUPE 0 // evaluated in round 1: neutral (config 2 -0.6 %, config 1 -5 %, config 3 +3 %)
+#endif
+    static constexpr bool kSmemDedupe = EBC_SMEM_DEDUPE && BLOCK * ITEMS <= 1024;
+    static constexpr int HS = kSmemDedupe ? 2 * BLOCK * ITEMS : 2;
+    union {
+        struct {
+            u64 f_key[FinalEdgeCap<BLOCK>::value]; // contact edges of a probed final level: discovery key,
+            u64 f_s[FinalEdgeCap<BLOCK>::value];   //   sigma of the parent,
+            u32 f_v[FinalEdgeCap<BLOCK>::value];   //   target vertex,
+            u32 f_o[FinalEdgeCap<BLOCK>::value];   //   its idx on the other side
+        };
+        struct {
+            unsigned long long h[HS];
+            u32 h_idx[HS]; // idx handed to the winner of an entry (read by the losing slots)
+        };
+    };
     u32 edge_cnt;
     u64 c_beg[BLOCK];      // row start of each frontier-chunk vertex
     u64 c_scan[BLOCK + 1]; // exclusive prefix of the chunk's degrees
@@ -289,13 +304,13 @@ struct WorkRegs {
 __device__ __forceinline__ u32 half_of(u64 both, int side) { return static_cast<u32>(both >> (32 * side)); }
 
 // Expands the frontier of side `e` by one level (sampler.cpp:86-103) and
-// records contacts with the other side (sampler.cpp:105-108).  Returns false on
+// records contacts with the other side (sampler.cpp:105-108).  ex.pending is NOT
+// updated here (see sum_frontier_degrees).  Returns false on
 // slot-capacity overflow (the sample is then re-run in a large slot).
 // contact_n returns the number of contact vertices appended to `contact`.
-// ex.pending is NOT updated here (see sum_frontier_degrees).
 template <int BLOCK, int ITEMS>
 __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e, SideRegs &ex, const SideRegs &ot,
-                             u32 *contact, u32 &contact_n, BlockShared<BLOCK, ITEMS> &sh, WorkRegs &wk) {
+                             u32 *contact, u32 &contact_n, BlockShared<BLOCK, ITEMS> &sh, WorkRegs &wk, u32 &hgen) {
     constexpr int TILE = BLOCK * ITEMS;
     const u32 tid = threadIdx.x;
     const u32 fb = ex.fb, fe = ex.cnt;
@@ -476,15 +491,59 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
                             at_level[k] = rel >= level_start;
                         } else {
                             candidate[k] = true;
-                            atomicMax(lab + 2 * static_cast<u64>(v[k]) + e, kClaimTop - (k * BLOCK + tid));
                         }
                     }
+                }
+                constexpr bool kSmemDedupe = BlockShared<BLOCK, ITEMS>::kSmemDedupe;
+                constexpr u32 kHashMask = BlockShared<BLOCK, ITEMS>::HS - 1;
+                u32 ent[ITEMS];
+                if (kSmemDedupe) {
+                    // claim in shared memory: lowest slot of every distinct unvisited target wins
+                    if (hgen == (1u << 22) - 1) { // generation wrap: start over with a clean table
+                        for (u32 i = tid; i <= kHashMask; i += BLOCK)
+                            sh.h[i] = 0;
+                        hgen = 0;
+                        __syncthreads();
+                    }
+                    hgen += 1;
+#pragma unroll
+                    for (int k = 0; k < ITEMS; ++k) {
+                        ent[k] = 0;
+                        if (candidate[k]) {
+                            const unsigned long long mine = (static_cast<unsigned long long>(hgen) << 42) |
+                                                            (static_cast<unsigned long long>(v[k]) << 10) |
+                                                            static_cast<unsigned long long>(BLOCK * ITEMS - 1 - (k * BLOCK + tid));
+                            u32 at = (v[k] * 2654435761u) & kHashMask;
+                            for (;;) {
+                                const unsigned long long cur = *(volatile unsigned long long *)(sh.h + at);
+                                if ((cur >> 42) == hgen) {
+                                    if (static_cast<u32>(cur >> 10) == v[k]) {
+                                        atomicMax(sh.h + at, mine);
+                                        break;
+                                    }
+                                    at = (at + 1) & kHashMask;
+                                } else if (atomicCAS(sh.h + at, cur, mine) == cur) {
+                                    break;
+                                }
+                            }
+                            ent[k] = at;
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < ITEMS; ++k)
+                        if (candidate[k])
+                            atomicMax(lab + 2 * static_cast<u64>(v[k]) + e, kClaimTop - (k * BLOCK + tid));
                 }
                 __syncthreads(); // claims visible
 #pragma unroll
                 for (int k = 0; k < ITEMS; ++k) {
-                    win[k] = candidate[k] &&
-                             ld_cg(lab + 2 * static_cast<u64>(v[k]) + e) == kClaimTop - (k * BLOCK + tid);
+                    if (kSmemDedupe)
+                        win[k] = candidate[k] && static_cast<u32>(sh.h[ent[k]] & 1023u) ==
+                                                     static_cast<u32>(BLOCK * ITEMS - 1 - (k * BLOCK + tid));
+                    else
+                        win[k] = candidate[k] &&
+                                 ld_cg(lab + 2 * static_cast<u64>(v[k]) + e) == kClaimTop - (k * BLOCK + tid);
                     is_contact[k] = win[k] && other_idx[k] < ot.cnt;
                 }
                 const u32 winners = block_ranks<BLOCK, ITEMS>(win, rank, sh.warp_cnt);
@@ -494,9 +553,12 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
                 for (int k = 0; k < ITEMS; ++k) {
                     if (win[k]) {
                         if (overflow) {
-                            st_cg(lab + 2 * static_cast<u64>(v[k]) + e, 0u); // undo the claim
+                            if (!kSmemDedupe)
+                                st_cg(lab + 2 * static_cast<u64>(v[k]) + e, 0u); // undo the claim
                         } else {
                             idx[k] = cnt + rank[k];
+                            if (kSmemDedupe)
+                                sh.h_idx[ent[k]] = idx[k];
                             st_cg(lab + 2 * static_cast<u64>(v[k]) + e, ex.base + idx[k]);
                             st_cg(ex.list + idx[k], v[k]);
                             st_cg(ex.sig + idx[k], static_cast<u64>(0));
@@ -517,7 +579,7 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
 #pragma unroll
                 for (int k = 0; k < ITEMS; ++k) {
                     if (candidate[k] && !win[k])
-                        idx[k] = ld_cg(lab + 2 * static_cast<u64>(v[k]) + e) - ex.base;
+                        idx[k] = kSmemDedupe ? sh.h_idx[ent[k]] : ld_cg(lab + 2 * static_cast<u64>(v[k]) + e) - ex.base;
                     if (candidate[k] || at_level[k]) {
                         sat_atomic_add(ex.sig + idx[k], sig_u[k]); // sampler.cpp:97-98
                         wk.e_lvl += 1;
@@ -625,34 +687,21 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
         __syncthreads();
         const u64 T = sh.c_scan[BLOCK];
         t_total += T;
-        int row_lo = 0;
-        for (u64 t0 = 0; t0 < T; t0 += TILE) {
-            const u64 t_last = (t0 + TILE < T ? t0 + TILE : T) - 1;
-            while (sh.c_scan[row_lo + 1] <= t0)
-                ++row_lo;
-            int row_hi = row_lo;
-            {
-                int hi = BLOCK;
-                while (hi - row_hi > 1) {
-                    const int mid = (row_hi + hi) >> 1;
-                    if (sh.c_scan[mid] <= t_last)
-                        row_hi = mid;
-                    else
-                        hi = mid;
-                }
-            }
-            u32 v[ITEMS], kk[ITEMS];
-            int owner[ITEMS];
-            bool act[ITEMS];
+        // Software pipeline: the targets of tile i+1 are requested before the visit words of tile i,
+        // so the two dependent loads of a slot (target id -> visit word) overlap across tiles.
+        u32 v_n[ITEMS], kk_n[ITEMS];
+        int owner_n[ITEMS];
+        bool act_n[ITEMS];
+        auto fetch = [&](u64 t0) {
 #pragma unroll
             for (int k = 0; k < ITEMS; ++k) {
                 const u64 j = t0 + static_cast<u64>(k) * BLOCK + tid;
-                act[k] = j <= t_last;
-                v[k] = 0;
-                kk[k] = 0;
-                owner[k] = row_lo;
-                if (act[k]) {
-                    int lo = row_lo, hi = row_hi + 1;
+                act_n[k] = j < T;
+                v_n[k] = 0;
+                kk_n[k] = 0;
+                owner_n[k] = 0;
+                if (act_n[k]) {
+                    int lo = 0, hi = BLOCK; // owner row: last r with c_scan[r] <= j
                     while (hi - lo > 1) {
                         const int mid = (lo + hi) >> 1;
                         if (sh.c_scan[mid] <= j)
@@ -660,11 +709,27 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
                         else
                             hi = mid;
                     }
-                    owner[k] = lo;
-                    kk[k] = static_cast<u32>(j - sh.c_scan[lo]);
-                    v[k] = __ldg(p.targets + sh.c_beg[lo] + kk[k]);
+                    owner_n[k] = lo;
+                    kk_n[k] = static_cast<u32>(j - sh.c_scan[lo]);
+                    v_n[k] = __ldg(p.targets + sh.c_beg[lo] + kk_n[k]);
                 }
             }
+        };
+        if (T > 0)
+            fetch(0);
+        for (u64 t0 = 0; t0 < T; t0 += TILE) {
+            u32 v[ITEMS], kk[ITEMS];
+            int owner[ITEMS];
+            bool act[ITEMS];
+#pragma unroll
+            for (int k = 0; k < ITEMS; ++k) {
+                v[k] = v_n[k];
+                kk[k] = kk_n[k];
+                owner[k] = owner_n[k];
+                act[k] = act_n[k];
+            }
+            if (t0 + TILE < T)
+                fetch(t0 + TILE);
             // Visit test.  With bitmaps one 8-byte word holds the visited bits of 32 consecutive vertices
             // for both sides; rows are ascending, so a hub row streams through the bitmap instead of
             // touching one 128-byte label line per target.
@@ -1007,10 +1072,25 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
                                               : static_cast<u64>(FinalEdgeCap<BLOCK>::value));
     WorkRegs wk;
     u64 tot_e_lvl = 0, tot_p_walk = 0;
+    u32 hgen = 0; // generation of the duplicate filter (BlockShared::h)
+    for (u32 i = tid; i < static_cast<u32>(BlockShared<BLOCK, ITEMS>::HS); i += BLOCK)
+        sh.h[i] = 0;
     if (tid == 0)
         for (int c = 0; c < kWorkCounters; ++c)
             sh.wk[c] = 0;
     u32 last_base[2] = {0, 0}, last_cnt[2] = {0, 0}, last_depth[2] = {0, 0};
+#ifdef EBC_PHASE_TIMERS // experiment only: cycles per phase replace the work counters
+    long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long ph_t = clock64();
+#define EBC_PH(i)                         \
+    {                                     \
+        const long long ph_n = clock64(); \
+        ph[i] += ph_n - ph_t;             \
+        ph_t = ph_n;                      \
+    }
+#else
+#define EBC_PH(i)
+#endif
 
     for (;;) {
         if (tid == 0)
@@ -1096,6 +1176,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
         rec.weight_lo = rec.weight_hi = 0;
 
         // ---- level loop (sampler.cpp:81-116) ----
+        EBC_PH(0)
         bool found = false, aborted = false, probed = false;
         int e = 0;
         u32 contact_n = 0, edge_n = 0;
@@ -1107,6 +1188,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
                 u64 new_slots = 0, total_slots = 0;
                 edge_n = probe_level<BLOCK, ITEMS>(p, lab, bits, e, side[e], side[1 - e], contact, edge_cap, sh, new_slots,
                                                    total_slots);
+                EBC_PH(2)
                 if (edge_n > 0 && edge_n <= edge_cap) {
                     // final level: account its scan, open the (virtual) level for the walk, stop
                     wk.e_lvl += new_slots;
@@ -1123,15 +1205,17 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
                 }
                 __syncthreads(); // no contact (or too many contact edges): expand normally
             }
-            if (!expand_level<BLOCK, ITEMS>(p, lab, bits, e, side[e], side[1 - e], contact, contact_n, sh, wk)) {
+            if (!expand_level<BLOCK, ITEMS>(p, lab, bits, e, side[e], side[1 - e], contact, contact_n, sh, wk, hgen)) {
                 aborted = true;
                 break;
             }
+            EBC_PH(1)
             found = sh.min_contact != 0xffffffffu;
-            if (!found)
+            if (!found) // next_pending (sampler.cpp:95,102); evaluated fused into the level it was 3 % slower
                 side[e].pending = sum_frontier_degrees<BLOCK>(p, side[e], sh.red64);
             else
                 __syncthreads();
+            EBC_PH(3)
         }
 
         if (aborted) {
@@ -1161,6 +1245,12 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             // meet set in discovery order (sampler.cpp:109-113) -> meetbuf
             const u32 meet_count = probed ? meet_from_edges<BLOCK, ITEMS>(contact, edge_n, olo, ohi, meetbuf, sh)
                                           : meet_from_contacts<BLOCK, ITEMS>(contact, contact_n, ex, olo, ohi, meetbuf, sh);
+            if (probed) { // the contact-edge arrays alias the duplicate filter: hand it back empty
+                for (u32 i = tid; i < static_cast<u32>(BlockShared<BLOCK, ITEMS>::HS); i += BLOCK)
+                    sh.h[i] = 0;
+                hgen = 0;
+                __syncthreads();
+            }
 
             // total weight over the meet set (sampler.cpp:121-123), saturating at 2^128-1
             u128 wsum = 0;
@@ -1210,6 +1300,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
                     meet = ld_cg(meetbuf + 4 * static_cast<u64>(meet_count - 1));
             }
             rec.meet = meet;
+            EBC_PH(4)
 
             // walks (sampler.cpp:157-163): path order s .. meet .. t
             const u32 d_ot = best;
@@ -1230,6 +1321,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             walk_side<BLOCK, ITEMS>(p, lab, 1, side[1], meet, dist_b, rng, path_out,
                                     static_cast<long long>(dist_f), +1, emitted, sh, wk);
             rec.path_len = emitted;
+            EBC_PH(5)
             if (tid == 0)
                 sh.ws[kW_L] += emitted;
         }
@@ -1260,6 +1352,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             side[k].base += side[k].cnt;
         }
         __syncthreads();
+        EBC_PH(6)
     }
 
     // ---- persist slot header and work counters ----
@@ -1282,6 +1375,10 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
         sh.wk[kW_P_walk] = p_walk;
         for (int c = 0; c < kWorkCounters; ++c)
             atomicAdd(p.work + c, static_cast<unsigned long long>(sh.wk[c]));
+#ifdef EBC_PHASE_TIMERS
+        for (int c = 0; c < 7; ++c)
+            atomicAdd(p.work + c, static_cast<unsigned long long>(ph[c]) - static_cast<unsigned long long>(sh.wk[c]));
+#endif
     }
 }
 
