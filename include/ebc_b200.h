@@ -180,6 +180,38 @@ EBC_API ebc_status ebc_result_original_ids(const ebc_result *r, const uint64_t *
 EBC_API ebc_status ebc_result_stats(const ebc_result *r, ebc_run_stats *stats);
 EBC_API void ebc_result_free(ebc_result *r);
 
+/* ------------------------------------------------------------ score files --- */
+/* The result / score path of the reference CLI. */
+typedef struct ebc_scores ebc_scores;
+typedef struct ebc_compare_report { /* CompareReport (score_io.hpp:31-37) */
+    double max_abs_error;
+    uint64_t vertices_above_eps;
+    double top10_overlap, top100_overlap;
+    uint64_t vertices;
+} ebc_compare_report;
+
+/* write_scores (score_io.cpp:12-21): "# key=value" lines sorted by key, then "id<TAB>%.12g". */
+EBC_API ebc_status ebc_scores_write(const char *path, const uint64_t *vertex_ids, const double *scores,
+                                    uint64_t n, const char *const *meta_keys, const char *const *meta_values,
+                                    uint64_t meta_count);
+/* scores_from_result + run_meta + write_scores as cmd_run does (tools/epochbc.cpp:179-190,219-222):
+ * header eps, delta, tau, seed, algo; one line per vertex in original-id order of the graph. */
+EBC_API ebc_status ebc_result_write_scores(const ebc_result *r, const ebc_run_config *cfg, const char *path);
+/* read_scores (score_io.cpp:23-52). */
+EBC_API ebc_status ebc_scores_read(const char *path, ebc_scores **out);
+EBC_API ebc_status ebc_scores_data(const ebc_scores *s, const uint64_t **vertex_ids, const double **scores,
+                                   uint64_t *n);
+/* Value of a "# key=value" header entry, or NULL. */
+EBC_API const char *ebc_scores_meta(const ebc_scores *s, const char *key);
+EBC_API void ebc_scores_free(ebc_scores *s);
+/* compare_scores (score_io.cpp:98-122); the reference CLI exits 1 iff max_abs_error > eps. */
+EBC_API ebc_status ebc_scores_compare(const ebc_scores *approx, const ebc_scores *exact, double eps,
+                                      ebc_compare_report *out);
+/* stats_to_json (stats.cpp:7-40): same keys in the same order; fields that have no GPU counterpart
+ * (barrier_s, transition_s, bcast_s) are 0.  Writes at most cap bytes incl. NUL; *needed = full size. */
+EBC_API ebc_status ebc_result_stats_json(const ebc_result *r, const ebc_run_config *cfg, char *buf, uint64_t cap,
+                                         uint64_t *needed);
+
 /* --------------------------------------------------------- device sampler --- */
 /* The device-resident pieces ebc_run is built from, exposed for parity tests
  * and benchmarks: replicated CSR + per-slot search state + two epoch frames +

@@ -429,6 +429,9 @@ class RefPlain:
             L.refplain_rng_draws.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, _u64p, C.c_uint64,
                                              _u64p]
             L.refplain_run.argtypes = [C.c_void_p, C.POINTER(_RunArgs), _f64p, C.POINTER(_RunStats)]
+            L.refplain_write_scores.argtypes = [C.c_char_p, _u64p, _f64p, C.c_uint64, C.POINTER(C.c_char_p),
+                                                C.POINTER(C.c_char_p), C.c_uint64]
+            L.refplain_compare_files.argtypes = [C.c_char_p, C.c_char_p, C.c_double, _f64p, _u64p]
             cls._lib = L
         return cls._lib
 
@@ -515,6 +518,26 @@ class RefPlain:
     @classmethod
     def epoch_length(cls, ranks, threads, base=1000.0, exponent=1.33):
         return int(cls.lib().refplain_epoch_length(ranks, threads, base, exponent))
+
+    @classmethod
+    def write_scores(cls, path, ids, scores, meta=None):
+        ids = _as(ids, np.uint64)
+        scores = _as(scores, np.float64)
+        meta = meta or {}
+        keys = (C.c_char_p * max(len(meta), 1))(*[str(k).encode() for k in meta])
+        vals = (C.c_char_p * max(len(meta), 1))(*[str(v).encode() for v in meta.values()])
+        if cls.lib().refplain_write_scores(path.encode(), _ptr(ids, _u64p), _ptr(scores, _f64p), len(ids), keys, vals,
+                                           len(meta)) != 0:
+            raise RuntimeError(cls.lib().refplain_last_error().decode())
+
+    @classmethod
+    def compare_files(cls, approx, exact, eps):
+        out = np.zeros(3, dtype=np.float64)
+        cnt = np.zeros(2, dtype=np.uint64)
+        if cls.lib().refplain_compare_files(approx.encode(), exact.encode(), eps, _ptr(out, _f64p), _ptr(cnt, _u64p)) != 0:
+            raise ValueError(cls.lib().refplain_last_error().decode())
+        return dict(max_abs_error=float(out[0]), top10_overlap=float(out[1]), top100_overlap=float(out[2]),
+                    vertices_above_eps=int(cnt[0]), vertices=int(cnt[1]))
 
     @classmethod
     def rng_draws(cls, master, rank, thread, bounds):

@@ -11,6 +11,7 @@
 //   * the CPU baseline timed by bench.py (cpu_baseline.kind = "reference").
 #include <cstdint>
 #include <cstring>
+#include <fstream>
 #include <vector>
 
 #include "epochbc/bfs.hpp"
@@ -20,6 +21,7 @@
 #include "epochbc/rmat.hpp"
 #include "epochbc/rng.hpp"
 #include "epochbc/sampler.hpp"
+#include "epochbc/score_io.hpp"
 #include "epochbc/stopping.hpp"
 
 using namespace epochbc;
@@ -229,6 +231,44 @@ int refplain_run(void *g, const refplain_run_args *a, double *scores_out,
         st->check_s = s.check_s;
         st->wall_s = s.wall_s;
         st->wall_ms = o.wall_ms;
+        return 0;
+    } catch (const std::exception &e) {
+        set_err(e.what());
+        return -1;
+    }
+}
+
+// write_scores (score_io.cpp:12-21) with an explicit meta map.
+int refplain_write_scores(const char *path, const std::uint64_t *ids, const double *scores, std::uint64_t n,
+                          const char *const *keys, const char *const *values, std::uint64_t meta_count) {
+    try {
+        ScoreFile f;
+        for (std::uint64_t i = 0; i < meta_count; ++i)
+            f.meta[keys[i]] = values[i];
+        f.vertex_ids.assign(ids, ids + n);
+        f.scores.assign(scores, scores + n);
+        std::ofstream out(path, std::ios::binary);
+        write_scores(out, f);
+        return out ? 0 : -1;
+    } catch (const std::exception &e) {
+        set_err(e.what());
+        return -1;
+    }
+}
+
+// read_scores + compare_scores (score_io.cpp:23-52, 98-122): out = {max_abs_error, top10, top100},
+// counts = {vertices_above_eps, vertices}.
+int refplain_compare_files(const char *approx, const char *exact, double eps, double *out, std::uint64_t *counts) {
+    try {
+        std::ifstream a(approx, std::ios::binary), b(exact, std::ios::binary);
+        if (!a || !b)
+            throw std::runtime_error("cannot open score file");
+        CompareReport r = compare_scores(read_scores(a), read_scores(b), eps);
+        out[0] = r.max_abs_error;
+        out[1] = r.top10_overlap;
+        out[2] = r.top100_overlap;
+        counts[0] = r.vertices_above_eps;
+        counts[1] = r.vertices;
         return 0;
     } catch (const std::exception &e) {
         set_err(e.what());

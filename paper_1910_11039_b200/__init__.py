@@ -7,7 +7,8 @@ from .api import (EMPIRICAL_BERNSTEIN, HOEFFDING, TAG_ADAPTIVE, TAG_CALIBRATION,
                   WORK_NAMES, ApproxResult, BackendFault, ConfigError, CudaError, Graph, ParseError,
                   RunConfig, Sampler, algorithmic_bytes, calibrate, compute_omega, diameter_upper_bound,
                   epoch_length, gen_erdos_renyi, gen_grid, gen_rmat, parse_allocator_kind,
-                  parse_bound_kind, run_pipeline, shard_range)
+                  parse_bound_kind, read_scores, run_pipeline, shard_range, write_scores,
+                  compare_score_files)
 from .build import build
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -49,6 +49,11 @@ class SampleRecord(C.Structure):
                 ("flags", C.c_uint32), ("weight_lo", C.c_uint64), ("weight_hi", C.c_uint64)]
 
 
+class CompareReport(C.Structure):
+    _fields_ = [("max_abs_error", C.c_double), ("vertices_above_eps", C.c_uint64), ("top10_overlap", C.c_double),
+                ("top100_overlap", C.c_double), ("vertices", C.c_uint64)]
+
+
 # name -> (restype, argtypes); every symbol include/ebc_b200.h declares.
 SIGNATURES = {
     "ebc_last_error": (C.c_char_p, []),
@@ -103,6 +108,15 @@ SIGNATURES = {
     "ebc_sampler_bfs": (C.c_int, [C.c_void_p, C.c_uint32, u32p, u64p]),
     "ebc_sampler_flush_l2": (C.c_int, [C.c_void_p]),
     "ebc_release_device_cache": (None, []),
+    "ebc_scores_write": (C.c_int, [C.c_char_p, u64p, f64p, C.c_uint64, C.POINTER(C.c_char_p), C.POINTER(C.c_char_p),
+                                   C.c_uint64]),
+    "ebc_result_write_scores": (C.c_int, [C.c_void_p, C.POINTER(RunConfig), C.c_char_p]),
+    "ebc_scores_read": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p)]),
+    "ebc_scores_data": (C.c_int, [C.c_void_p, C.POINTER(u64p), C.POINTER(f64p), u64p]),
+    "ebc_scores_meta": (C.c_char_p, [C.c_void_p, C.c_char_p]),
+    "ebc_scores_free": (None, [C.c_void_p]),
+    "ebc_scores_compare": (C.c_int, [C.c_void_p, C.c_void_p, C.c_double, C.POINTER(CompareReport)]),
+    "ebc_result_stats_json": (C.c_int, [C.c_void_p, C.POINTER(RunConfig), C.c_char_p, C.c_uint64, u64p]),
 }
 
 _lib = None

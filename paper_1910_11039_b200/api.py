@@ -259,15 +259,25 @@ def _stats_dict(st: _CRunStats) -> dict:
     return d
 
 
-def run_pipeline(g: Graph, cfg: RunConfig):
+def run_pipeline(g: Graph, cfg: RunConfig, scores_path: Optional[str] = None, stats_path: Optional[str] = None):
     """Full pipeline on this process' GPU (run_pipeline / run_simulated, engine.cpp:281-434).
 
-    Returns (ApproxResult, stats dict)."""
+    Returns (ApproxResult, stats dict).  scores_path / stats_path write the score file and the stats
+    JSON exactly as the reference CLI's `run` does (tools/epochbc.cpp:219-224)."""
     L = _capi.load()
     c = cfg.to_c()
     out = C.c_void_p()
     _check(L.ebc_run(g._h, C.byref(c), C.byref(out)))
     try:
+        if scores_path is not None:
+            _check(L.ebc_result_write_scores(out, C.byref(c), str(scores_path).encode()))
+        if stats_path is not None:
+            need = C.c_uint64()
+            _check(L.ebc_result_stats_json(out, C.byref(c), None, 0, C.byref(need)))
+            buf = C.create_string_buffer(need.value)
+            _check(L.ebc_result_stats_json(out, C.byref(c), buf, need.value, None))
+            with open(stats_path, "wb") as f:
+                f.write(buf.value)
         n = C.c_uint64()
         sp = _capi.f64p()
         _check(L.ebc_result_scores(out, C.byref(sp), C.byref(n)))
@@ -412,6 +422,57 @@ class Sampler:
 
     def flush_l2(self):
         _check(_capi.load().ebc_sampler_flush_l2(self._h))
+
+
+# --------------------------------------------------------------------- score files (N2)
+def write_scores(path: str, vertex_ids, scores, meta: Optional[dict] = None) -> None:
+    """write_scores (score_io.cpp:12-21)."""
+    ids = np.ascontiguousarray(vertex_ids, dtype=np.uint64)
+    sc = np.ascontiguousarray(scores, dtype=np.float64)
+    if ids.shape != sc.shape:
+        raise ConfigError("write_scores: ids and scores differ in length")
+    meta = meta or {}
+    keys = (C.c_char_p * max(len(meta), 1))(*[str(k).encode() for k in meta])
+    vals = (C.c_char_p * max(len(meta), 1))(*[str(v).encode() for v in meta.values()])
+    _check(_capi.load().ebc_scores_write(str(path).encode(), _p(ids, _capi.u64p), _p(sc, _capi.f64p), len(ids), keys,
+                                         vals, len(meta)))
+
+
+def read_scores(path: str):
+    """read_scores (score_io.cpp:23-52) -> (meta dict for the given keys is fetched lazily, ids, scores)."""
+    L = _capi.load()
+    h = C.c_void_p()
+    _check(L.ebc_scores_read(str(path).encode(), C.byref(h)))
+    try:
+        ip, sp, n = _capi.u64p(), _capi.f64p(), C.c_uint64()
+        _check(L.ebc_scores_data(h, C.byref(ip), C.byref(sp), C.byref(n)))
+        ids = np.ctypeslib.as_array(ip, shape=(n.value,)).copy() if n.value else np.zeros(0, dtype=np.uint64)
+        sc = np.ctypeslib.as_array(sp, shape=(n.value,)).copy() if n.value else np.zeros(0, dtype=np.float64)
+        meta = {}
+        for k in ("eps", "delta", "tau", "seed", "algo"):
+            v = L.ebc_scores_meta(h, k.encode())
+            if v is not None:
+                meta[k] = v.decode()
+        return meta, ids, sc
+    finally:
+        L.ebc_scores_free(h)
+
+
+def compare_score_files(approx_path: str, exact_path: str, eps: float) -> dict:
+    """compare_scores (score_io.cpp:98-122) on two score files."""
+    L = _capi.load()
+    a, b = C.c_void_p(), C.c_void_p()
+    _check(L.ebc_scores_read(str(approx_path).encode(), C.byref(a)))
+    try:
+        _check(L.ebc_scores_read(str(exact_path).encode(), C.byref(b)))
+        try:
+            rep = _capi.CompareReport()
+            _check(L.ebc_scores_compare(a, b, eps, C.byref(rep)))
+            return {k: getattr(rep, k) for k, _ in _capi.CompareReport._fields_}
+        finally:
+            L.ebc_scores_free(b)
+    finally:
+        L.ebc_scores_free(a)
 
 
 def algorithmic_bytes(work: dict) -> int:

@@ -12,6 +12,7 @@
 #include "cuda_sampler.hpp"
 #include "epoch_driver.hpp"
 #include "host_common.hpp"
+#include "host_scores.hpp"
 
 using namespace ebc;
 
@@ -21,6 +22,10 @@ struct ebc_graph {
 
 struct ebc_result {
     RunOutput out;
+};
+
+struct ebc_scores {
+    ScoreTable t;
 };
 
 struct ebc_sampler {
@@ -372,6 +377,103 @@ ebc_status ebc_result_stats(const ebc_result *r, ebc_run_stats *stats) {
 }
 
 void ebc_result_free(ebc_result *r) { delete r; }
+
+// ------------------------------------------------------------ score files ---
+ebc_status ebc_scores_write(const char *path, const uint64_t *vertex_ids, const double *scores, uint64_t n,
+                            const char *const *meta_keys, const char *const *meta_values, uint64_t meta_count) {
+    return guarded([&] {
+        need(path, "ebc_scores_write: null path");
+        if (n) {
+            need(vertex_ids, "ebc_scores_write: null ids");
+            need(scores, "ebc_scores_write: null scores");
+        }
+        ScoreTable t;
+        for (uint64_t i = 0; i < meta_count; ++i) {
+            if (!(meta_keys && meta_keys[i] && meta_values && meta_values[i]))
+                throw ContractViolation("ebc_scores_write: null meta entry");
+            t.meta[meta_keys[i]] = meta_values[i];
+        }
+        t.vertex_ids.assign(vertex_ids, vertex_ids + n);
+        t.scores.assign(scores, scores + n);
+        write_scores(path, t);
+    });
+}
+
+ebc_status ebc_result_write_scores(const ebc_result *r, const ebc_run_config *cfg, const char *path) {
+    return guarded([&] {
+        need(r, "ebc_result_write_scores: null result");
+        need(cfg, "ebc_result_write_scores: null config");
+        need(path, "ebc_result_write_scores: null path");
+        ScoreTable t;
+        t.meta = run_meta(cfg->eps, cfg->delta, cfg->seed, r->out.tau_total);
+        t.vertex_ids = r->out.original_ids;
+        t.scores = r->out.scores;
+        write_scores(path, t);
+    });
+}
+
+ebc_status ebc_scores_read(const char *path, ebc_scores **out) {
+    return guarded([&] {
+        need(path, "ebc_scores_read: null path");
+        need(out, "ebc_scores_read: null out");
+        auto h = std::make_unique<ebc_scores>();
+        h->t = read_scores(path);
+        *out = h.release();
+    });
+}
+
+ebc_status ebc_scores_data(const ebc_scores *s, const uint64_t **vertex_ids, const double **scores, uint64_t *n) {
+    return guarded([&] {
+        need(s, "ebc_scores_data: null scores");
+        if (vertex_ids)
+            *vertex_ids = s->t.vertex_ids.data();
+        if (scores)
+            *scores = s->t.scores.data();
+        if (n)
+            *n = s->t.vertex_ids.size();
+    });
+}
+
+const char *ebc_scores_meta(const ebc_scores *s, const char *key) {
+    if (!s || !key)
+        return nullptr;
+    auto it = s->t.meta.find(key);
+    return it == s->t.meta.end() ? nullptr : it->second.c_str();
+}
+
+void ebc_scores_free(ebc_scores *s) { delete s; }
+
+ebc_status ebc_scores_compare(const ebc_scores *approx, const ebc_scores *exact, double eps,
+                              ebc_compare_report *out) {
+    return guarded([&] {
+        need(approx, "ebc_scores_compare: null approx");
+        need(exact, "ebc_scores_compare: null exact");
+        need(out, "ebc_scores_compare: null out");
+        CompareReport r = compare_scores(approx->t, exact->t, eps);
+        out->max_abs_error = r.max_abs_error;
+        out->vertices_above_eps = r.vertices_above_eps;
+        out->top10_overlap = r.top10_overlap;
+        out->top100_overlap = r.top100_overlap;
+        out->vertices = r.vertices;
+    });
+}
+
+ebc_status ebc_result_stats_json(const ebc_result *r, const ebc_run_config *cfg, char *buf, uint64_t cap,
+                                 uint64_t *needed) {
+    return guarded([&] {
+        need(r, "ebc_result_stats_json: null result");
+        need(cfg, "ebc_result_stats_json: null config");
+        const std::string j = stats_json(r->out.stats, cfg->eps, cfg->delta, cfg->seed, cfg->bound, cfg->allocator,
+                                         cfg->world_size);
+        if (needed)
+            *needed = j.size() + 1;
+        if (buf && cap) {
+            const std::size_t k = std::min<std::size_t>(cap - 1, j.size());
+            std::memcpy(buf, j.data(), k);
+            buf[k] = 0;
+        }
+    });
+}
 
 // --------------------------------------------------------- device sampler ---
 ebc_status ebc_sampler_create(const ebc_graph *g, const ebc_run_config *cfg, ebc_sampler **out) {

@@ -1024,8 +1024,8 @@ __device__ void walk_side(const SamplerParams &p, const u32 *lab, int x, const S
         if (d > 0) { // sampler.cpp:152-153: endpoints are never counted
             if (tid == 0) {
                 atomicAdd(p.frame + 1 + u, 1u); // apply_sample (sampler.hpp:77)
-                if (path_out)
-                    path_out[pos] = u;
+                if (path_out && pos >= 0 && static_cast<u64>(pos) < p.path_stride)
+                    path_out[pos] = u; // longer paths are truncated to path_stride entries
             }
             pos += pos_step;
             emitted += 1;
@@ -1313,7 +1313,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             if (meet != s && meet != t) {
                 if (tid == 0) {
                     atomicAdd(p.frame + 1 + meet, 1u);
-                    if (path_out)
+                    if (path_out && static_cast<u64>(dist_f - 1) < p.path_stride)
                         path_out[dist_f - 1] = meet;
                 }
                 emitted += 1;

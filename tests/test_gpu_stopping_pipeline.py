@@ -168,3 +168,42 @@ def test_nccl_allreduce_hook_single_rank():
     finally:
         if own:
             dist.destroy_process_group()
+
+
+def test_pipeline_writes_reference_score_file_and_stats_json(tmp_path):
+    """`run` of the reference CLI writes a score file and a stats JSON (tools/epochbc.cpp:219-224)."""
+    import json
+    g, o = _graph(1500, 5000, 8)
+    cfg = ebc.RunConfig(eps=0.05, delta=0.1, seed=SEED)
+    sp, jp = str(tmp_path / "scores.tsv"), str(tmp_path / "stats.json")
+    res, st = ebc.run_pipeline(g, cfg, scores_path=sp, stats_path=jp)
+    meta, ids, scores = ebc.read_scores(sp)
+    assert meta == {"eps": "0.05", "delta": "0.1", "tau": str(res.tau_total), "seed": "7", "algo": "2"}
+    assert np.array_equal(ids, g.original_ids)
+    assert np.array_equal(scores, np.array([float("%.12g" % x) for x in res.scores]))
+    exact_path = str(tmp_path / "exact.tsv")
+    ebc.write_scores(exact_path, g.original_ids, o.brandes())
+    rep = ebc.compare_score_files(sp, exact_path, 0.05)
+    assert rep["max_abs_error"] <= 0.05 and rep["vertices_above_eps"] == 0     # the CLI's `compare` would exit 0
+    stats = json.load(open(jp), object_pairs_hook=list)
+    keys = [k for k, _ in stats]
+    assert keys == ["schema_version", "epochs", "samples", "barrier_s", "comm_mib_per_epoch", "adaptive_s", "diameter_s",
+                    "calibration_s", "transition_s", "reduce_s", "check_s", "bcast_s", "wall_s", "tau", "omega",
+                    "calibration_samples", "discarded_samples", "n0", "n", "m", "diameter_upper_bound",
+                    "vertex_diameter_bound", "eps", "delta", "ranks", "threads", "seed", "algo", "bound", "allocator"]
+    d = dict(stats)
+    assert d["tau"] == st["tau"] and d["omega"] == st["omega"] and d["bound"] == "hoeffding" and d["eps"] == 0.05
+
+
+def test_debug_paths_are_truncated_to_the_stride():
+    off, tg = grid_graph(14, 14, 0.0, 0)
+    g = ebc.Graph.from_csr(off, tg)
+    o = Oracle(off, tg)
+    s = ebc.Sampler(g, ebc.RunConfig(block_threads=32, slots=4))
+    rec, paths = s.sample_debug(SEED, 0, 300, path_stride=3)
+    for i in range(300):
+        w = o.sample(SEED, i)
+        assert int(rec[i]["path_len"]) == len(w["path"])
+        k = min(3, len(w["path"]))
+        assert np.array_equal(paths[i, :k], w["path"][:k])
+    assert np.array_equal(s.read_frame(0), o.accumulate(SEED, 0, 300))

@@ -217,3 +217,39 @@ def test_product_does_not_link_or_import_the_oracle():
             if f.endswith((".py", ".cpp", ".cu", ".cuh", ".hpp", ".h")):
                 text = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in text and "from oracle" not in text and "oracle/" not in text.replace("reference/proj/src/oracle", ""), f
+
+
+def test_score_files_round_trip_and_compare(tmp_path):
+    """write_scores / read_scores / compare_scores (score_io.cpp) behave like the reference's."""
+    rng = np.random.default_rng(3)
+    n = 400
+    ids = rng.permutation(np.arange(1000, 1000 + n)).astype(np.uint64)
+    exact = rng.random(n) ** 6
+    approx = exact + rng.normal(0, 0.003, n)
+    approx[5] += 0.05
+    pa, pe = str(tmp_path / "approx.tsv"), str(tmp_path / "exact.tsv")
+    ebc.write_scores(pa, ids, approx, {"tau": 12345, "eps": 0.01, "delta": 0.1, "seed": 7, "algo": 2})
+    ebc.write_scores(pe, ids[::-1].copy(), exact[::-1].copy())
+    text = open(pa).read().splitlines()
+    assert text[:5] == ["# algo=2", "# delta=0.1", "# eps=0.01", "# seed=7", "# tau=12345"]      # std::map key order
+    assert text[5] == "%d\t%.12g" % (int(ids[0]), approx[0])
+    meta, rid, rsc = ebc.read_scores(pa)
+    assert meta["tau"] == "12345" and np.array_equal(rid, ids)
+    assert np.array_equal(rsc, np.array([float("%.12g" % x) for x in approx]))
+    rep = ebc.compare_score_files(pa, pe, 0.01)
+    assert rep["vertices"] == n and rep["vertices_above_eps"] >= 1 and rep["max_abs_error"] > 0.04
+    assert 0.0 <= rep["top10_overlap"] <= 1.0 and 0.0 <= rep["top100_overlap"] <= 1.0
+    with pytest.raises(ebc.ConfigError, match="vertex sets differ"):
+        ebc.write_scores(str(tmp_path / "other.tsv"), ids + 1, exact)
+        ebc.compare_score_files(pa, str(tmp_path / "other.tsv"), 0.01)
+    (tmp_path / "bad.tsv").write_text("# a=b\n12 x\n")
+    with pytest.raises(ebc.ParseError, match="malformed line 2"):
+        ebc.read_scores(str(tmp_path / "bad.tsv"))
+    if oracle.have_ref():
+        from oracle import RefPlain
+        pr = str(tmp_path / "ref.tsv")
+        RefPlain.write_scores(pr, ids, approx, {"tau": 12345, "eps": 0.01, "delta": 0.1, "seed": 7, "algo": 2})
+        assert open(pr, "rb").read() == open(pa, "rb").read()                                       # byte-identical files
+        want = RefPlain.compare_files(pa, pe, 0.01)
+        for k, v in want.items():
+            assert rep[k] == v, k
