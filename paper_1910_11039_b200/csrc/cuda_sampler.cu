@@ -79,6 +79,10 @@ public:
         idle_.emplace(key, p);
         idle_bytes_ += key.second;
     }
+    std::size_t idle_bytes() {
+        std::lock_guard<std::mutex> lk(mu_);
+        return idle_bytes_;
+    }
     void release_idle() {
         std::lock_guard<std::mutex> lk(mu_);
         for (auto &kv : idle_)
@@ -336,6 +340,7 @@ struct SlotArrays {
 
 constexpr u32 kOverflowCap = 1u << 20; // also the largest number of samples per launch
 constexpr int kEvents = 8;
+constexpr u64 kLargeSlots = 8; // full-capacity slots of the re-run pass
 
 } // namespace
 
@@ -354,15 +359,20 @@ struct CudaSampler::Impl {
     u32 *d_frame[2] = {nullptr, nullptr};
     u64 *d_S = nullptr;
     u64 *d_wide = nullptr; // scratch for read_frame
-    unsigned long long *d_ticket = nullptr; // [2]: main pass, re-run pass
+    unsigned long long *d_ticket = nullptr; // [lane][2]: main pass, re-run pass
+    u32 *d_ring = nullptr;                  // free slots (see acquire_slot in sampler_kernels.cuh)
+    unsigned long long *d_ring_pos = nullptr; // {head, tail}
     unsigned long long *d_work = nullptr;
-    u32 *d_overflow_list = nullptr, *d_overflow_count = nullptr; // count[0] main, count[1] re-run
+    u32 *d_overflow_list = nullptr, *d_overflow_count = nullptr; // per lane: list[kOverflowCap], count{main, re-run}
     u32 *d_fail = nullptr;
     double *d_log_lower = nullptr, *d_log_upper = nullptr;
     StopParams stop{};
     u64 *h_result[2] = {nullptr, nullptr}; // pinned, mapped: {stop, tau} per frame
     unsigned long long *d_ovf_total = nullptr; // [2]: abandoned samples in the main / re-run pass
-    cudaStream_t s_sample = nullptr, s_agg = nullptr;
+    // Two sampling lanes (one per epoch frame): consecutive epochs run on different streams, so the CTAs
+    // of epoch e+1 start on SMs that epoch e's tail has already left; slots are handed out dynamically.
+    cudaStream_t s_sample = nullptr, s_sample2 = nullptr, s_agg = nullptr;
+    cudaEvent_t ev_rerun[2]{}, ev_lane{};
     cudaEvent_t ev_sampled[2]{}, ev_folded[2]{}, ev_user[kEvents]{};
     bool folded_pending[2] = {false, false};
     u64 overflow_seen = 0;
@@ -391,57 +401,77 @@ struct CudaSampler::Impl {
         p.bit_words = (n + 31) / 32;
         p.cap = a.cap;
         p.work = d_work;
-        p.overflow_list = d_overflow_list;
         p.overflow_cap = kOverflowCap;
         p.flags = flags;
         return p;
     }
 
-    // Launches the main pass and the re-run pass for [first, first+count), count <= kOverflowCap.
+    cudaStream_t lane_stream(int lane) const { return lane == 0 ? s_sample : s_sample2; }
+
+    // Launches the main pass and the re-run pass for [first, first+count), count <= kOverflowCap, on the
+    // sampling lane of `frame`.
     void launch(u64 seed, u32 tag, u64 first, u64 count, int frame, const u32 *d_pairs,
                 SampleRecordDev *d_records, u32 *d_paths, u64 path_stride) {
-        EBC_CUDA(cudaMemsetAsync(d_ticket, 0, 2 * sizeof(unsigned long long), s_sample));
-        EBC_CUDA(cudaMemsetAsync(d_overflow_count, 0, 2 * sizeof(u32), s_sample));
+        const int lane = frame;
+        cudaStream_t st = lane_stream(lane);
+        unsigned long long *ticket = d_ticket + 2 * lane;
+        u32 *ovf_count = d_overflow_count + 2 * lane;
+        u32 *ovf_list = d_overflow_list + static_cast<u64>(lane) * kOverflowCap;
+        EBC_CUDA(cudaMemsetAsync(ticket, 0, 2 * sizeof(unsigned long long), st));
+        EBC_CUDA(cudaMemsetAsync(ovf_count, 0, 2 * sizeof(u32), st));
         SamplerParams p = base_params(small);
         p.seed = seed;
         p.tag = tag;
         p.first = first;
         p.count = count;
-        p.ticket = d_ticket;
+        p.ticket = ticket;
         p.frame = d_frame[frame];
         p.pairs = d_pairs;
         p.records = d_records;
         p.paths = d_paths;
         p.path_stride = path_stride;
-        p.overflow_count = d_overflow_count;
+        p.overflow_list = ovf_list;
+        p.overflow_count = ovf_count;
         p.overflow_total = d_ovf_total;
+        p.ring = d_ring;
+        p.ring_size = static_cast<u32>(small.slots);
+        p.ring_pos = d_ring_pos;
         const u32 grid = static_cast<u32>(std::min<u64>(small.slots, count));
-        launch_sample_dispatch(block, items, p, grid, s_sample);
+        launch_sample_dispatch(block, items, p, grid, st);
         ++launches;
         if (small.cap < n) { // capacity overflow is impossible when cap == n
+            // the large slots are bound to blockIdx: re-run passes of the two lanes must not overlap
+            EBC_CUDA(cudaStreamWaitEvent(st, ev_rerun[1 - lane], 0));
             SamplerParams q = base_params(big);
             q.seed = seed;
             q.tag = tag;
             q.first = first;
             q.count = count;
-            q.ticket = d_ticket + 1;
+            q.ticket = ticket + 1;
             q.frame = d_frame[frame];
             q.pairs = d_pairs;
             q.records = d_records;
             q.paths = d_paths;
             q.path_stride = path_stride;
-            q.overflow_count = d_overflow_count + 1;
+            q.overflow_list = ovf_list;
+            q.overflow_count = ovf_count + 1;
             q.overflow_total = d_ovf_total + 1;
-            q.relist = d_overflow_list;
-            q.count_ptr = d_overflow_count;
-            launch_sample_dispatch(block, items, q, static_cast<u32>(big.slots), s_sample);
+            q.relist = ovf_list;
+            q.count_ptr = ovf_count;
+            launch_sample_dispatch(block, items, q, static_cast<u32>(big.slots), st);
+            EBC_CUDA(cudaEventRecord(ev_rerun[lane], st));
             ++launches;
         }
     }
 
+    void sync_sampling() {
+        EBC_CUDA(cudaStreamSynchronize(s_sample));
+        EBC_CUDA(cudaStreamSynchronize(s_sample2));
+    }
+
     // Synchronises the sampling stream and returns {abandoned in small slots, abandoned in large slots}.
     void read_overflow(unsigned long long out[2]) {
-        EBC_CUDA(cudaStreamSynchronize(s_sample));
+        sync_sampling();
         EBC_CUDA(cudaMemcpy(out, d_ovf_total, 16, cudaMemcpyDeviceToHost));
         if (out[1] != 0)
             throw CudaError("internal: capacity overflow in a full-capacity slot");
@@ -483,11 +513,14 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
     m.arcs = g.targets.size();
 
     EBC_CUDA(cudaStreamCreateWithFlags(&m.s_sample, cudaStreamNonBlocking));
+    EBC_CUDA(cudaStreamCreateWithFlags(&m.s_sample2, cudaStreamNonBlocking));
     EBC_CUDA(cudaStreamCreateWithFlags(&m.s_agg, cudaStreamNonBlocking));
     for (int i = 0; i < 2; ++i) {
         EBC_CUDA(cudaEventCreateWithFlags(&m.ev_sampled[i], cudaEventDisableTiming));
         EBC_CUDA(cudaEventCreateWithFlags(&m.ev_folded[i], cudaEventDisableTiming));
+        EBC_CUDA(cudaEventCreateWithFlags(&m.ev_rerun[i], cudaEventDisableTiming));
     }
+    EBC_CUDA(cudaEventCreateWithFlags(&m.ev_lane, cudaEventDisableTiming));
     for (int i = 0; i < kEvents; ++i)
         EBC_CUDA(cudaEventCreate(&m.ev_user[i]));
 
@@ -519,13 +552,18 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
         throw CudaError("sampling kernel does not fit on an SM");
     u64 cap = opt.slot_capacity ? std::min<u64>(opt.slot_capacity, g.n)
                                 : std::min<u64>(g.n, std::max<u64>(u64{1} << 17, g.n / 4));
+    // (n/4 is not generous: on R-MAT graphs about 1 % of the samples settle more than n/6 vertices on one
+    // side -- a non-final level behind a hub -- and n/6 already costs 10x throughput through the re-run
+    // path; measured in profiles/r01_capacity_sweep.txt.)
     cap = std::max<u64>(cap, 2);
     u64 slots = opt.slots ? opt.slots : static_cast<u64>(per_sm) * m.sm_count;
     size_t free_b = 0, total_b = 0;
     EBC_CUDA(cudaMemGetInfo(&free_b, &total_b));
     const u64 fixed = (g.n + 1) * (4 * 2 + 8 + 8 + 16 + 12) + (u64{256} << 20) + kOverflowCap * 4 +
-                      (cap < g.n ? 2 * SlotArrays::bytes_per_slot(g.n, g.n) : 0);
-    const u64 budget = static_cast<u64>(free_b) > fixed ? (static_cast<u64>(free_b) - fixed) / 10 * 8 : 0;
+                      (cap < g.n ? kLargeSlots * SlotArrays::bytes_per_slot(g.n, g.n) : 0);
+    // Buffers cached by the pool are reusable (or released on demand), so they count as free.
+    const u64 avail = static_cast<u64>(free_b) + pool().idle_bytes();
+    const u64 budget = avail > fixed ? (avail - fixed) / 10 * 8 : 0;
     const u64 per_slot = SlotArrays::bytes_per_slot(g.n, cap);
     if (!opt.slots && slots * per_slot > budget)
         slots = budget / per_slot;
@@ -533,7 +571,7 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
         throw CudaError("not enough device memory for a single sampling slot");
     m.small.allocate(slots, cap, g.n, m.s_sample);
     if (cap < g.n)
-        m.big.allocate(2, g.n, g.n, m.s_sample);
+        m.big.allocate(kLargeSlots, g.n, g.n, m.s_sample);
 
     // ---- frames, state, bookkeeping ----
     for (int i = 0; i < 2; ++i) {
@@ -547,11 +585,21 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
     m.d_S = dev_alloc<u64>(g.n + 1);
     m.d_wide = dev_alloc<u64>(g.n + 1);
     EBC_CUDA(cudaMemsetAsync(m.d_S, 0, (g.n + 1) * 8, m.s_sample));
-    m.d_ticket = dev_alloc<unsigned long long>(2);
+    m.d_ticket = dev_alloc<unsigned long long>(4);
+    {
+        m.d_ring = dev_alloc<u32>(m.small.slots);
+        std::vector<u32> ids(m.small.slots);
+        for (u64 i = 0; i < m.small.slots; ++i)
+            ids[i] = static_cast<u32>(i);
+        EBC_CUDA(cudaMemcpyAsync(m.d_ring, ids.data(), ids.size() * 4, cudaMemcpyHostToDevice, m.s_sample));
+        m.d_ring_pos = dev_alloc<unsigned long long>(2);
+        EBC_CUDA(cudaMemsetAsync(m.d_ring_pos, 0, 16, m.s_sample));
+        EBC_CUDA(cudaStreamSynchronize(m.s_sample)); // ids goes out of scope
+    }
     m.d_work = dev_alloc<unsigned long long>(kWorkCounters);
     EBC_CUDA(cudaMemsetAsync(m.d_work, 0, kWorkCounters * 8, m.s_sample));
-    m.d_overflow_list = dev_alloc<u32>(kOverflowCap);
-    m.d_overflow_count = dev_alloc<u32>(2);
+    m.d_overflow_list = dev_alloc<u32>(2 * static_cast<u64>(kOverflowCap));
+    m.d_overflow_count = dev_alloc<u32>(4);
     m.d_fail = dev_alloc<u32>(1);
     EBC_CUDA(cudaMemsetAsync(m.d_fail, 0, 4, m.s_sample));
     m.d_log_lower = dev_alloc<double>(g.n);
@@ -577,13 +625,17 @@ CudaSampler::~CudaSampler() {
         cudaFreeHost(m.h_result[i]);
         cudaEventDestroy(m.ev_sampled[i]);
         cudaEventDestroy(m.ev_folded[i]);
+        cudaEventDestroy(m.ev_rerun[i]);
     }
+    cudaEventDestroy(m.ev_lane);
     for (int i = 0; i < kEvents; ++i)
         cudaEventDestroy(m.ev_user[i]);
     dev_free(m.d_ovf_total);
     dev_free(m.d_S);
     dev_free(m.d_wide);
     dev_free(m.d_ticket);
+    dev_free(m.d_ring);
+    dev_free(m.d_ring_pos);
     dev_free(m.d_work);
     dev_free(m.d_overflow_list);
     dev_free(m.d_overflow_count);
@@ -597,6 +649,7 @@ CudaSampler::~CudaSampler() {
     dev_free(m.d_best);
     dev_free(m.d_flush);
     cudaStreamDestroy(m.s_sample);
+    cudaStreamDestroy(m.s_sample2);
     cudaStreamDestroy(m.s_agg);
     if (trace)
         std::fprintf(stderr, "[ebc] ~CudaSampler: total %.3f ms\n",
@@ -615,12 +668,13 @@ void CudaSampler::sample(std::uint64_t seed, std::uint32_t tag, std::uint64_t fi
     Impl &m = *impl_;
     require(frame == 0 || frame == 1, "sample: frame must be 0 or 1");
     // The frame is being reused: the fold that zeroes it must have finished (epoch.hpp:24-30).
-    EBC_CUDA(cudaStreamWaitEvent(m.s_sample, m.ev_folded[frame], 0));
+    cudaStream_t st = m.lane_stream(frame);
+    EBC_CUDA(cudaStreamWaitEvent(st, m.ev_folded[frame], 0));
     for (u64 done = 0; done < count; done += kOverflowCap) {
         const u64 chunk = std::min<u64>(kOverflowCap, count - done);
         m.launch(seed, tag, first + done, chunk, frame, nullptr, nullptr, nullptr, 0);
     }
-    EBC_CUDA(cudaEventRecord(m.ev_sampled[frame], m.s_sample));
+    EBC_CUDA(cudaEventRecord(m.ev_sampled[frame], st));
 }
 
 void CudaSampler::sample_debug(std::uint64_t seed, std::uint32_t tag, std::uint64_t first, std::uint64_t count,
@@ -634,24 +688,25 @@ void CudaSampler::sample_debug(std::uint64_t seed, std::uint32_t tag, std::uint6
     SampleRecordDev *d_rec = nullptr;
     if (count == 0)
         return;
+    cudaStream_t st = m.lane_stream(frame);
     try {
-        EBC_CUDA(cudaStreamWaitEvent(m.s_sample, m.ev_folded[frame], 0));
+        EBC_CUDA(cudaStreamWaitEvent(st, m.ev_folded[frame], 0));
         if (pairs) {
             d_pairs = dev_alloc<u32>(2 * count);
-            EBC_CUDA(cudaMemcpyAsync(d_pairs, pairs, 2 * count * 4, cudaMemcpyHostToDevice, m.s_sample));
+            EBC_CUDA(cudaMemcpyAsync(d_pairs, pairs, 2 * count * 4, cudaMemcpyHostToDevice, st));
         }
         if (records)
             d_rec = dev_alloc<SampleRecordDev>(count);
         if (paths && path_stride) {
             d_paths = dev_alloc<u32>(count * path_stride);
-            EBC_CUDA(cudaMemsetAsync(d_paths, 0xff, count * path_stride * 4, m.s_sample));
+            EBC_CUDA(cudaMemsetAsync(d_paths, 0xff, count * path_stride * 4, st));
         }
         m.launch(seed, tag, first, count, frame, d_pairs, d_rec, d_paths, d_paths ? path_stride : 0);
-        EBC_CUDA(cudaEventRecord(m.ev_sampled[frame], m.s_sample));
+        EBC_CUDA(cudaEventRecord(m.ev_sampled[frame], st));
         if (records)
-            EBC_CUDA(cudaMemcpyAsync(records, d_rec, count * sizeof(SampleRecordDev), cudaMemcpyDeviceToHost, m.s_sample));
+            EBC_CUDA(cudaMemcpyAsync(records, d_rec, count * sizeof(SampleRecordDev), cudaMemcpyDeviceToHost, st));
         if (d_paths)
-            EBC_CUDA(cudaMemcpyAsync(paths, d_paths, count * path_stride * 4, cudaMemcpyDeviceToHost, m.s_sample));
+            EBC_CUDA(cudaMemcpyAsync(paths, d_paths, count * path_stride * 4, cudaMemcpyDeviceToHost, st));
         unsigned long long ovf[2];
         m.read_overflow(ovf);
     } catch (...) {
@@ -757,7 +812,7 @@ void CudaSampler::discard_frame(int frame) {
 void CudaSampler::read_frame(int which, std::uint64_t *words_out) {
     Impl &m = *impl_;
     require(which >= 0 && which <= 2, "read_frame: which must be 0, 1 or 2");
-    EBC_CUDA(cudaStreamSynchronize(m.s_sample));
+    m.sync_sampling();
     EBC_CUDA(cudaStreamSynchronize(m.s_agg));
     if (which == 2) {
         EBC_CUDA(cudaMemcpy(words_out, m.d_S, (m.n + 1) * 8, cudaMemcpyDeviceToHost));
@@ -771,14 +826,14 @@ void CudaSampler::read_frame(int which, std::uint64_t *words_out) {
 
 void CudaSampler::write_state(const std::uint64_t *words) {
     Impl &m = *impl_;
-    EBC_CUDA(cudaStreamSynchronize(m.s_sample));
+    m.sync_sampling();
     EBC_CUDA(cudaStreamSynchronize(m.s_agg));
     EBC_CUDA(cudaMemcpy(m.d_S, words, (m.n + 1) * 8, cudaMemcpyHostToDevice));
 }
 
 void CudaSampler::clear() {
     Impl &m = *impl_;
-    EBC_CUDA(cudaStreamSynchronize(m.s_sample));
+    m.sync_sampling();
     EBC_CUDA(cudaStreamSynchronize(m.s_agg));
     for (int i = 0; i < 2; ++i)
         EBC_CUDA(cudaMemset(m.d_frame[i], 0, (m.n + 1) * 4));
@@ -787,7 +842,7 @@ void CudaSampler::clear() {
 
 void CudaSampler::work(std::uint64_t *out, bool reset) {
     Impl &m = *impl_;
-    EBC_CUDA(cudaStreamSynchronize(m.s_sample));
+    m.sync_sampling();
     EBC_CUDA(cudaMemcpy(out, m.d_work, kWorkCounters * 8, cudaMemcpyDeviceToHost));
     if (reset)
         EBC_CUDA(cudaMemset(m.d_work, 0, kWorkCounters * 8));
@@ -795,7 +850,12 @@ void CudaSampler::work(std::uint64_t *out, bool reset) {
 
 void CudaSampler::mark(int event) {
     require(event >= 0 && event < kEvents, "mark: event index out of range");
-    EBC_CUDA(cudaEventRecord(impl_->ev_user[event], impl_->s_sample));
+    // The mark completes when BOTH sampling lanes have reached this point.
+    Impl &m = *impl_;
+    EBC_CUDA(cudaEventRecord(m.ev_lane, m.s_sample2));
+    EBC_CUDA(cudaStreamWaitEvent(m.s_sample, m.ev_lane, 0));
+    EBC_CUDA(cudaEventRecord(m.ev_user[event], m.s_sample));
+    EBC_CUDA(cudaStreamWaitEvent(m.s_sample2, m.ev_user[event], 0));
 }
 
 float CudaSampler::elapsed_ms(int from, int to) {
@@ -807,7 +867,7 @@ float CudaSampler::elapsed_ms(int from, int to) {
 }
 
 void CudaSampler::sync() {
-    EBC_CUDA(cudaStreamSynchronize(impl_->s_sample));
+    impl_->sync_sampling();
     EBC_CUDA(cudaStreamSynchronize(impl_->s_agg));
 }
 

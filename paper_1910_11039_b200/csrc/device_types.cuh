@@ -86,6 +86,10 @@ struct SamplerParams {
     u32 flags;                  // kFlag*
     u32 *bits;                  // [slots][2 * bit_words] visited bitmaps, bits[2*(v>>5) + side]
     u64 bit_words;              // ceil(n / 32)
+    // dynamic slot hand-out (main pass): ring of free slot ids, ring_pos = {head, tail}; null => slot = slot_base + blockIdx.x
+    u32 *ring;
+    u32 ring_size;
+    unsigned long long *ring_pos;
 };
 
 } // namespace ebc

@@ -1048,7 +1048,23 @@ template <int BLOCK, int ITEMS>
 __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kernel(const SamplerParams p) {
     __shared__ BlockShared<BLOCK, ITEMS> sh;
     const u32 tid = threadIdx.x;
-    const u64 slot = p.slot_base + blockIdx.x;
+    // Slot hand-out.  Launches of consecutive epochs overlap on two streams, so a CTA cannot own
+    // slot blockIdx.x: it takes a free slot id from a ring (at most ring_size CTAs are resident, each
+    // holds one slot, so a free one is always there or about to be returned) and puts it back at exit.
+    u64 slot = p.slot_base + blockIdx.x;
+    if (p.ring) {
+        if (tid == 0) {
+            u32 got = 0xffffffffu;
+            while (got == 0xffffffffu) {
+                const unsigned long long h = atomicAdd(p.ring_pos, 1ull);
+                got = atomicExch(p.ring + (h % p.ring_size), 0xffffffffu);
+            }
+            __threadfence();
+            sh.bcast[2] = got;
+        }
+        __syncthreads();
+        slot = sh.bcast[2];
+    }
     const u64 n = p.n;
     u64 ticket_count = p.count;
     if (p.count_ptr) {
@@ -1063,7 +1079,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
         side[k].list = p.list + (slot * 2 + k) * p.cap;
         side[k].sig = p.sig + (slot * 2 + k) * p.cap;
         side[k].lvl = p.lvl + (slot * 2 + k) * (p.cap + 2);
-        side[k].base = p.hdr[slot * kHdrWords + kHdrBase0 + k];
+        side[k].base = ld_cg(p.hdr + slot * kHdrWords + kHdrBase0 + k); // written by another SM's CTA
     }
     u32 *contact = p.contact + slot * 6 * p.cap; // 2*cap words: contacts / contact edges
     u32 *meetbuf = contact + 2 * p.cap;          // 4*cap words: ordered meet set
@@ -1379,6 +1395,17 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
         for (int c = 0; c < 7; ++c)
             atomicAdd(p.work + c, static_cast<unsigned long long>(ph[c]) - static_cast<unsigned long long>(sh.wk[c]));
 #endif
+    }
+    if (p.ring) { // hand the slot back (its header and labels are written; make them visible first)
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            for (;;) {
+                const unsigned long long t = atomicAdd(p.ring_pos + 1, 1ull);
+                if (atomicCAS(p.ring + (t % p.ring_size), 0xffffffffu, static_cast<u32>(slot)) == 0xffffffffu)
+                    break;
+            }
+        }
     }
 }
 
