@@ -33,12 +33,11 @@ def make_allreduce_hook(group=None, on_error=None):
 
     def hook(user, buf, count, stream):
         try:
-            if dist.get_backend(group) == "nccl":
+            if stream:  # the CUDA backend always passes its aggregation stream: `buf` is device memory
                 t = torch.as_tensor(_DeviceWords(buf, count), device="cuda")
-                ext = torch.cuda.ExternalStream(stream) if stream else torch.cuda.current_stream()
-                with torch.cuda.stream(ext):
-                    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
-            else:  # host memory (CPU tests)
+                with torch.cuda.stream(torch.cuda.ExternalStream(stream)):
+                    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)  # NCCL; gloo stages through the host
+            else:  # host memory (the CPU test backend passes no stream)
                 arr = np.ctypeslib.as_array(C.cast(buf, C.POINTER(C.c_int32)), shape=(count,))
                 dist.all_reduce(torch.from_numpy(arr), op=dist.ReduceOp.SUM, group=group)
             return 0
