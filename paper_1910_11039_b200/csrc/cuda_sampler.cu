@@ -321,6 +321,13 @@ struct SlotArrays {
         std::vector<u32> h(slots * kHdrWords, 0);
         for (u64 s = 0; s < slots; ++s)
             h[s * kHdrWords + kHdrBase0] = h[s * kHdrWords + kHdrBase1] = 1; // label 0 == never visited
+        if (const char *env = std::getenv("EBC_TEST_LABEL_BASE")) { // test hook: start close to the label-space reset
+            const u32 base = static_cast<u32>(std::strtoul(env, nullptr, 0));
+            for (u64 s = 0; s < slots; ++s) {
+                h[s * kHdrWords + kHdrBase0] = base;
+                h[s * kHdrWords + kHdrBase1] = base - 7; // the two sides reset at different samples
+            }
+        }
         EBC_CUDA(cudaMemcpyAsync(hdr, h.data(), h.size() * 4, cudaMemcpyHostToDevice, stream));
         EBC_CUDA(cudaStreamSynchronize(stream));
     }

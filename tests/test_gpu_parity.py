@@ -107,11 +107,25 @@ def test_capacity_overflow_reruns_in_large_slots():
     assert s.work()["samples"] == 800
 
 
-def test_label_space_wraparound():
-    """Many samples in ONE slot of a tiny graph, enough to cross no label reset, plus a forced one."""
+def test_label_space_wraparound(monkeypatch):
+    """Labels are base + idx with base growing monotonically; when the u32 space runs out the slot's
+    labels are zeroed and base restarts.  EBC_TEST_LABEL_BASE starts the slots just below the reset
+    threshold so both sides cross it within a few samples (at different samples)."""
     off, tg = small_graphs()["grid12"]
     g = ebc.Graph.from_csr(off, tg)
     o = Oracle(off, tg)
+    n = g.num_vertices
+    # reset happens when base + cap + 1 >= 0xffffffff - 4096 - 2 (cap == n here)
+    monkeypatch.setenv("EBC_TEST_LABEL_BASE", str(0xFFFFFFFF - 4096 - 2 - n - 1 - 2000))
+    for block, slots in ((32, 1), (128, 3)):
+        s = ebc.Sampler(g, ebc.RunConfig(block_threads=block, slots=slots, materialize_final_level=True))
+        s.sample(SEED, 0, 3000)
+        assert np.array_equal(s.read_frame(0), o.accumulate(SEED, 0, 3000))
+        rec, paths = s.sample_debug(SEED, 3000, 50, frame=1, path_stride=24)
+        for i in range(50):
+            w = o.sample(SEED, 3000 + i)
+            assert int(rec[i]["dist"]) == w["dist"] and np.array_equal(paths[i, :len(w["path"])], w["path"])
+    monkeypatch.delenv("EBC_TEST_LABEL_BASE")
     s = ebc.Sampler(g, ebc.RunConfig(block_threads=32, slots=1))
     s.sample(SEED, 0, 20000)
     assert np.array_equal(s.read_frame(0), o.accumulate(SEED, 0, 20000))
