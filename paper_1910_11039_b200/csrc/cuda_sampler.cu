@@ -302,17 +302,18 @@ int occupancy_for(u32 block, u32 items) {
 struct SlotArrays {
     u32 *lab = nullptr, *list = nullptr, *lvl = nullptr, *contact = nullptr, *hdr = nullptr, *bits = nullptr;
     u64 *sig = nullptr;
-    u64 slots = 0, cap = 0;
+    u64 slots = 0, cap = 0, aux_cap = 0;
     u64 bytes = 0;
 
     void allocate(u64 slots_, u64 cap_, u64 n, cudaStream_t stream) {
         slots = slots_;
         cap = cap_;
+        aux_cap = aux_cap_of(cap_, n);
         lab = dev_alloc<u32>(slots * 2 * n);
         list = dev_alloc<u32>(slots * 2 * cap);
         sig = dev_alloc<u64>(slots * 2 * cap);
-        lvl = dev_alloc<u32>(slots * 2 * (cap + 2));
-        contact = dev_alloc<u32>(slots * 6 * cap);
+        lvl = dev_alloc<u32>(slots * 2 * (aux_cap + 2));
+        contact = dev_alloc<u32>(slots * 6 * aux_cap);
         bits = dev_alloc<u32>(slots * 2 * ((n + 31) / 32));
         EBC_CUDA(cudaMemsetAsync(bits, 0, slots * 2 * ((n + 31) / 32) * 4, stream));
         hdr = dev_alloc<u32>(slots * kHdrWords);
@@ -340,8 +341,12 @@ struct SlotArrays {
         dev_free(bits);
         dev_free(hdr);
     }
+    // Level table and contact list are far smaller than the settle lists in practice: 2^16 entries unless
+    // the slot is a full-capacity one (cap == n), which must never overflow.
+    static u64 aux_cap_of(u64 cap, u64 n) { return cap >= n ? n : std::min<u64>(cap, u64{1} << 16); }
     static u64 bytes_per_slot(u64 n, u64 cap) {
-        return 2 * n * 4 + 2 * ((n + 31) / 32) * 4 + 2 * cap * (4 + 8) + 2 * (cap + 2) * 4 + 6 * cap * 4 + kHdrWords * 4;
+        const u64 aux = aux_cap_of(cap, n);
+        return 2 * n * 4 + 2 * ((n + 31) / 32) * 4 + 2 * cap * (4 + 8) + 2 * (aux + 2) * 4 + 6 * aux * 4 + kHdrWords * 4;
     }
 };
 
@@ -407,6 +412,7 @@ struct CudaSampler::Impl {
         p.bits = a.bits;
         p.bit_words = (n + 31) / 32;
         p.cap = a.cap;
+        p.aux_cap = a.aux_cap;
         p.work = d_work;
         p.overflow_cap = kOverflowCap;
         p.flags = flags;
@@ -746,7 +752,7 @@ void CudaSampler::last_state(int side, std::uint32_t *dist_out, std::uint64_t *s
     std::vector<u64> sig(cnt);
     EBC_CUDA(cudaMemcpy(list.data(), a.list + static_cast<u64>(side) * a.cap, cnt * 4ull, cudaMemcpyDeviceToHost));
     EBC_CUDA(cudaMemcpy(sig.data(), a.sig + static_cast<u64>(side) * a.cap, cnt * 8ull, cudaMemcpyDeviceToHost));
-    EBC_CUDA(cudaMemcpy(lvl.data(), a.lvl + static_cast<u64>(side) * (a.cap + 2), (depth + 1) * 4ull, cudaMemcpyDeviceToHost));
+    EBC_CUDA(cudaMemcpy(lvl.data(), a.lvl + static_cast<u64>(side) * (a.aux_cap + 2), (depth + 1) * 4ull, cudaMemcpyDeviceToHost));
     lvl[depth + 1] = cnt;
     for (u64 v = 0; v < m.n; ++v) {
         dist_out[v] = 0xffffffffu;

@@ -58,10 +58,11 @@ struct SamplerParams {
     u32 *lab;      // [slots][2][n]
     u32 *list;     // [slots][2][cap]   settled vertices in discovery order
     u64 *sig;      // [slots][2][cap]   sigma, same indexing
-    u32 *lvl;      // [slots][2][cap+2] level start offsets into list
-    u32 *contact;  // [slots][2][cap]   (idx on expanding side, idx on other side) of contact vertices
+    u32 *lvl;      // [slots][2][aux_cap+2] level start offsets into list
+    u32 *contact;  // [slots][6*aux_cap] contacts / contact edges, then the ordered meet set
     u32 *hdr;      // [slots][kHdrWords]
-    u64 cap;
+    u64 cap;                    // settled vertices per side (list, sig)
+    u64 aux_cap;                // levels per side and contacts per sample (lvl, contact); <= cap
     // work
     u64 seed;
     u32 tag;

@@ -319,6 +319,8 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
     const u64 *lab64 = reinterpret_cast<const u64 *>(lab);
     u32 cnt = fe;
     contact_n = 0;
+    if (static_cast<u64>(next_depth) + 1 > p.aux_cap) // more levels than the slot's level table holds
+        return false;
     if (tid == 0) {
         st_cg(ex.lvl + next_depth, level_start);
         sh.min_contact = 0xffffffffu;
@@ -440,6 +442,10 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
                 if (__syncthreads_or(any_contact_local ? 1 : 0)) {
                     u32 crank[ITEMS];
                     const u32 ctot = block_ranks<BLOCK, ITEMS>(is_contact, crank, sh.warp_cnt2);
+                    if (static_cast<u64>(contact_n) + ctot > p.aux_cap) { // contact list full: re-run in a large slot
+                        ex.cnt = cnt + winners;
+                        return false;
+                    }
 #pragma unroll
                     for (int k = 0; k < ITEMS; ++k)
                         if (is_contact[k]) {
@@ -588,6 +594,10 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
                 if (any_contact) {
                     u32 crank[ITEMS];
                     const u32 ctot = block_ranks<BLOCK, ITEMS>(is_contact, crank, sh.warp_cnt2);
+                    if (static_cast<u64>(contact_n) + ctot > p.aux_cap) {
+                        ex.cnt = cnt + winners;
+                        return false;
+                    }
 #pragma unroll
                     for (int k = 0; k < ITEMS; ++k)
                         if (is_contact[k]) {
@@ -1078,13 +1088,13 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
     for (int k = 0; k < 2; ++k) {
         side[k].list = p.list + (slot * 2 + k) * p.cap;
         side[k].sig = p.sig + (slot * 2 + k) * p.cap;
-        side[k].lvl = p.lvl + (slot * 2 + k) * (p.cap + 2);
+        side[k].lvl = p.lvl + (slot * 2 + k) * (p.aux_cap + 2);
         side[k].base = ld_cg(p.hdr + slot * kHdrWords + kHdrBase0 + k); // written by another SM's CTA
     }
-    u32 *contact = p.contact + slot * 6 * p.cap; // 2*cap words: contacts / contact edges
-    u32 *meetbuf = contact + 2 * p.cap;          // 4*cap words: ordered meet set
-    const u32 edge_cap = static_cast<u32>((2 * p.cap) / 6 < static_cast<u64>(FinalEdgeCap<BLOCK>::value)
-                                              ? (2 * p.cap) / 6
+    u32 *contact = p.contact + slot * 6 * p.aux_cap; // 2*aux_cap words: contacts / contact edges
+    u32 *meetbuf = contact + 2 * p.aux_cap;          // 4*aux_cap words: ordered meet set
+    const u32 edge_cap = static_cast<u32>((2 * p.aux_cap) / 6 < static_cast<u64>(FinalEdgeCap<BLOCK>::value)
+                                              ? (2 * p.aux_cap) / 6
                                               : static_cast<u64>(FinalEdgeCap<BLOCK>::value));
     WorkRegs wk;
     u64 tot_e_lvl = 0, tot_p_walk = 0;
@@ -1200,7 +1210,8 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             if (side[0].cnt == side[0].fb || side[1].cnt == side[1].fb)
                 break; // a frontier ran empty: t unreachable, empty sample (sampler.cpp:82-83)
             e = side[0].pending <= side[1].pending ? 0 : 1; // tie -> forward (sampler.cpp:84)
-            if (!(p.flags & kFlagMaterializeFinal) && edge_cap > 0 && side[e].pending >= kProbeMinSlots) {
+            if (!(p.flags & kFlagMaterializeFinal) && edge_cap > 0 && side[e].pending >= kProbeMinSlots &&
+                static_cast<u64>(side[e].depth) + 2 <= p.aux_cap) {
                 u64 new_slots = 0, total_slots = 0;
                 edge_n = probe_level<BLOCK, ITEMS>(p, lab, bits, e, side[e], side[1 - e], contact, edge_cap, sh, new_slots,
                                                    total_slots);
