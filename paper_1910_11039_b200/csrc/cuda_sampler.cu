@@ -50,6 +50,8 @@ public:
             }
         }
         void *p = nullptr;
+        ++mallocs_;
+        malloc_bytes_ += bytes;
         cudaError_t e = cudaMalloc(&p, bytes);
         if (e == cudaErrorMemoryAllocation) { // make room and retry once
             cudaGetLastError();
@@ -73,11 +75,17 @@ public:
         const auto key = it->second;
         live_.erase(it);
         if (idle_bytes_ + key.second > kMaxIdleBytes) {
+            ++frees_;
             cudaFree(p);
             return;
         }
         idle_.emplace(key, p);
         idle_bytes_ += key.second;
+    }
+    void stats(const char *where) {
+        std::lock_guard<std::mutex> lk(mu_);
+        std::fprintf(stderr, "[ebc] pool %s: %zu cudaMalloc (%.1f MB), %zu cudaFree, idle %.1f MB in %zu buffers, live %zu\n", where,
+                     mallocs_, malloc_bytes_ / 1e6, frees_, idle_bytes_ / 1e6, idle_.size(), live_.size());
     }
     std::size_t idle_bytes() {
         std::lock_guard<std::mutex> lk(mu_);
@@ -97,6 +105,7 @@ private:
     std::map<void *, std::pair<int, std::size_t>> live_;
     std::multimap<std::pair<int, std::size_t>, void *> idle_;
     std::size_t idle_bytes_ = 0;
+    std::size_t mallocs_ = 0, malloc_bytes_ = 0, frees_ = 0;
 };
 
 DevicePool &pool() {
@@ -493,6 +502,15 @@ struct CudaSampler::Impl {
 
 CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(new Impl) {
     Impl &m = *impl_;
+    const bool trace = std::getenv("EBC_TRACE") != nullptr;
+    const auto c0 = std::chrono::steady_clock::now();
+    auto lap = [&](const char *what) {
+        if (trace) {
+            cudaDeviceSynchronize();
+            std::fprintf(stderr, "[ebc] CudaSampler ctor: %-22s at %.3f ms\n", what,
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - c0).count());
+        }
+    };
     int count = 0;
     cudaError_t e = cudaGetDeviceCount(&count);
     if (e != cudaSuccess || count == 0)
@@ -540,10 +558,12 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
     // ---- graph: replicated CSR, u64 offsets + u32 targets ----
     m.d_offsets = dev_alloc<u64>(g.n + 1);
     m.d_targets = dev_alloc<u32>(m.arcs);
+    // (a staged copy through pinned buffers was measured slower than the driver's pageable path here)
     EBC_CUDA(cudaMemcpyAsync(m.d_offsets, g.offsets.data(), (g.n + 1) * 8, cudaMemcpyHostToDevice, m.s_sample));
     if (m.arcs)
         EBC_CUDA(cudaMemcpyAsync(m.d_targets, g.targets.data(), m.arcs * 4, cudaMemcpyHostToDevice, m.s_sample));
     m.graph_bytes = (g.n + 1) * 8 + m.arcs * 4;
+    lap("graph upload");
 
     // ---- launch shape ----
     m.block = opt.block_threads ? opt.block_threads : 128;
@@ -585,6 +605,7 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
     m.small.allocate(slots, cap, g.n, m.s_sample);
     if (cap < g.n)
         m.big.allocate(kLargeSlots, g.n, g.n, m.s_sample);
+    lap("slot arrays");
 
     // ---- frames, state, bookkeeping ----
     for (int i = 0; i < 2; ++i) {
@@ -619,6 +640,9 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
     m.d_log_upper = dev_alloc<double>(g.n);
     m.stop.have = 0;
     EBC_CUDA(cudaStreamSynchronize(m.s_sample));
+    lap("frames and bookkeeping");
+    if (trace)
+        pool().stats("after ctor");
 }
 
 CudaSampler::~CudaSampler() {
@@ -664,6 +688,8 @@ CudaSampler::~CudaSampler() {
     cudaStreamDestroy(m.s_sample);
     cudaStreamDestroy(m.s_sample2);
     cudaStreamDestroy(m.s_agg);
+    if (trace)
+        pool().stats("after dtor");
     if (trace)
         std::fprintf(stderr, "[ebc] ~CudaSampler: total %.3f ms\n",
                      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());

@@ -5,6 +5,8 @@
 #include "epoch_driver.hpp"
 
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 
 #include "philox.cuh"
 
@@ -167,6 +169,9 @@ RunOutput run_pipeline(const HostGraph &g, const RunConfig &cfg, SamplerBackend 
             out.scores[v] = static_cast<double>(out.counts[v]) / static_cast<double>(tau);
     be.finish(st);
     st.wall_s = now_s() - run_start;
+    if (std::getenv("EBC_TRACE"))
+        std::fprintf(stderr, "[ebc] run_pipeline: diameter %.3f ms, calibration %.3f ms, adaptive %.3f ms, total %.3f ms\n",
+                     st.diameter_s * 1e3, st.calibration_s * 1e3, st.adaptive_s * 1e3, st.wall_s * 1e3);
     return out;
 }
 
