@@ -209,11 +209,17 @@ struct BfsState {
     u32 depth;
     u32 done;
     u64 reached;
+    // direction optimisation (Beamer et al.): a level whose frontier carries more than 1/16 of the arcs is
+    // expanded bottom-up (every unvisited vertex looks for one parent in the frontier and stops at the first)
+    u64 frontier_arcs[2]; // sum of the degrees of the frontier being built, by level parity
+    u32 bottom_up;        // mode of the level about to run
+    u32 have_queue;       // the frontier of the level about to run exists as a queue
+    u32 bu_found;         // vertices settled by the bottom-up pass of this level
 };
 
 __global__ void __launch_bounds__(256) bfs_level_kernel(const u64 *offsets, const u32 *targets, u32 *dist,
                                                         u32 *queue0, u32 *queue1, BfsState *st, u32 level) {
-    if (st->done)
+    if (st->done || st->bottom_up)
         return;
     const u32 *in = (level & 1) ? queue1 : queue0;
     u32 *out = (level & 1) ? queue0 : queue1;
@@ -221,6 +227,7 @@ __global__ void __launch_bounds__(256) bfs_level_kernel(const u64 *offsets, cons
     const u32 warps = (gridDim.x * blockDim.x) >> 5;
     const u32 warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const u32 lane = threadIdx.x & 31;
+    u64 arcs = 0;
     for (u32 i = warp; i < count; i += warps) {
         const u32 u = in[i];
         const u64 beg = offsets[u], end = offsets[u + 1];
@@ -229,23 +236,79 @@ __global__ void __launch_bounds__(256) bfs_level_kernel(const u64 *offsets, cons
             if (dist[v] == 0xffffffffu && atomicCAS(dist + v, 0xffffffffu, level + 1) == 0xffffffffu) {
                 const u32 pos = atomicAdd(&st->queue_size[(level + 1) & 1], 1u);
                 out[pos] = v;
+                arcs += offsets[v + 1] - offsets[v];
             }
         }
     }
+    for (int o = 16; o > 0; o >>= 1)
+        arcs += __shfl_xor_sync(0xffffffffu, arcs, o);
+    if (lane == 0 && arcs)
+        atomicAdd(reinterpret_cast<unsigned long long *>(&st->frontier_arcs[(level + 1) & 1]), static_cast<unsigned long long>(arcs));
 }
 
-// Runs as one thread between levels: closes level `level`, opens level + 1.
-__global__ void bfs_advance_kernel(BfsState *st, u32 level) {
+// Bottom-up level: one thread per vertex; an unvisited vertex scans its row until it meets the frontier.
+__global__ void __launch_bounds__(256) bfs_bottom_up_kernel(const u64 *offsets, const u32 *targets, u32 *dist, u64 n,
+                                                            BfsState *st, u32 level) {
+    if (st->done || !st->bottom_up)
+        return;
+    u32 found = 0;
+    u64 arcs = 0;
+    for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v < n;
+         v += static_cast<u64>(gridDim.x) * blockDim.x) {
+        if (dist[v] != 0xffffffffu)
+            continue;
+        const u64 beg = offsets[v], end = offsets[v + 1];
+        for (u64 k = beg; k < end; ++k)
+            if (dist[targets[k]] == level) {
+                dist[v] = level + 1; // only this thread writes dist[v]; readers compare with `level`
+                ++found;
+                arcs += end - beg;
+                break;
+            }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        found += __shfl_xor_sync(0xffffffffu, found, o);
+        arcs += __shfl_xor_sync(0xffffffffu, arcs, o);
+    }
+    if ((threadIdx.x & 31) == 0 && found) {
+        atomicAdd(&st->bu_found, found);
+        atomicAdd(reinterpret_cast<unsigned long long *>(&st->frontier_arcs[(level + 1) & 1]), static_cast<unsigned long long>(arcs));
+    }
+}
+
+// After a bottom-up level the next frontier exists only as dist == level + 1; a top-down level needs it
+// as a queue.
+__global__ void __launch_bounds__(256) bfs_rebuild_queue_kernel(const u32 *dist, u64 n, u32 *queue0, u32 *queue1,
+                                                                BfsState *st, u32 level) {
+    if (st->done || st->bottom_up || st->have_queue)
+        return;
+    u32 *out = (level & 1) ? queue1 : queue0;
+    for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v < n;
+         v += static_cast<u64>(gridDim.x) * blockDim.x)
+        if (dist[v] == level)
+            out[atomicAdd(&st->queue_size[level & 1], 1u)] = static_cast<u32>(v);
+}
+
+// Runs as one thread between levels: closes level `level`, opens level + 1 and picks its direction.
+__global__ void bfs_advance_kernel(BfsState *st, u32 level, u64 arcs_total, u32 allow_bottom_up) {
     if (st->done)
         return;
-    const u32 next = st->queue_size[(level + 1) & 1];
+    const u32 next = st->bottom_up ? st->bu_found : st->queue_size[(level + 1) & 1];
+    const bool next_is_queue = !st->bottom_up;
     st->queue_size[level & 1] = 0;
+    st->bu_found = 0;
+    st->frontier_arcs[level & 1] = 0;
     if (next == 0) {
         st->done = 1;
         st->depth = level;
-    } else {
-        st->reached += next;
+        return;
     }
+    st->reached += next;
+    const u64 next_arcs = st->frontier_arcs[(level + 1) & 1];
+    st->bottom_up = allow_bottom_up && next_arcs > arcs_total / 16 ? 1u : 0u;
+    st->have_queue = next_is_queue ? 1u : 0u;
+    if (!next_is_queue)
+        st->queue_size[(level + 1) & 1] = 0; // rebuilt on demand by bfs_rebuild_queue_kernel
 }
 
 // farthest = max distance, lowest id on ties (bfs.cpp:21-24): key = dist << 32 | ~v.
@@ -376,6 +439,7 @@ struct CudaSampler::Impl {
     u32 block = 128;
     u32 items = 4;
     u32 flags = 0;
+    bool hub_graph = false; // max degree >= 1024: visited bitmaps, direction-optimising BFS
     SlotArrays small, big;
     u32 *d_frame[2] = {nullptr, nullptr};
     u64 *d_S = nullptr;
@@ -576,7 +640,8 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
         for (std::uint64_t v = 0; v < g.n; ++v)
             max_degree = std::max<std::uint64_t>(max_degree, g.degree(v));
         const char *env = std::getenv("EBC_BITMAP");
-        const bool want = env ? std::atoi(env) != 0 : max_degree >= 1024;
+        m.hub_graph = max_degree >= 1024;
+        const bool want = env ? std::atoi(env) != 0 : m.hub_graph;
         if (want && !opt.materialize_final_level)
             m.flags |= kFlagUseBitmap;
     }
@@ -943,17 +1008,24 @@ BfsSummary CudaSampler::bfs(std::uint32_t source, std::uint32_t *dist_out) {
     BfsState init{};
     init.queue_size[0] = 1;
     init.reached = 1;
+    init.have_queue = 1;
     EBC_CUDA(cudaMemcpyAsync(m.d_bfs, &init, sizeof(init), cudaMemcpyHostToDevice, st));
     const u32 zero = 0;
     EBC_CUDA(cudaMemcpyAsync(m.d_dist + source, &zero, 4, cudaMemcpyHostToDevice, st));
     EBC_CUDA(cudaMemcpyAsync(m.d_queue[0], &source, 4, cudaMemcpyHostToDevice, st));
     EBC_CUDA(cudaMemsetAsync(m.d_best, 0, 8, st));
     const u32 grid = static_cast<u32>(m.sm_count) * 8;
+    const u32 allow_bu = m.hub_graph ? 1u : 0u; // low-degree graphs stay top-down (2 launches per level)
     BfsState host{};
     for (u32 level = 0;;) {
         for (int k = 0; k < 32; ++k, ++level) { // 32 levels per host round trip
+            if (allow_bu) {
+                bfs_rebuild_queue_kernel<<<grid, 256, 0, st>>>(m.d_dist, m.n, m.d_queue[0], m.d_queue[1], m.d_bfs, level);
+                bfs_bottom_up_kernel<<<grid, 256, 0, st>>>(m.d_offsets, m.d_targets, m.d_dist, m.n, m.d_bfs, level);
+                m.launches += 2;
+            }
             bfs_level_kernel<<<grid, 256, 0, st>>>(m.d_offsets, m.d_targets, m.d_dist, m.d_queue[0], m.d_queue[1], m.d_bfs, level);
-            bfs_advance_kernel<<<1, 1, 0, st>>>(m.d_bfs, level);
+            bfs_advance_kernel<<<1, 1, 0, st>>>(m.d_bfs, level, m.arcs, allow_bu);
             m.launches += 2;
         }
         EBC_CUDA(cudaGetLastError());

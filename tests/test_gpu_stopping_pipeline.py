@@ -207,3 +207,17 @@ def test_debug_paths_are_truncated_to_the_stride():
         k = min(3, len(w["path"]))
         assert np.array_equal(paths[i, :k], w["path"][:k])
     assert np.array_equal(s.read_frame(0), o.accumulate(SEED, 0, 300))
+
+
+def test_direction_optimising_bfs_on_hub_graph():
+    """max degree >= 1024 switches dense levels to bottom-up; distances / farthest vertex must not change."""
+    g = ebc.gen_rmat(15, 16, seed=5).largest_connected_component()
+    assert np.diff(g.offsets.astype(np.int64)).max() >= 1024
+    o = Oracle(g.offsets, g.targets)
+    s = ebc.Sampler(g, ebc.RunConfig(slots=1, block_threads=32))
+    for src in (0, 1, 4242, g.num_vertices - 1):
+        d, far, ecc, reached = s.bfs(src, want_dist=True)
+        od, ofar, oecc, oreached = o.bfs(src)
+        assert np.array_equal(d, od) and (far, ecc, reached) == (ofar, oecc, oreached)
+    for seed in (0, 7):
+        assert ebc.diameter_upper_bound(g, 4, seed) == o.diameter(4, seed)
