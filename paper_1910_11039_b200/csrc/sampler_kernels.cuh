@@ -75,6 +75,14 @@ __device__ __forceinline__ u128 uniform_below_u128(SampleStream &rng, u128 bound
     return uniform_below_wide(rng, bound);
 }
 
+// The slot's array addresses live in shared memory (BlockShared::sp), not in registers: the kernel
+// is compiled for 64 registers and every pointer kept live across a sample is a spill elsewhere.
+struct SidePtrs {
+    u32 *list;
+    u64 *sig;
+    u32 *lvl;
+};
+
 constexpr int kPredCache = 32;
 
 // Final-level probe (see probe_level): a level with at least kProbeMinSlots adjacency slots is first
@@ -107,6 +115,10 @@ template <int BLOCK, int ITEMS> struct BlockShared {
         };
     };
     u32 edge_cnt;
+    SidePtrs sp[2];
+    u32 last[6]; // base / cnt / depth of both sides of the last finished sample (state dumps)
+    u32 *lab, *bits, *contact, *meetbuf; // the slot's label / bitmap / contact arrays
+    SampleRecordDev rec; // record of the sample in flight (thread 0)
     u64 c_beg[BLOCK];      // row start of each frontier-chunk vertex
     u64 c_scan[BLOCK + 1]; // exclusive prefix of the chunk's degrees
     u64 c_sig[BLOCK];      // sigma of each chunk vertex
@@ -285,9 +297,7 @@ __device__ __noinline__ u32 block_first_exceeding(u128 w, u128 &running, bool &r
 // 32-byte sector therefore serves the visit test of the expanding side AND the
 // contact test against the other side.
 struct SideRegs {
-    u32 *list;
-    u64 *sig;
-    u32 *lvl;
+    const SidePtrs *pp;
     u32 base;  // label base of this sample
     u32 cnt;   // settled vertices so far
     u32 fb;    // frontier = list[fb .. cnt)
@@ -322,7 +332,7 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
     if (static_cast<u64>(next_depth) + 1 > p.aux_cap) // more levels than the slot's level table holds
         return false;
     if (tid == 0) {
-        st_cg(ex.lvl + next_depth, level_start);
+        st_cg(ex.pp->lvl + next_depth, level_start);
         sh.min_contact = 0xffffffffu;
         sh.ws[kW_V_exp] += fe - fb;
         sh.ws[kW_levels] += 1;
@@ -332,10 +342,10 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
         const u32 i = c0 + tid;
         u64 beg = 0, deg = 0, su = 0;
         if (i < fe) {
-            const u32 u = ld_cg(ex.list + i);
+            const u32 u = ld_cg(ex.pp->list + i);
             beg = __ldg(p.offsets + u);
             deg = __ldg(p.offsets + u + 1) - beg;
-            su = ld_cg(ex.sig + i);
+            su = ld_cg(ex.pp->sig + i);
         }
         u64 inc = deg;
 #pragma unroll
@@ -425,8 +435,8 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
                     if (win[k]) { // settle (sampler.cpp:93-95) and the discovering edge's sigma (sampler.cpp:98)
                         idx[k] = cnt + rank[k];
                         st_cg(lab + 2 * static_cast<u64>(v[k]) + e, ex.base + idx[k]);
-                        st_cg(ex.list + idx[k], v[k]);
-                        st_cg(ex.sig + idx[k], sig_u);
+                        st_cg(ex.pp->list + idx[k], v[k]);
+                        st_cg(ex.pp->sig + idx[k], sig_u);
                         if (bits)
                             atomicOr(bits + 2 * static_cast<u64>(v[k] >> 5) + e, 1u << (v[k] & 31));
                         if (is_contact[k]) {
@@ -435,7 +445,7 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
                         }
                         wk.e_lvl += 1;
                     } else if (at_level[k]) {
-                        sat_atomic_add(ex.sig + idx[k], sig_u);
+                        sat_atomic_add(ex.pp->sig + idx[k], sig_u);
                         wk.e_lvl += 1;
                     }
                 }
@@ -566,8 +576,8 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
                             if (kSmemDedupe)
                                 sh.h_idx[ent[k]] = idx[k];
                             st_cg(lab + 2 * static_cast<u64>(v[k]) + e, ex.base + idx[k]);
-                            st_cg(ex.list + idx[k], v[k]);
-                            st_cg(ex.sig + idx[k], static_cast<u64>(0));
+                            st_cg(ex.pp->list + idx[k], v[k]);
+                            st_cg(ex.pp->sig + idx[k], static_cast<u64>(0));
                             if (bits)
                                 atomicOr(bits + 2 * static_cast<u64>(v[k] >> 5) + e, 1u << (v[k] & 31));
                             if (is_contact[k]) {
@@ -587,7 +597,7 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
                     if (candidate[k] && !win[k])
                         idx[k] = kSmemDedupe ? sh.h_idx[ent[k]] : ld_cg(lab + 2 * static_cast<u64>(v[k]) + e) - ex.base;
                     if (candidate[k] || at_level[k]) {
-                        sat_atomic_add(ex.sig + idx[k], sig_u[k]); // sampler.cpp:97-98
+                        sat_atomic_add(ex.pp->sig + idx[k], sig_u[k]); // sampler.cpp:97-98
                         wk.e_lvl += 1;
                     }
                 }
@@ -628,7 +638,7 @@ template <int BLOCK>
 __device__ __forceinline__ u64 sum_frontier_degrees(const SamplerParams &p, const SideRegs &sd, u64 *red) {
     u64 s = 0;
     for (u32 i = sd.fb + threadIdx.x; i < sd.cnt; i += BLOCK) {
-        const u32 v = ld_cg(sd.list + i);
+        const u32 v = ld_cg(sd.pp->list + i);
         s += __ldg(p.offsets + v + 1) - __ldg(p.offsets + v);
     }
     const u64 r = block_sum_u64<BLOCK>(s, red);
@@ -668,10 +678,10 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
         const u32 i = c0 + tid;
         u64 beg = 0, deg = 0, su = 0;
         if (i < fe) {
-            const u32 u = ld_cg(ex.list + i);
+            const u32 u = ld_cg(ex.pp->list + i);
             beg = __ldg(p.offsets + u);
             deg = __ldg(p.offsets + u + 1) - beg;
-            su = ld_cg(ex.sig + i);
+            su = ld_cg(ex.pp->sig + i);
         }
         u64 inc = deg;
 #pragma unroll
@@ -888,9 +898,9 @@ __device__ u32 meet_from_contacts(const u32 *contact, u32 contact_n, const SideR
         u32 rank[1];
         const u32 tot = block_ranks<BLOCK, 1>(in, rank, sh.warp_cnt);
         if (in[0]) {
-            const u64 sg = ld_cg(ex.sig + ei);
+            const u64 sg = ld_cg(ex.pp->sig + ei);
             u32 *w = meetbuf + 4 * static_cast<u64>(count + rank[0]);
-            st_cg(w + 0, ld_cg(ex.list + ei));
+            st_cg(w + 0, ld_cg(ex.pp->list + ei));
             st_cg(w + 1, oi);
             st_cg(w + 2, static_cast<u32>(sg));
             st_cg(w + 3, static_cast<u32>(sg >> 32));
@@ -928,11 +938,11 @@ __device__ void walk_side(const SamplerParams &p, const u32 *lab, int x, const S
         if (d == 1) {
             // the only vertex at depth 0 is the root and sigma[root] == 1: total = 1, r = 0
             (void)uniform_below_u128(rng, 1);
-            chosen = ld_cg(sd.list);
+            chosen = ld_cg(sd.pp->list);
             if (tid == 0)
                 wk.p_walk += 1;
         } else {
-            const u32 lo = ld_cg(sd.lvl + (d - 1)), hi = ld_cg(sd.lvl + d);
+            const u32 lo = ld_cg(sd.pp->lvl + (d - 1)), hi = ld_cg(sd.pp->lvl + d);
             const u32 span = hi - lo;
             const u32 lab_lo = sd.base + lo;
             const u64 degu = end - beg;
@@ -944,7 +954,7 @@ __device__ void walk_side(const SamplerParams &p, const u32 *lab, int x, const S
             const bool by_level = static_cast<u64>(span) * (66 - __clzll(degu)) < degu;
             if (by_level) {
                 for (u32 i = lo + tid; i < hi; i += BLOCK) {
-                    const u32 w = ld_cg(sd.list + i);
+                    const u32 w = ld_cg(sd.pp->list + i);
                     u64 a = beg, b = end; // lower_bound of w in the row of u
                     while (a < b) {
                         const u64 mid = (a + b) >> 1;
@@ -954,7 +964,7 @@ __device__ void walk_side(const SamplerParams &p, const u32 *lab, int x, const S
                             b = mid;
                     }
                     if (a < end && __ldg(p.targets + a) == w) {
-                        const u64 sg = ld_cg(sd.sig + i);
+                        const u64 sg = ld_cg(sd.pp->sig + i);
                         total_local += sg;
                         wk.p_walk += 1;
                         const u32 slot = atomicAdd(&sh.pred_cnt, 1u);
@@ -970,7 +980,7 @@ __device__ void walk_side(const SamplerParams &p, const u32 *lab, int x, const S
                     const u32 w = __ldg(p.targets + k);
                     const u32 rel = ld_cg(lab + 2 * static_cast<u64>(w) + x) - lab_lo;
                     if (rel < span) {
-                        const u64 sg = ld_cg(sd.sig + lo + rel);
+                        const u64 sg = ld_cg(sd.pp->sig + lo + rel);
                         total_local += sg;
                         wk.p_walk += 1;
                         const u32 slot = atomicAdd(&sh.pred_cnt, 1u);
@@ -1015,7 +1025,7 @@ __device__ void walk_side(const SamplerParams &p, const u32 *lab, int x, const S
                         w = __ldg(p.targets + k);
                         const u32 rel = ld_cg(lab + 2 * static_cast<u64>(w) + x) - lab_lo;
                         if (rel < span)
-                            wv = ld_cg(sd.sig + lo + rel);
+                            wv = ld_cg(sd.pp->sig + lo + rel);
                     }
                     const u32 f = block_first_exceeding<BLOCK>(wv, running, running_ovf, r, sh.red64, &sh.found_lane);
                     if (f != BLOCK) {
@@ -1082,20 +1092,28 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
         ticket_count = listed < ticket_count ? listed : ticket_count;
     }
 
-    u32 *lab = p.lab + slot * 2 * n; // lab[2v + side]
-    u32 *bits = (p.flags & kFlagUseBitmap) ? p.bits + slot * 2 * p.bit_words : nullptr;
     SideRegs side[2];
     for (int k = 0; k < 2; ++k) {
-        side[k].list = p.list + (slot * 2 + k) * p.cap;
-        side[k].sig = p.sig + (slot * 2 + k) * p.cap;
-        side[k].lvl = p.lvl + (slot * 2 + k) * (p.aux_cap + 2);
+        if (tid == 0) {
+            if (k == 0) {
+                sh.lab = p.lab + slot * 2 * n; // lab[2v + side]
+                sh.bits = (p.flags & kFlagUseBitmap) ? p.bits + slot * 2 * p.bit_words : nullptr;
+                sh.contact = p.contact + slot * 6 * p.aux_cap; // 2*aux_cap words: contacts / contact edges
+                sh.meetbuf = sh.contact + 2 * p.aux_cap;       // 4*aux_cap words: ordered meet set
+            }
+            sh.sp[k].list = p.list + (slot * 2 + k) * p.cap;
+            sh.sp[k].sig = p.sig + (slot * 2 + k) * p.cap;
+            sh.sp[k].lvl = p.lvl + (slot * 2 + k) * (p.aux_cap + 2);
+        }
+        side[k].pp = &sh.sp[k];
         side[k].base = ld_cg(p.hdr + slot * kHdrWords + kHdrBase0 + k); // written by another SM's CTA
     }
-    u32 *contact = p.contact + slot * 6 * p.aux_cap; // 2*aux_cap words: contacts / contact edges
-    u32 *meetbuf = contact + 2 * p.aux_cap;          // 4*aux_cap words: ordered meet set
-    const u32 edge_cap = static_cast<u32>((2 * p.aux_cap) / 6 < static_cast<u64>(FinalEdgeCap<BLOCK>::value)
-                                              ? (2 * p.aux_cap) / 6
-                                              : static_cast<u64>(FinalEdgeCap<BLOCK>::value));
+    __syncthreads();
+    auto edge_cap = [&]() -> u32 { // contact edges the probe may collect (recomputed: not worth a register)
+        const u64 room = (2 * p.aux_cap) / 6;
+        return static_cast<u32>(room < static_cast<u64>(FinalEdgeCap<BLOCK>::value) ? room
+                                                                                   : static_cast<u64>(FinalEdgeCap<BLOCK>::value));
+    };
     WorkRegs wk;
     u64 tot_e_lvl = 0, tot_p_walk = 0;
     u32 hgen = 0; // generation of the duplicate filter (BlockShared::h)
@@ -1104,7 +1122,9 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
     if (tid == 0)
         for (int c = 0; c < kWorkCounters; ++c)
             sh.wk[c] = 0;
-    u32 last_base[2] = {0, 0}, last_cnt[2] = {0, 0}, last_depth[2] = {0, 0};
+    if (tid == 0)
+        for (int c = 0; c < 6; ++c)
+            sh.last[c] = 0;
 #ifdef EBC_PHASE_TIMERS // experiment only: cycles per phase replace the work counters
     long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     long long ph_t = clock64();
@@ -1137,9 +1157,9 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             if (r0 || r1) {
                 for (u64 i = tid; i < n; i += BLOCK) {
                     if (r0)
-                        st_cg(lab + 2 * i, 0u);
+                        st_cg(sh.lab + 2 * i, 0u);
                     if (r1)
-                        st_cg(lab + 2 * i + 1, 0u);
+                        st_cg(sh.lab + 2 * i + 1, 0u);
                 }
                 if (r0)
                     side[0].base = 1;
@@ -1172,12 +1192,12 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             side[k].depth = 0;
             side[k].pending = __ldg(p.offsets + root + 1) - __ldg(p.offsets + root);
             if (tid == 0) {
-                st_cg(lab + 2 * static_cast<u64>(root) + k, side[k].base);
-                if (bits)
-                    atomicOr(bits + 2 * static_cast<u64>(root >> 5) + k, 1u << (root & 31));
-                st_cg(side[k].list, root);
-                st_cg(side[k].sig, static_cast<u64>(1));
-                st_cg(side[k].lvl, 0u);
+                st_cg(sh.lab + 2 * static_cast<u64>(root) + k, side[k].base);
+                if (sh.bits)
+                    atomicOr(sh.bits + 2 * static_cast<u64>(root >> 5) + k, 1u << (root & 31));
+                st_cg(side[k].pp->list, root);
+                st_cg(side[k].pp->sig, static_cast<u64>(1));
+                st_cg(side[k].pp->lvl, 0u);
             }
         }
         if (tid == 0) {
@@ -1190,16 +1210,17 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
         wk.p_walk = 0;
         __syncthreads();
 
-        u32 *path_out = p.paths ? p.paths + local * p.path_stride : nullptr;
-        SampleRecordDev rec;
-        rec.s = s;
-        rec.t = t;
-        rec.dist = 0xffffffffu;
-        rec.meet = 0xffffffffu;
-        rec.meet_count = 0;
-        rec.path_len = 0;
-        rec.flags = 0;
-        rec.weight_lo = rec.weight_hi = 0;
+        if (tid == 0) { // the sample's record is kept in shared memory, written by thread 0 only
+            SampleRecordDev &rec = sh.rec;
+            rec.s = s;
+            rec.t = t;
+            rec.dist = 0xffffffffu;
+            rec.meet = 0xffffffffu;
+            rec.meet_count = 0;
+            rec.path_len = 0;
+            rec.flags = 0;
+            rec.weight_lo = rec.weight_hi = 0;
+        }
 
         // ---- level loop (sampler.cpp:81-116) ----
         EBC_PH(0)
@@ -1210,29 +1231,29 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             if (side[0].cnt == side[0].fb || side[1].cnt == side[1].fb)
                 break; // a frontier ran empty: t unreachable, empty sample (sampler.cpp:82-83)
             e = side[0].pending <= side[1].pending ? 0 : 1; // tie -> forward (sampler.cpp:84)
-            if (!(p.flags & kFlagMaterializeFinal) && edge_cap > 0 && side[e].pending >= kProbeMinSlots &&
+            if (!(p.flags & kFlagMaterializeFinal) && edge_cap() > 0 && side[e].pending >= kProbeMinSlots &&
                 static_cast<u64>(side[e].depth) + 2 <= p.aux_cap) {
                 u64 new_slots = 0, total_slots = 0;
-                edge_n = probe_level<BLOCK, ITEMS>(p, lab, bits, e, side[e], side[1 - e], contact, edge_cap, sh, new_slots,
+                edge_n = probe_level<BLOCK, ITEMS>(p, sh.lab, sh.bits, e, side[e], side[1 - e], sh.contact, edge_cap(), sh, new_slots,
                                                    total_slots);
                 EBC_PH(2)
-                if (edge_n > 0 && edge_n <= edge_cap) {
+                if (edge_n > 0 && edge_n <= edge_cap()) {
                     // final level: account its scan, open the (virtual) level for the walk, stop
                     wk.e_lvl += new_slots;
                     if (tid == 0) {
                         sh.ws[kW_E_bfs] += total_slots;
                         sh.ws[kW_V_exp] += side[e].cnt - side[e].fb;
                         sh.ws[kW_levels] += 1;
-                        st_cg(side[e].lvl + side[e].depth + 1, side[e].cnt);
+                        st_cg(side[e].pp->lvl + side[e].depth + 1, side[e].cnt);
                     }
                     __syncthreads();
                     probed = true;
                     found = true;
                     break;
                 }
-                __syncthreads(); // no contact (or too many contact edges): expand normally
+                __syncthreads(); // no sh.contact (or too many sh.contact edges): expand normally
             }
-            if (!expand_level<BLOCK, ITEMS>(p, lab, bits, e, side[e], side[1 - e], contact, contact_n, sh, wk, hgen)) {
+            if (!expand_level<BLOCK, ITEMS>(p, sh.lab, sh.bits, e, side[e], side[1 - e], sh.contact, contact_n, sh, wk, hgen)) {
                 aborted = true;
                 break;
             }
@@ -1246,8 +1267,8 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
         }
 
         if (aborted) {
-            rec.flags |= 1u;
             if (tid == 0) {
+                sh.rec.flags |= 1u;
                 const u32 k = atomicAdd(p.overflow_count, 1u);
                 if (k < p.overflow_cap)
                     p.overflow_list[k] = static_cast<u32>(local);
@@ -1260,19 +1281,21 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             // best = min other.dist over contacts = level of the smallest other-side idx
             const u32 min_idx = sh.min_contact;
             u32 best = ot.depth;
-            while (ld_cg(ot.lvl + best) > min_idx)
+            while (ld_cg(ot.pp->lvl + best) > min_idx)
                 --best;
-            const u32 olo = ld_cg(ot.lvl + best);
-            const u32 ohi = best == ot.depth ? ot.cnt : ld_cg(ot.lvl + best + 1);
-            rec.dist = d_ex + best;
-            if (probed)
-                rec.flags |= 2u;
+            const u32 olo = ld_cg(ot.pp->lvl + best);
+            const u32 ohi = best == ot.depth ? ot.cnt : ld_cg(ot.pp->lvl + best + 1);
+            if (tid == 0) {
+                sh.rec.dist = d_ex + best;
+                if (probed)
+                    sh.rec.flags |= 2u;
+            }
             __syncthreads();
 
-            // meet set in discovery order (sampler.cpp:109-113) -> meetbuf
-            const u32 meet_count = probed ? meet_from_edges<BLOCK, ITEMS>(contact, edge_n, olo, ohi, meetbuf, sh)
-                                          : meet_from_contacts<BLOCK, ITEMS>(contact, contact_n, ex, olo, ohi, meetbuf, sh);
-            if (probed) { // the contact-edge arrays alias the duplicate filter: hand it back empty
+            // meet set in discovery order (sampler.cpp:109-113) -> sh.meetbuf
+            const u32 meet_count = probed ? meet_from_edges<BLOCK, ITEMS>(sh.contact, edge_n, olo, ohi, sh.meetbuf, sh)
+                                          : meet_from_contacts<BLOCK, ITEMS>(sh.contact, contact_n, ex, olo, ohi, sh.meetbuf, sh);
+            if (probed) { // the sh.contact-edge arrays alias the duplicate filter: hand it back empty
                 for (u32 i = tid; i < static_cast<u32>(BlockShared<BLOCK, ITEMS>::HS); i += BLOCK)
                     sh.h[i] = 0;
                 hgen = 0;
@@ -1282,19 +1305,20 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             // total weight over the meet set (sampler.cpp:121-123), saturating at 2^128-1
             u128 wsum = 0;
             for (u32 c = tid; c < meet_count; c += BLOCK) {
-                const u32 *w = meetbuf + 4 * static_cast<u64>(c);
+                const u32 *w = sh.meetbuf + 4 * static_cast<u64>(c);
                 const u64 sg = static_cast<u64>(ld_cg(w + 2)) | (static_cast<u64>(ld_cg(w + 3)) << 32);
-                wsum += static_cast<u128>(sg) * ld_cg(ot.sig + ld_cg(w + 1));
+                wsum += static_cast<u128>(sg) * ld_cg(ot.pp->sig + ld_cg(w + 1));
             }
             u64 wlo, whi, wov;
             block_sum_u128<BLOCK>(wsum, wlo, whi, wov, sh.red64);
             __syncthreads();
             const u128 total_weight = wov ? ~static_cast<u128>(0) : ((static_cast<u128>(whi) << 64) | wlo);
-            rec.weight_lo = static_cast<u64>(total_weight);
-            rec.weight_hi = static_cast<u64>(total_weight >> 64);
-            rec.meet_count = meet_count;
-            if (tid == 0)
+            if (tid == 0) {
+                sh.rec.weight_lo = static_cast<u64>(total_weight);
+                sh.rec.weight_hi = static_cast<u64>(total_weight >> 64);
+                sh.rec.meet_count = meet_count;
                 sh.ws[kW_M] += meet_count;
+            }
 
             // pick and ordered prefix search (sampler.cpp:124-133).  pick < total_weight <=
             // sum of the weights, so a hit always exists; the reference's fall-through
@@ -1309,9 +1333,9 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
                     u128 wv = 0;
                     u32 mv = 0;
                     if (c < meet_count) {
-                        const u32 *w = meetbuf + 4 * static_cast<u64>(c);
+                        const u32 *w = sh.meetbuf + 4 * static_cast<u64>(c);
                         const u64 sg = static_cast<u64>(ld_cg(w + 2)) | (static_cast<u64>(ld_cg(w + 3)) << 32);
-                        wv = static_cast<u128>(sg) * ld_cg(ot.sig + ld_cg(w + 1));
+                        wv = static_cast<u128>(sg) * ld_cg(ot.pp->sig + ld_cg(w + 1));
                         mv = ld_cg(w);
                     }
                     const u32 f = block_first_exceeding<BLOCK>(wv, running, running_ovf, pick, sh.red64, &sh.found_lane);
@@ -1324,9 +1348,10 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
                     }
                 }
                 if (meet == 0xffffffffu)
-                    meet = ld_cg(meetbuf + 4 * static_cast<u64>(meet_count - 1));
+                    meet = ld_cg(sh.meetbuf + 4 * static_cast<u64>(meet_count - 1));
             }
-            rec.meet = meet;
+            if (tid == 0)
+                sh.rec.meet = meet;
             EBC_PH(4)
 
             // walks (sampler.cpp:157-163): path order s .. meet .. t
@@ -1335,26 +1360,28 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             const u32 dist_b = e == 0 ? d_ot : d_ex;
             u32 emitted = 0;
             // forward side: vertices at forward depth d sit at internal position d-1
-            walk_side<BLOCK, ITEMS>(p, lab, 0, side[0], meet, dist_f, rng, path_out,
+            walk_side<BLOCK, ITEMS>(p, sh.lab, 0, side[0], meet, dist_f, rng, p.paths ? p.paths + local * p.path_stride : nullptr,
                                     static_cast<long long>(dist_f) - 2, -1, emitted, sh, wk);
             if (meet != s && meet != t) {
                 if (tid == 0) {
                     atomicAdd(p.frame + 1 + meet, 1u);
-                    if (path_out && static_cast<u64>(dist_f - 1) < p.path_stride)
-                        path_out[dist_f - 1] = meet;
+                    if (p.paths && static_cast<u64>(dist_f - 1) < p.path_stride)
+                        p.paths[local * p.path_stride + (dist_f - 1)] = meet;
                 }
                 emitted += 1;
             }
-            walk_side<BLOCK, ITEMS>(p, lab, 1, side[1], meet, dist_b, rng, path_out,
+            walk_side<BLOCK, ITEMS>(p, sh.lab, 1, side[1], meet, dist_b, rng, p.paths ? p.paths + local * p.path_stride : nullptr,
                                     static_cast<long long>(dist_f), +1, emitted, sh, wk);
-            rec.path_len = emitted;
+            if (tid == 0)
+                sh.rec.path_len = emitted;
             EBC_PH(5)
             if (tid == 0)
                 sh.ws[kW_L] += emitted;
         }
 
         // ---- apply_sample: tau += 1 (sampler.hpp:75); retire the sample's labels ----
-        rec.draws = rng.draws();
+        if (tid == 0)
+            sh.rec.draws = rng.draws();
         if (!aborted) {
             tot_e_lvl += wk.e_lvl;
             tot_p_walk += wk.p_walk;
@@ -1365,17 +1392,19 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             }
         }
         if (p.records && tid == 0)
-            p.records[local] = rec;
-        if (bits) { // clear the bitmap words of every settled vertex (both sides share the 8-byte word)
-            u64 *bits64 = reinterpret_cast<u64 *>(bits);
+            p.records[local] = sh.rec;
+        if (sh.bits) { // clear the bitmap words of every settled vertex (both sides share the 8-byte word)
+            u64 *bits64 = reinterpret_cast<u64 *>(sh.bits);
             for (int k = 0; k < 2; ++k)
                 for (u32 i = tid; i < side[k].cnt; i += BLOCK)
-                    st_cg(bits64 + (ld_cg(side[k].list + i) >> 5), static_cast<u64>(0));
+                    st_cg(bits64 + (ld_cg(side[k].pp->list + i) >> 5), static_cast<u64>(0));
         }
         for (int k = 0; k < 2; ++k) {
-            last_base[k] = side[k].base;
-            last_cnt[k] = side[k].cnt;
-            last_depth[k] = side[k].depth;
+            if (tid == 0) {
+                sh.last[k] = side[k].base;
+                sh.last[2 + k] = side[k].cnt;
+                sh.last[4 + k] = side[k].depth;
+            }
             side[k].base += side[k].cnt;
         }
         __syncthreads();
@@ -1387,12 +1416,12 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
         u32 *h = p.hdr + slot * kHdrWords;
         h[kHdrBase0] = side[0].base;
         h[kHdrBase1] = side[1].base;
-        h[kHdrLastBase0] = last_base[0];
-        h[kHdrLastBase1] = last_base[1];
-        h[kHdrLastCnt0] = last_cnt[0];
-        h[kHdrLastCnt1] = last_cnt[1];
-        h[kHdrLastDepth0] = last_depth[0];
-        h[kHdrLastDepth1] = last_depth[1];
+        h[kHdrLastBase0] = sh.last[0];
+        h[kHdrLastBase1] = sh.last[1];
+        h[kHdrLastCnt0] = sh.last[2];
+        h[kHdrLastCnt1] = sh.last[3];
+        h[kHdrLastDepth0] = sh.last[4];
+        h[kHdrLastDepth1] = sh.last[5];
     }
     const u64 e_lvl = block_sum_u64<BLOCK>(tot_e_lvl, sh.red64);
     __syncthreads();
