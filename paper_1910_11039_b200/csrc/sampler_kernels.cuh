@@ -49,8 +49,14 @@ __device__ __forceinline__ u32 lanemask_lt() {
 // sigma[idx] = sat_add_u64(sigma[idx], add)  (sampler.cpp:11-13,98) with atomics:
 // a wrapped add is always followed by the same thread's atomicMax(.., 2^64-1),
 // so the value after the level barrier is 2^64-1 iff the true sum overflowed.
-__device__ __forceinline__ void sat_atomic_add(u64 *p, u64 add) {
+// `small`: the sum of sigma over the whole frontier fits 64 bits (see sum_frontier_degrees), so no
+// sum can wrap and the add needs no return value (a fire-and-forget reduction).
+__device__ __forceinline__ void sat_atomic_add(u64 *p, u64 add, bool small) {
     unsigned long long *q = reinterpret_cast<unsigned long long *>(p);
+    if (small) {
+        atomicAdd(q, static_cast<unsigned long long>(add));
+        return;
+    }
     const unsigned long long old = atomicAdd(q, static_cast<unsigned long long>(add));
     if (old + add < old)
         atomicMax(q, ~0ull);
@@ -116,6 +122,7 @@ template <int BLOCK, int ITEMS> struct BlockShared {
     };
     u32 edge_cnt;
     SidePtrs sp[2];
+    u32 sigma_small[2]; // per side: the frontier's sigma values sum to < 2^63 (no add of the next level can wrap)
     u32 last[6]; // base / cnt / depth of both sides of the last finished sample (state dumps)
     u32 *lab, *bits, *contact, *meetbuf; // the slot's label / bitmap / contact arrays
     SampleRecordDev rec; // record of the sample in flight (thread 0)
@@ -329,6 +336,7 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
     const u64 *lab64 = reinterpret_cast<const u64 *>(lab);
     u32 cnt = fe;
     contact_n = 0;
+    const bool sigma_small = sh.sigma_small[e] != 0; // uniform; written behind a barrier
     if (static_cast<u64>(next_depth) + 1 > p.aux_cap) // more levels than the slot's level table holds
         return false;
     if (tid == 0) {
@@ -445,7 +453,7 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
                         }
                         wk.e_lvl += 1;
                     } else if (at_level[k]) {
-                        sat_atomic_add(ex.pp->sig + idx[k], sig_u);
+                        sat_atomic_add(ex.pp->sig + idx[k], sig_u, sigma_small);
                         wk.e_lvl += 1;
                     }
                 }
@@ -597,7 +605,7 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
                     if (candidate[k] && !win[k])
                         idx[k] = kSmemDedupe ? sh.h_idx[ent[k]] : ld_cg(lab + 2 * static_cast<u64>(v[k]) + e) - ex.base;
                     if (candidate[k] || at_level[k]) {
-                        sat_atomic_add(ex.pp->sig + idx[k], sig_u[k]); // sampler.cpp:97-98
+                        sat_atomic_add(ex.pp->sig + idx[k], sig_u[k], sigma_small); // sampler.cpp:97-98
                         wk.e_lvl += 1;
                     }
                 }
@@ -635,14 +643,21 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
 // Only needed when the search continues, so it is evaluated after the level,
 // not per settled vertex (the last level of a sample never needs it).
 template <int BLOCK>
-__device__ __forceinline__ u64 sum_frontier_degrees(const SamplerParams &p, const SideRegs &sd, u64 *red) {
-    u64 s = 0;
+__device__ __forceinline__ u64 sum_frontier_degrees(const SamplerParams &p, const SideRegs &sd, u64 *red,
+                                                    u32 *sigma_small) {
+    u64 s = 0, g = 0;
     for (u32 i = sd.fb + threadIdx.x; i < sd.cnt; i += BLOCK) {
         const u32 v = ld_cg(sd.pp->list + i);
         s += __ldg(p.offsets + v + 1) - __ldg(p.offsets + v);
+        const u64 sg = ld_cg(sd.pp->sig + i);
+        g = g > ~0ull - sg ? ~0ull : g + sg;
     }
     const u64 r = block_sum_u64<BLOCK>(s, red);
-    __syncthreads();
+    // The graph is simple, so sigma of a vertex of the next level is a sum over DISTINCT frontier
+    // vertices and cannot exceed the frontier's total; every thread's share below 2^63 / BLOCK bounds it.
+    const int big = __syncthreads_or(g >= (1ull << 63) / BLOCK ? 1 : 0);
+    if (threadIdx.x == 0)
+        *sigma_small = big ? 0u : 1u;
     return r;
 }
 
@@ -712,16 +727,24 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
         u32 v_n[ITEMS], kk_n[ITEMS];
         int owner_n[ITEMS];
         bool act_n[ITEMS];
-        auto fetch = [&](u64 t0) {
+        // The slots of a thread ascend (over k, then over tiles), so the owner row of a slot is searched
+        // upwards from the owner of the thread's previous slot: one shared-memory compare for the common
+        // case of a long row, a galloping + binary search otherwise.
+        auto fetch = [&](u64 t0, int hint) {
 #pragma unroll
             for (int k = 0; k < ITEMS; ++k) {
                 const u64 j = t0 + static_cast<u64>(k) * BLOCK + tid;
                 act_n[k] = j < T;
                 v_n[k] = 0;
                 kk_n[k] = 0;
-                owner_n[k] = 0;
+                owner_n[k] = hint;
                 if (act_n[k]) {
-                    int lo = 0, hi = BLOCK; // owner row: last r with c_scan[r] <= j
+                    int lo = hint, hi = hint + 1, step = 1; // owner row: last r with c_scan[r] <= j; c_scan[BLOCK] = T > j
+                    while (sh.c_scan[hi] <= j) {
+                        lo = hi;
+                        hi = hi + step < BLOCK ? hi + step : BLOCK;
+                        step <<= 1;
+                    }
                     while (hi - lo > 1) {
                         const int mid = (lo + hi) >> 1;
                         if (sh.c_scan[mid] <= j)
@@ -729,6 +752,7 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
                         else
                             hi = mid;
                     }
+                    hint = lo;
                     owner_n[k] = lo;
                     kk_n[k] = static_cast<u32>(j - sh.c_scan[lo]);
                     v_n[k] = __ldg(p.targets + sh.c_beg[lo] + kk_n[k]);
@@ -736,7 +760,7 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
             }
         };
         if (T > 0)
-            fetch(0);
+            fetch(0, 0);
         for (u64 t0 = 0; t0 < T; t0 += TILE) {
             u32 v[ITEMS], kk[ITEMS];
             int owner[ITEMS];
@@ -749,7 +773,7 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
                 act[k] = act_n[k];
             }
             if (t0 + TILE < T)
-                fetch(t0 + TILE);
+                fetch(t0 + TILE, owner[ITEMS - 1]);
             // Visit test.  With bitmaps one 8-byte word holds the visited bits of 32 consecutive vertices
             // for both sides; rows are ascending, so a hub row streams through the bitmap instead of
             // touching one 128-byte label line per target.
@@ -1205,6 +1229,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
                 sh.ws[c] = 0;
             sh.ws[kW_V_set] = 2;
             sh.ws[kW_samples] = 1;
+            sh.sigma_small[0] = sh.sigma_small[1] = 1; // sigma[root] = 1
         }
         wk.e_lvl = 0;
         wk.p_walk = 0;
@@ -1260,7 +1285,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             EBC_PH(1)
             found = sh.min_contact != 0xffffffffu;
             if (!found) // next_pending (sampler.cpp:95,102); evaluated fused into the level it was 3 % slower
-                side[e].pending = sum_frontier_degrees<BLOCK>(p, side[e], sh.red64);
+                side[e].pending = sum_frontier_degrees<BLOCK>(p, side[e], sh.red64, &sh.sigma_small[e]);
             else
                 __syncthreads();
             EBC_PH(3)
@@ -1395,9 +1420,22 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             p.records[local] = sh.rec;
         if (sh.bits) { // clear the bitmap words of every settled vertex (both sides share the 8-byte word)
             u64 *bits64 = reinterpret_cast<u64 *>(sh.bits);
-            for (int k = 0; k < 2; ++k)
-                for (u32 i = tid; i < side[k].cnt; i += BLOCK)
-                    st_cg(bits64 + (ld_cg(side[k].pp->list + i) >> 5), static_cast<u64>(0));
+            for (int k = 0; k < 2; ++k) {
+                const u32 c = side[k].cnt;
+                const u32 *lst = side[k].pp->list;
+                for (u32 i0 = 0; i0 < c; i0 += 4 * BLOCK) { // four independent loads in flight per thread
+                    u32 w[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const u32 i = i0 + q * BLOCK + tid;
+                        w[q] = i < c ? ld_cg(lst + i) >> 5 : 0xffffffffu;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (w[q] != 0xffffffffu)
+                            st_cg(bits64 + w[q], static_cast<u64>(0));
+                }
+            }
         }
         for (int k = 0; k < 2; ++k) {
             if (tid == 0) {
