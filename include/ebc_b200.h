@@ -152,6 +152,11 @@ typedef struct ebc_run_config {
                                   * paths, counters, tau), but vertices that cannot lie on the sampled path
                                   * are not labelled.  Needed for ebc_sampler_last_state and for work
                                   * counters V_set / F_chk / E_lvl that equal the reference algorithm's. */
+    int renumber;              /* device-side vertex numbering of the search state: 0 = auto, 1 = always, -1 = never.
+                                * On graphs with hubs (max degree >= 1024) the sampler keeps a copy of the graph
+                                * renumbered by descending degree, so probes of hub vertices share cache lines.
+                                * Purely internal: row order, discovery order, samples, counters and every id
+                                * that crosses this interface stay those of the caller's graph. */
 } ebc_run_config;
 
 EBC_API void ebc_run_config_default(ebc_run_config *cfg);
@@ -289,7 +294,8 @@ EBC_API ebc_status ebc_sampler_work(ebc_sampler *s, uint64_t work_out[12], int r
 EBC_API ebc_status ebc_sampler_mark(ebc_sampler *s, int event);
 EBC_API ebc_status ebc_sampler_elapsed_ms(ebc_sampler *s, int from_event, int to_event, float *ms);
 EBC_API ebc_status ebc_sampler_sync(ebc_sampler *s);
-/* slots, block_threads, slot_capacity, device bytes actually in use. */
+/* slots, block_threads, slot_capacity, device bytes in use, SM count,
+ * launches (bits 0-47) | renumbered (bits 48-55) | items_per_thread (bits 56-63). */
 EBC_API ebc_status ebc_sampler_info(ebc_sampler *s, uint64_t info_out[6]);
 /* The sampler's cudaStream_t and the device address of epoch frame 0|1
  * (for callers that aggregate frames themselves, e.g. NCCL in bench.py). */

@@ -229,13 +229,14 @@ class RunConfig:
     overlap: bool = True
     items_per_thread: int = 0
     materialize_final_level: bool = False
+    renumber: int = 0  # device-side hub-clustered numbering: 0 auto (hub graphs), 1 always, -1 never
 
     def to_c(self) -> _CRunConfig:
         c = _CRunConfig()
         _capi.load().ebc_run_config_default(C.byref(c))
         for f in ("eps", "delta", "seed", "bound", "allocator", "omega_override", "calib_samples",
                   "diameter_sweeps", "vertex_diameter_override", "epoch_samples", "max_epochs", "device",
-                  "rank", "world_size", "block_threads", "slots", "slot_capacity", "items_per_thread"):
+                  "rank", "world_size", "block_threads", "slots", "slot_capacity", "items_per_thread", "renumber"):
             setattr(c, f, getattr(self, f))
         c.overlap = int(self.overlap)
         c.materialize_final_level = int(self.materialize_final_level)
@@ -398,8 +399,8 @@ class Sampler:
         w = np.zeros(6, dtype=np.uint64)
         _check(_capi.load().ebc_sampler_info(self._h, _p(w, _capi.u64p)))
         return dict(slots=int(w[0]), block_threads=int(w[1]), slot_capacity=int(w[2]),
-                    device_bytes=int(w[3]), sm_count=int(w[4]), launches=int(w[5]) & ((1 << 56) - 1),
-                    items_per_thread=int(w[5]) >> 56)
+                    device_bytes=int(w[3]), sm_count=int(w[4]), launches=int(w[5]) & ((1 << 48) - 1),
+                    renumbered=(int(w[5]) >> 48) & 0xFF, items_per_thread=int(w[5]) >> 56)
 
     def stream(self) -> int:
         p = C.c_void_p()

@@ -80,6 +80,7 @@ SamplerOptions sampler_options(const ebc_run_config *cfg) {
         o.slot_capacity = cfg->slot_capacity;
         o.items_per_thread = cfg->items_per_thread;
         o.materialize_final_level = cfg->materialize_final_level != 0;
+        o.renumber = cfg->renumber;
     }
     return o;
 }

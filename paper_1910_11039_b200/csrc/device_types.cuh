@@ -54,6 +54,17 @@ struct SamplerParams {
     u64 n;
     const u64 *offsets;
     const u32 *targets;
+    // Hub-clustered numbering (optional).  The search state (labels, bitmaps) is indexed by DENSE ids:
+    // vertices renumbered by descending degree, so the probes of hub targets share cache lines.
+    // offsets/targets above are then the dense graph: row i = the row of vertex to_ext[i], its entries
+    // in the ORIGINAL (ascending external id) order but holding dense ids, so discovery order, meet
+    // order and row positions are those of the external graph.  ext_offsets/ext_targets are the graph
+    // as uploaded (rows ascending), used to locate a vertex inside a row.  Without renumbering
+    // to_dense == to_ext == nullptr and ext_* alias offsets/targets.
+    const u32 *to_dense; // external id -> dense id
+    const u32 *to_ext;   // dense id -> external id
+    const u64 *ext_offsets;
+    const u32 *ext_targets;
     // slots
     u32 *lab;      // [slots][2][n]
     u32 *list;     // [slots][2][cap]   settled vertices in discovery order

@@ -46,6 +46,9 @@ __device__ __forceinline__ u32 lanemask_lt() {
     return m;
 }
 
+// External (caller-visible) id of a dense vertex id (see SamplerParams::to_ext).
+__device__ __forceinline__ u32 ext_id(const SamplerParams &p, u32 v) { return p.to_ext ? __ldg(p.to_ext + v) : v; }
+
 // sigma[idx] = sat_add_u64(sigma[idx], add)  (sampler.cpp:11-13,98) with atomics:
 // a wrapped add is always followed by the same thread's atomicMax(.., 2^64-1),
 // so the value after the level barrier is 2^64-1 iff the true sum overflowed.
@@ -977,23 +980,26 @@ __device__ void walk_side(const SamplerParams &p, const u32 *lab, int x, const S
             u128 total_local = 0;
             const bool by_level = static_cast<u64>(span) * (66 - __clzll(degu)) < degu;
             if (by_level) {
+                // rows are ascending in EXTERNAL ids: search the uploaded graph's row of u
+                const u64 xbeg = __ldg(p.ext_offsets + ext_id(p, u)), xend = xbeg + degu;
                 for (u32 i = lo + tid; i < hi; i += BLOCK) {
                     const u32 w = ld_cg(sd.pp->list + i);
-                    u64 a = beg, b = end; // lower_bound of w in the row of u
+                    const u32 wx = ext_id(p, w);
+                    u64 a = xbeg, b = xend; // lower_bound of w in the row of u
                     while (a < b) {
                         const u64 mid = (a + b) >> 1;
-                        if (__ldg(p.targets + mid) < w)
+                        if (__ldg(p.ext_targets + mid) < wx)
                             a = mid + 1;
                         else
                             b = mid;
                     }
-                    if (a < end && __ldg(p.targets + a) == w) {
+                    if (a < xend && __ldg(p.ext_targets + a) == wx) {
                         const u64 sg = ld_cg(sd.pp->sig + i);
                         total_local += sg;
                         wk.p_walk += 1;
                         const u32 slot = atomicAdd(&sh.pred_cnt, 1u);
                         if (slot < kPredCache) {
-                            sh.pred_pos[slot] = static_cast<u32>(a - beg);
+                            sh.pred_pos[slot] = static_cast<u32>(a - xbeg);
                             sh.pred_sig[slot] = sg;
                             sh.pred_vtx[slot] = w;
                         }
@@ -1067,9 +1073,10 @@ __device__ void walk_side(const SamplerParams &p, const u32 *lab, int x, const S
         d -= 1;
         if (d > 0) { // sampler.cpp:152-153: endpoints are never counted
             if (tid == 0) {
-                atomicAdd(p.frame + 1 + u, 1u); // apply_sample (sampler.hpp:77)
+                const u32 ux = ext_id(p, u);
+                atomicAdd(p.frame + 1 + ux, 1u); // apply_sample (sampler.hpp:77)
                 if (path_out && pos >= 0 && static_cast<u64>(pos) < p.path_stride)
-                    path_out[pos] = u; // longer paths are truncated to path_stride entries
+                    path_out[pos] = ux; // longer paths are truncated to path_stride entries
             }
             pos += pos_step;
             emitted += 1;
@@ -1207,6 +1214,11 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             s = static_cast<u32>(a);
             t = static_cast<u32>(b);
         }
+        const u32 s_ext = s, t_ext = t;
+        if (p.to_dense) {
+            s = __ldg(p.to_dense + s);
+            t = __ldg(p.to_dense + t);
+        }
 
         // ---- init both sides (sampler.cpp:65-76) ----
         for (int k = 0; k < 2; ++k) {
@@ -1237,8 +1249,8 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
 
         if (tid == 0) { // the sample's record is kept in shared memory, written by thread 0 only
             SampleRecordDev &rec = sh.rec;
-            rec.s = s;
-            rec.t = t;
+            rec.s = s_ext;
+            rec.t = t_ext;
             rec.dist = 0xffffffffu;
             rec.meet = 0xffffffffu;
             rec.meet_count = 0;
@@ -1376,7 +1388,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
                     meet = ld_cg(sh.meetbuf + 4 * static_cast<u64>(meet_count - 1));
             }
             if (tid == 0)
-                sh.rec.meet = meet;
+                sh.rec.meet = ext_id(p, meet);
             EBC_PH(4)
 
             // walks (sampler.cpp:157-163): path order s .. meet .. t
@@ -1389,9 +1401,10 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
                                     static_cast<long long>(dist_f) - 2, -1, emitted, sh, wk);
             if (meet != s && meet != t) {
                 if (tid == 0) {
-                    atomicAdd(p.frame + 1 + meet, 1u);
+                    const u32 mx = ext_id(p, meet);
+                    atomicAdd(p.frame + 1 + mx, 1u);
                     if (p.paths && static_cast<u64>(dist_f - 1) < p.path_stride)
-                        p.paths[local * p.path_stride + (dist_f - 1)] = meet;
+                        p.paths[local * p.path_stride + (dist_f - 1)] = mx;
                 }
                 emitted += 1;
             }
