@@ -115,6 +115,108 @@ DevicePool &pool() {
     return *p;
 }
 
+// Streams, events and the pinned result words are cached the same way: creating and, above all,
+// destroying them (cudaFreeHost, cudaStreamDestroy) sporadically blocks for 10^2 ms in the driver, which
+// is longer than a whole run on a small input.
+class HandleCache {
+public:
+    cudaStream_t take_stream() {
+        int dev = device();
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            auto &v = streams_[dev];
+            if (!v.empty()) {
+                cudaStream_t s = v.back();
+                v.pop_back();
+                return s;
+            }
+        }
+        cudaStream_t s = nullptr;
+        EBC_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        return s;
+    }
+    void give_stream(cudaStream_t s) {
+        if (!s)
+            return;
+        std::lock_guard<std::mutex> lk(mu_);
+        streams_[device()].push_back(s);
+    }
+    cudaEvent_t take_event(bool timing) {
+        int dev = device();
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            auto &v = events_[{dev, timing}];
+            if (!v.empty()) {
+                cudaEvent_t e = v.back();
+                v.pop_back();
+                return e;
+            }
+        }
+        cudaEvent_t e = nullptr;
+        EBC_CUDA(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming));
+        return e;
+    }
+    void give_event(cudaEvent_t e, bool timing) {
+        if (!e)
+            return;
+        std::lock_guard<std::mutex> lk(mu_);
+        events_[{device(), timing}].push_back(e);
+    }
+    // two u64 of pinned, mapped host memory
+    u64 *take_words() {
+        int dev = device();
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            auto &v = words_[dev];
+            if (!v.empty()) {
+                u64 *w = v.back();
+                v.pop_back();
+                return w;
+            }
+        }
+        u64 *w = nullptr;
+        EBC_CUDA(cudaHostAlloc(reinterpret_cast<void **>(&w), 2 * sizeof(u64), cudaHostAllocMapped));
+        return w;
+    }
+    void give_words(u64 *w) {
+        if (!w)
+            return;
+        std::lock_guard<std::mutex> lk(mu_);
+        words_[device()].push_back(w);
+    }
+    void release_idle() {
+        std::lock_guard<std::mutex> lk(mu_);
+        for (auto &kv : streams_)
+            for (cudaStream_t s : kv.second)
+                cudaStreamDestroy(s);
+        for (auto &kv : events_)
+            for (cudaEvent_t e : kv.second)
+                cudaEventDestroy(e);
+        for (auto &kv : words_)
+            for (u64 *w : kv.second)
+                cudaFreeHost(w);
+        streams_.clear();
+        events_.clear();
+        words_.clear();
+    }
+
+private:
+    static int device() {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        return dev;
+    }
+    std::mutex mu_;
+    std::map<int, std::vector<cudaStream_t>> streams_;
+    std::map<std::pair<int, bool>, std::vector<cudaEvent_t>> events_;
+    std::map<int, std::vector<u64 *>> words_;
+};
+
+HandleCache &handles() {
+    static HandleCache *h = new HandleCache; // leaked on purpose, like the pool
+    return *h;
+}
+
 template <typename T> T *dev_alloc(std::uint64_t count) {
     return static_cast<T *>(pool().alloc(std::max<std::uint64_t>(count, 1) * sizeof(T)));
 }
@@ -497,7 +599,10 @@ constexpr u64 kLargeSlots = 8; // full-capacity slots of the re-run pass
 
 } // namespace
 
-void release_device_cache() { pool().release_idle(); }
+void release_device_cache() {
+    pool().release_idle();
+    handles().release_idle();
+}
 
 struct CudaSampler::Impl {
     int device = 0;
@@ -700,38 +805,42 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
         EBC_CUDA(cudaSetDevice(opt.device));
     }
     EBC_CUDA(cudaGetDevice(&m.device));
-    cudaDeviceProp prop{};
-    EBC_CUDA(cudaGetDeviceProperties(&prop, m.device));
-    if (prop.major < 10)
+    int cc_major = 0, cc_minor = 0; // (cudaGetDeviceProperties costs milliseconds; three attributes do not)
+    EBC_CUDA(cudaDeviceGetAttribute(&cc_major, cudaDevAttrComputeCapabilityMajor, m.device));
+    EBC_CUDA(cudaDeviceGetAttribute(&cc_minor, cudaDevAttrComputeCapabilityMinor, m.device));
+    EBC_CUDA(cudaDeviceGetAttribute(&m.sm_count, cudaDevAttrMultiProcessorCount, m.device));
+    if (cc_major < 10)
         throw CudaError("this build targets sm_100a (B200); found compute capability " +
-                        std::to_string(prop.major) + "." + std::to_string(prop.minor));
-    m.sm_count = prop.multiProcessorCount;
+                        std::to_string(cc_major) + "." + std::to_string(cc_minor));
+    lap("device query");
     {
-        // The path is dominated by random 4..8-byte probes of per-vertex labels.  With the default
-        // L2 fetch granularity every such probe pulls a whole 128-byte line from HBM (measured with
-        // ncu: 4 sectors per request); 32 bytes makes DRAM traffic match the sectors actually used.
-        size_t granularity = 32;
-        if (const char *env = std::getenv("EBC_L2_FETCH_GRANULARITY"))
-            granularity = static_cast<size_t>(std::atoi(env));
-        if (granularity == 32 || granularity == 64 || granularity == 128)
-            cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, granularity); // a hint; failure is harmless
+        // Experiment hook: cudaLimitMaxL2FetchGranularity.  The path is dominated by random 4..8-byte
+        // probes, each of which pulls a 128-byte line from HBM; the limit was measured to change neither
+        // the DRAM bytes nor the probe rate on B200 (profiles/r01_microbench_random_gather.txt), and
+        // cudaDeviceSetLimit is not free, so it is only applied on request.
+        if (const char *env = std::getenv("EBC_L2_FETCH_GRANULARITY")) {
+            const size_t granularity = static_cast<size_t>(std::atoi(env));
+            if (granularity == 32 || granularity == 64 || granularity == 128)
+                cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, granularity);
+        }
         cudaGetLastError();
     }
     require(g.n >= 2, "sampler: need at least two vertices");
     m.n = g.n;
     m.arcs = g.targets.size();
 
-    EBC_CUDA(cudaStreamCreateWithFlags(&m.s_sample, cudaStreamNonBlocking));
-    EBC_CUDA(cudaStreamCreateWithFlags(&m.s_sample2, cudaStreamNonBlocking));
-    EBC_CUDA(cudaStreamCreateWithFlags(&m.s_agg, cudaStreamNonBlocking));
+    m.s_sample = handles().take_stream();
+    m.s_sample2 = handles().take_stream();
+    m.s_agg = handles().take_stream();
     for (int i = 0; i < 2; ++i) {
-        EBC_CUDA(cudaEventCreateWithFlags(&m.ev_sampled[i], cudaEventDisableTiming));
-        EBC_CUDA(cudaEventCreateWithFlags(&m.ev_folded[i], cudaEventDisableTiming));
-        EBC_CUDA(cudaEventCreateWithFlags(&m.ev_rerun[i], cudaEventDisableTiming));
+        m.ev_sampled[i] = handles().take_event(false);
+        m.ev_folded[i] = handles().take_event(false);
+        m.ev_rerun[i] = handles().take_event(false);
     }
-    EBC_CUDA(cudaEventCreateWithFlags(&m.ev_lane, cudaEventDisableTiming));
+    m.ev_lane = handles().take_event(false);
     for (int i = 0; i < kEvents; ++i)
-        EBC_CUDA(cudaEventCreate(&m.ev_user[i]));
+        m.ev_user[i] = handles().take_event(true);
+    lap("streams and events");
 
     // ---- graph: replicated CSR, u64 offsets + u32 targets ----
     m.d_offsets = dev_alloc<u64>(g.n + 1);
@@ -745,7 +854,6 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
 
     // ---- launch shape ----
     m.block = opt.block_threads ? opt.block_threads : 128;
-    m.items = opt.items_per_thread ? opt.items_per_thread : 4;
     m.flags = opt.materialize_final_level ? kFlagMaterializeFinal : 0u;
     {
         // Visited bitmaps pay off when single rows are long enough to be probed (hub graphs); on
@@ -755,6 +863,12 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
             max_degree = std::max<std::uint64_t>(max_degree, g.degree(v));
         const char *env = std::getenv("EBC_BITMAP");
         m.hub_graph = max_degree >= 1024;
+        // Adjacency slots per thread per tile.  The kernel's instruction footprint (121 KB at 2, 144 KB at
+        // 4) is a measured bottleneck -- eight CTAs per SM sit in different phases -- so 2 wins wherever
+        // levels are either long rows (hubs) or tiny (small graphs): R-MAT-20 4.19 M -> 4.51 M samples/s,
+        // config 1 14.6 M -> 17.0 M.  Large low-degree graphs expand many narrow multi-row levels whose
+        // cost is per tile (barriers, ranks), where 4 is better (config 3: 158 k vs 147 k).
+        m.items = opt.items_per_thread ? opt.items_per_thread : (m.hub_graph || m.arcs < (u64{1} << 22) ? 2 : 4);
         const bool want = env ? std::atoi(env) != 0 : m.hub_graph;
         if (want && !opt.materialize_final_level)
             m.flags |= kFlagUseBitmap;
@@ -802,7 +916,7 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
     for (int i = 0; i < 2; ++i) {
         m.d_frame[i] = dev_alloc<u32>(g.n + 1);
         EBC_CUDA(cudaMemsetAsync(m.d_frame[i], 0, (g.n + 1) * 4, m.s_sample));
-        EBC_CUDA(cudaHostAlloc(reinterpret_cast<void **>(&m.h_result[i]), 2 * sizeof(u64), cudaHostAllocMapped));
+        m.h_result[i] = handles().take_words();
         m.h_result[i][0] = m.h_result[i][1] = 0;
     }
     m.d_ovf_total = dev_alloc<unsigned long long>(2);
@@ -854,14 +968,14 @@ CudaSampler::~CudaSampler() {
     dev_free(m.d_to_ext);
     for (int i = 0; i < 2; ++i) {
         dev_free(m.d_frame[i]);
-        cudaFreeHost(m.h_result[i]);
-        cudaEventDestroy(m.ev_sampled[i]);
-        cudaEventDestroy(m.ev_folded[i]);
-        cudaEventDestroy(m.ev_rerun[i]);
+        handles().give_words(m.h_result[i]);
+        handles().give_event(m.ev_sampled[i], false);
+        handles().give_event(m.ev_folded[i], false);
+        handles().give_event(m.ev_rerun[i], false);
     }
-    cudaEventDestroy(m.ev_lane);
+    handles().give_event(m.ev_lane, false);
     for (int i = 0; i < kEvents; ++i)
-        cudaEventDestroy(m.ev_user[i]);
+        handles().give_event(m.ev_user[i], true);
     dev_free(m.d_ovf_total);
     dev_free(m.d_S);
     dev_free(m.d_wide);
@@ -880,9 +994,9 @@ CudaSampler::~CudaSampler() {
     dev_free(m.d_bfs);
     dev_free(m.d_best);
     dev_free(m.d_flush);
-    cudaStreamDestroy(m.s_sample);
-    cudaStreamDestroy(m.s_sample2);
-    cudaStreamDestroy(m.s_agg);
+    handles().give_stream(m.s_sample);
+    handles().give_stream(m.s_sample2);
+    handles().give_stream(m.s_agg);
     if (trace)
         pool().stats("after dtor");
     if (trace)

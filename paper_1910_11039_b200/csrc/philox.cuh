@@ -57,6 +57,18 @@ EBC_HD Philox4 philox4x32_10(Philox4 c, std::uint32_t k0, std::uint32_t k1) {
     return c;
 }
 
+#if defined(__CUDACC__)
+// Device code keeps ONE copy of the ten rounds per kernel: a sample makes a handful of draws, while the
+// sampling kernel's instruction footprint is a measured bottleneck (profiles/r01_icache.txt).
+__device__ __noinline__ static std::uint64_t philox_draw_device(std::uint32_t draw, std::uint32_t tag, std::uint32_t i0,
+                                                                std::uint32_t i1, std::uint32_t k0, std::uint32_t k1) {
+    const Philox4 r = philox4x32_10(Philox4{draw, tag, i0, i1}, k0, k1);
+    return static_cast<std::uint64_t>(r.x) | (static_cast<std::uint64_t>(r.y) << 32);
+}
+// (0 - bound) % bound, the rejection threshold of next_below: a 64-bit software division, kept out of line.
+__device__ __noinline__ static std::uint64_t lemire_threshold_device(std::uint64_t bound) { return (0 - bound) % bound; }
+#endif
+
 class SampleStream {
 public:
     EBC_HD SampleStream(std::uint64_t seed, std::uint32_t tag, std::uint64_t index)
@@ -64,9 +76,13 @@ public:
           i0_(static_cast<std::uint32_t>(index)), i1_(static_cast<std::uint32_t>(index >> 32)), draw_(0) {}
 
     EBC_HD std::uint64_t next_u64() {
+#if defined(__CUDA_ARCH__)
+        return philox_draw_device(draw_++, tag_, i0_, i1_, k0_, k1_);
+#else
         const Philox4 r = philox4x32_10(Philox4{draw_, tag_, i0_, i1_}, k0_, k1_);
         ++draw_;
         return static_cast<std::uint64_t>(r.x) | (static_cast<std::uint64_t>(r.y) << 32);
+#endif
     }
 
     // Both 64-bit halves of one block (generators only; counts as one draw).
@@ -81,7 +97,11 @@ public:
         std::uint64_t x = next_u64();
         std::uint64_t hi = mul64hi(x, bound), lo = x * bound;
         if (lo < bound) {
+#if defined(__CUDA_ARCH__)
+            const std::uint64_t threshold = lemire_threshold_device(bound);
+#else
             const std::uint64_t threshold = (0 - bound) % bound;
+#endif
             while (lo < threshold) {
                 x = next_u64();
                 hi = mul64hi(x, bound);

@@ -851,24 +851,29 @@ __device__ u32 meet_from_edges(const u32 *edges, u32 m, u32 olo, u32 ohi, u32 *m
         sh.f_s[i] = static_cast<u64>(ld_cg(w + 4)) | (static_cast<u64>(ld_cg(w + 5)) << 32);
     }
     __syncthreads();
-    u64 sum[PER];
+    // Every thread owns PER edges; the table is walked once per pass (j outer, shared loads broadcast).
+    u32 vi[PER];
+    u64 ki[PER], sum[PER];
     bool first[PER];
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
         const u32 i = tid + q * BLOCK;
+        vi[q] = i < m ? sh.f_v[i] : 0u;
+        ki[q] = i < m ? sh.f_key[i] : 0ull; // (no key is below 0: a padding item never loses `first`, and is ignored)
         sum[q] = 0;
         first[q] = i < m;
-        if (i < m) {
-            const u32 vi = sh.f_v[i];
-            const u64 ki = sh.f_key[i];
-            for (u32 j = 0; j < m; ++j)
-                if (sh.f_v[j] == vi) {
-                    const u64 sj = sh.f_s[j];
-                    sum[q] = sum[q] > ~0ull - sj ? ~0ull : sum[q] + sj; // sat_add_u64 (sampler.cpp:11-13)
-                    if (sh.f_key[j] < ki)
-                        first[q] = false;
-                }
-        }
+    }
+#pragma unroll 2
+    for (u32 j = 0; j < m; ++j) {
+        const u32 vj = sh.f_v[j];
+        const u64 kj = sh.f_key[j], sj = sh.f_s[j];
+#pragma unroll
+        for (int q = 0; q < PER; ++q)
+            if (vj == vi[q]) {
+                sum[q] = sum[q] > ~0ull - sj ? ~0ull : sum[q] + sj; // sat_add_u64 (sampler.cpp:11-13)
+                if (kj < ki[q])
+                    first[q] = false;
+            }
     }
     __syncthreads();
 #pragma unroll
@@ -882,18 +887,29 @@ __device__ u32 meet_from_edges(const u32 *edges, u32 m, u32 olo, u32 ohi, u32 *m
         }
     }
     __syncthreads();
+    u32 rank[PER];
+    bool member[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const u32 i = tid + q * BLOCK;
+        member[q] = i < m && sh.f_o[i] - olo < ohi - olo;
+        rank[q] = 0;
+    }
+#pragma unroll 2
+    for (u32 j = 0; j < m; ++j) {
+        const u64 kj = sh.f_key[j];
+        const bool in_range = sh.f_o[j] - olo < ohi - olo;
+#pragma unroll
+        for (int q = 0; q < PER; ++q)
+            rank[q] += in_range && kj < ki[q] ? 1u : 0u;
+    }
     u32 members = 0;
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
         const u32 i = tid + q * BLOCK;
-        if (i < m && sh.f_o[i] - olo < ohi - olo) {
-            const u64 ki = sh.f_key[i];
-            u32 rank = 0;
-            for (u32 j = 0; j < m; ++j)
-                if (sh.f_o[j] - olo < ohi - olo && sh.f_key[j] < ki)
-                    ++rank;
-            u32 *w = meetbuf + 4 * static_cast<u64>(rank);
-            st_cg(w + 0, sh.f_v[i]);
+        if (member[q]) {
+            u32 *w = meetbuf + 4 * static_cast<u64>(rank[q]);
+            st_cg(w + 0, vi[q]);
             st_cg(w + 1, sh.f_o[i]);
             st_cg(w + 2, static_cast<u32>(sh.f_s[i]));
             st_cg(w + 3, static_cast<u32>(sh.f_s[i] >> 32));
@@ -1397,19 +1413,23 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             const u32 dist_b = e == 0 ? d_ot : d_ex;
             u32 emitted = 0;
             // forward side: vertices at forward depth d sit at internal position d-1
-            walk_side<BLOCK, ITEMS>(p, sh.lab, 0, side[0], meet, dist_f, rng, p.paths ? p.paths + local * p.path_stride : nullptr,
-                                    static_cast<long long>(dist_f) - 2, -1, emitted, sh, wk);
-            if (meet != s && meet != t) {
-                if (tid == 0) {
-                    const u32 mx = ext_id(p, meet);
-                    atomicAdd(p.frame + 1 + mx, 1u);
-                    if (p.paths && static_cast<u64>(dist_f - 1) < p.path_stride)
-                        p.paths[local * p.path_stride + (dist_f - 1)] = mx;
+#pragma unroll 1 // one copy of the walk in the instruction stream
+            for (int x = 0; x < 2; ++x) {
+                const SideRegs sd = x == 0 ? side[0] : side[1];
+                walk_side<BLOCK, ITEMS>(p, sh.lab, x, sd, meet, x == 0 ? dist_f : dist_b, rng,
+                                        p.paths ? p.paths + local * p.path_stride : nullptr,
+                                        x == 0 ? static_cast<long long>(dist_f) - 2 : static_cast<long long>(dist_f),
+                                        x == 0 ? -1 : +1, emitted, sh, wk);
+                if (x == 0 && meet != s && meet != t) {
+                    if (tid == 0) {
+                        const u32 mx = ext_id(p, meet);
+                        atomicAdd(p.frame + 1 + mx, 1u);
+                        if (p.paths && static_cast<u64>(dist_f - 1) < p.path_stride)
+                            p.paths[local * p.path_stride + (dist_f - 1)] = mx;
+                    }
+                    emitted += 1;
                 }
-                emitted += 1;
             }
-            walk_side<BLOCK, ITEMS>(p, sh.lab, 1, side[1], meet, dist_b, rng, p.paths ? p.paths + local * p.path_stride : nullptr,
-                                    static_cast<long long>(dist_f), +1, emitted, sh, wk);
             if (tid == 0)
                 sh.rec.path_len = emitted;
             EBC_PH(5)
@@ -1433,9 +1453,10 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             p.records[local] = sh.rec;
         if (sh.bits) { // clear the bitmap words of every settled vertex (both sides share the 8-byte word)
             u64 *bits64 = reinterpret_cast<u64 *>(sh.bits);
+#pragma unroll 1
             for (int k = 0; k < 2; ++k) {
-                const u32 c = side[k].cnt;
-                const u32 *lst = side[k].pp->list;
+                const u32 c = k == 0 ? side[0].cnt : side[1].cnt;
+                const u32 *lst = sh.sp[k].list;
                 for (u32 i0 = 0; i0 < c; i0 += 4 * BLOCK) { // four independent loads in flight per thread
                     u32 w[4];
 #pragma unroll

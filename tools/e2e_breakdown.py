@@ -4,7 +4,7 @@ import paper_1910_11039_b200 as ebc
 g=ebc.gen_rmat(20,16,seed=2).largest_connected_component()
 off,tg=g.offsets,g.targets
 cfg=ebc.RunConfig(eps=0.005,delta=0.1,seed=7)
-for i in range(4):
+for i in range(int(sys.argv[1]) if len(sys.argv)>1 else 4):
     t0=time.time(); g2=ebc.Graph.from_csr(off,tg,validate=False); t1=time.time()
     res,st=ebc.run_pipeline(g2,cfg); t2=time.time()
     del g2; t3=time.time()

@@ -3,7 +3,7 @@
 usage: tools/ncu_lines.py report.ncu-rep lib.so kernel_mangled_name [top]"""
 import csv, re, subprocess, sys, os, tempfile, collections
 rep, so, kern = sys.argv[1:4]
-top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
+top = int(sys.argv[4]) if len(sys.argv) > 4 and sys.argv[4].isdigit() else 40
 tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(so)], cwd=tmp, capture_output=True)
 cub = [f for f in os.listdir(tmp) if f.endswith(".cubin") and "cuda_sampler" in f and "-" not in f][0]
@@ -27,7 +27,8 @@ rows = list(csv.reader(out.splitlines()))
 hdr = rows[1]; ci = {h: i for i, h in enumerate(hdr)}
 data = rows[2:]
 base = int(data[0][ci["Address"]], 16) if data[0][ci["Address"]].startswith("0x") else int(data[0][ci["Address"]])
-agg = collections.defaultdict(lambda: [0.0, 0.0, 0.0, 0.0])
+agg = collections.defaultdict(lambda: [0.0, 0.0, 0.0, 0.0, 0.0])
+sort_col = 4 if '--noinst' in sys.argv else 0
 tot = 0.0
 for r in data:
     a = r[ci["Address"]]; a = int(a, 16) if a.startswith("0x") else int(a)
@@ -37,6 +38,7 @@ for r in data:
     agg[key][1] += float(r[ci["stall_long_sb"]] or 0)
     agg[key][2] += float(r[ci["stall_barrier"]] or 0)
     agg[key][3] += float(r[ci["Instructions Executed"]] or 0)
+    agg[key][4] += float(r[ci["stall_no_inst"]] or 0)
 src = {}
 for (f, ln) in agg:
     if f != "?" and f not in src:
@@ -45,6 +47,6 @@ for (f, ln) in agg:
             if os.path.exists(p):
                 src[f] = open(p).read().splitlines(); break
 print(f"total samples {tot:.0f}")
-for (f, ln), v in sorted(agg.items(), key=lambda x: -x[1][0])[:top]:
+for (f, ln), v in sorted(agg.items(), key=lambda x: -x[1][sort_col])[:top]:
     text = src.get(f, [""] * (ln + 1))[ln - 1].strip()[:90] if f in src and ln - 1 < len(src[f]) else ""
-    print(f"{100*v[0]/tot:5.1f}%  long_sb {100*v[1]/max(v[0],1):3.0f}% bar {100*v[2]/max(v[0],1):3.0f}%  inst {v[3]:11.0f}  {f}:{ln}: {text}")
+    print(f"{100*v[0]/tot:5.1f}%  long_sb {100*v[1]/max(v[0],1):3.0f}% bar {100*v[2]/max(v[0],1):3.0f}% noinst {100*v[4]/max(v[0],1):3.0f}%  inst {v[3]:11.0f}  {f}:{ln}: {text}")
