@@ -39,6 +39,29 @@ __device__ __forceinline__ u64 ld_cg(const u64 *p) { return __ldcg(reinterpret_c
 __device__ __forceinline__ void st_cg(u32 *p, u32 v) { __stcg(p, v); }
 __device__ __forceinline__ void st_cg(u64 *p, u64 v) { __stcg(reinterpret_cast<unsigned long long *>(p), v); }
 
+// Atomics on the slot arrays, spelled as .global PTX.  The slot pointers are read back from shared
+// memory, so the compiler only knows them as generic addresses, and a generic 64-bit atomicAdd expands
+// to a run-time address-space test plus a shared-memory CAS loop next to the real instruction (21
+// instructions per call site, 16 call sites in the 4-item kernel).  None of the results is needed
+// except the old value of the saturating add, so the rest are fire-and-forget reductions.
+__device__ __forceinline__ void red_add_u64(u64 *p, u64 v) {
+    asm volatile("red.global.add.u64 [%0], %1;" ::"l"(__cvta_generic_to_global(p)), "l"(v) : "memory");
+}
+__device__ __forceinline__ u64 atom_add_u64(u64 *p, u64 v) {
+    u64 old;
+    asm volatile("atom.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(__cvta_generic_to_global(p)), "l"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ void red_max_u64(u64 *p, u64 v) {
+    asm volatile("red.global.max.u64 [%0], %1;" ::"l"(__cvta_generic_to_global(p)), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_max_u32(u32 *p, u32 v) {
+    asm volatile("red.global.max.u32 [%0], %1;" ::"l"(__cvta_generic_to_global(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_or_u32(u32 *p, u32 v) {
+    asm volatile("red.global.or.b32 [%0], %1;" ::"l"(__cvta_generic_to_global(p)), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ u32 lane_id() { return threadIdx.x & 31u; }
 __device__ __forceinline__ u32 lanemask_lt() {
     u32 m;
@@ -55,14 +78,13 @@ __device__ __forceinline__ u32 ext_id(const SamplerParams &p, u32 v) { return p.
 // `small`: the sum of sigma over the whole frontier fits 64 bits (see sum_frontier_degrees), so no
 // sum can wrap and the add needs no return value (a fire-and-forget reduction).
 __device__ __forceinline__ void sat_atomic_add(u64 *p, u64 add, bool small) {
-    unsigned long long *q = reinterpret_cast<unsigned long long *>(p);
     if (small) {
-        atomicAdd(q, static_cast<unsigned long long>(add));
+        red_add_u64(p, add);
         return;
     }
-    const unsigned long long old = atomicAdd(q, static_cast<unsigned long long>(add));
+    const u64 old = atom_add_u64(p, add);
     if (old + add < old)
-        atomicMax(q, ~0ull);
+        red_max_u64(p, ~0ull);
 }
 
 // uniform_below_u128 (sampler.cpp:21-30).  Executed redundantly by every thread
@@ -163,6 +185,23 @@ __device__ __forceinline__ u32 block_ranks(const bool (&flag)[ITEMS], u32 (&rank
             cnt[k * WARPS + warp] = __popc(ballot);
     }
     __syncthreads();
+    if (ITEMS * WARPS <= 32) {
+        // every warp scans the ITEMS * WARPS counts with shuffles (far fewer instructions than the
+        // unrolled ITEMS x WARPS walk; this code is instantiated in every tile loop)
+        const u32 mine = lane_id() < static_cast<u32>(ITEMS * WARPS) ? cnt[lane_id()] : 0u;
+        u32 incl = mine;
+#pragma unroll
+        for (int o = 1; o < ITEMS * WARPS; o <<= 1) {
+            const u32 t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane_id() >= static_cast<u32>(o))
+                incl += t;
+        }
+        const u32 excl = incl - mine;
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k)
+            rank[k] = __shfl_sync(0xffffffffu, excl, k * WARPS + static_cast<int>(warp)) + in_warp[k];
+        return __shfl_sync(0xffffffffu, incl, ITEMS * WARPS - 1);
+    }
     u32 running = 0;
 #pragma unroll
     for (int k = 0; k < ITEMS; ++k) {
@@ -323,6 +362,48 @@ struct WorkRegs {
 
 __device__ __forceinline__ u32 half_of(u64 both, int side) { return static_cast<u32>(both >> (32 * side)); }
 
+// Loads the chunk of BLOCK frontier vertices at list positions [c0, c0 + BLOCK) (clipped to fe): row
+// start and sigma of each into c_beg / c_sig, the exclusive prefix of their degrees into
+// c_scan[0..BLOCK]; returns the chunk's number of adjacency slots.  Starts with a barrier (the previous
+// chunk's readers of c_* are done) and ends with one.  Out of line: one copy serves expand_level and
+// probe_level, and it runs once per 128 frontier vertices.
+template <int BLOCK>
+__device__ __noinline__ u64 load_chunk(const SamplerParams &p, const SidePtrs *pp, u32 c0, u32 fe, u64 *c_beg, u64 *c_scan,
+                                       u64 *c_sig, u64 *red64) {
+    const u32 tid = threadIdx.x;
+    const u32 i = c0 + tid;
+    u64 beg = 0, deg = 0, su = 0;
+    if (i < fe) {
+        const u32 u = ld_cg(pp->list + i);
+        beg = __ldg(p.offsets + u);
+        deg = __ldg(p.offsets + u + 1) - beg;
+        su = ld_cg(pp->sig + i);
+    }
+    u64 inc = deg;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u64 t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane_id() >= static_cast<u32>(o))
+            inc += t;
+    }
+    __syncthreads();
+    if (BLOCK > 32 && lane_id() == 31)
+        red64[tid >> 5] = inc;
+    c_beg[tid] = beg;
+    c_sig[tid] = su;
+    if (BLOCK > 32)
+        __syncthreads();
+    u64 before = 0;
+    if (BLOCK > 32)
+        for (u32 w = 0; w < (tid >> 5); ++w)
+            before += red64[w];
+    c_scan[tid + 1] = before + inc;
+    if (tid == 0)
+        c_scan[0] = 0;
+    __syncthreads();
+    return c_scan[BLOCK];
+}
+
 // Expands the frontier of side `e` by one level (sampler.cpp:86-103) and
 // records contacts with the other side (sampler.cpp:105-108).  ex.pending is NOT
 // updated here (see sum_frontier_degrees).  Returns false on
@@ -350,37 +431,8 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
     }
     for (u32 c0 = fb; c0 < fe; c0 += BLOCK) {
         // ---- load a chunk of BLOCK frontier vertices, scan their degrees ----
-        const u32 i = c0 + tid;
-        u64 beg = 0, deg = 0, su = 0;
-        if (i < fe) {
-            const u32 u = ld_cg(ex.pp->list + i);
-            beg = __ldg(p.offsets + u);
-            deg = __ldg(p.offsets + u + 1) - beg;
-            su = ld_cg(ex.pp->sig + i);
-        }
-        u64 inc = deg;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const u64 t = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane_id() >= static_cast<u32>(o))
-                inc += t;
-        }
-        __syncthreads(); // previous chunk's tiles are done with c_*; their label stores are visible
-        if (BLOCK > 32 && lane_id() == 31)
-            sh.red64[tid >> 5] = inc;
-        sh.c_beg[tid] = beg;
-        sh.c_sig[tid] = su;
-        if (BLOCK > 32)
-            __syncthreads();
-        u64 before = 0;
-        if (BLOCK > 32)
-            for (u32 w = 0; w < (tid >> 5); ++w)
-                before += sh.red64[w];
-        sh.c_scan[tid + 1] = before + inc;
-        if (tid == 0)
-            sh.c_scan[0] = 0;
-        __syncthreads();
-        const u64 T = sh.c_scan[BLOCK];
+        // (the loader's first barrier: the previous chunk's tiles are done with c_*, their label stores visible)
+        const u64 T = load_chunk<BLOCK>(p, ex.pp, c0, fe, sh.c_beg, sh.c_scan, sh.c_sig, sh.red64);
         if (tid == 0)
             sh.ws[kW_E_bfs] += T;
 
@@ -449,7 +501,7 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
                         st_cg(ex.pp->list + idx[k], v[k]);
                         st_cg(ex.pp->sig + idx[k], sig_u);
                         if (bits)
-                            atomicOr(bits + 2 * static_cast<u64>(v[k] >> 5) + e, 1u << (v[k] & 31));
+                            red_or_u32(bits + 2 * static_cast<u64>(v[k] >> 5) + e, 1u << (v[k] & 31));
                         if (is_contact[k]) {
                             atomicMin(&sh.min_contact, other_idx[k]);
                             any_contact_local = true;
@@ -560,7 +612,7 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
 #pragma unroll
                     for (int k = 0; k < ITEMS; ++k)
                         if (candidate[k])
-                            atomicMax(lab + 2 * static_cast<u64>(v[k]) + e, kClaimTop - (k * BLOCK + tid));
+                            red_max_u32(lab + 2 * static_cast<u64>(v[k]) + e, kClaimTop - (k * BLOCK + tid));
                 }
                 __syncthreads(); // claims visible
 #pragma unroll
@@ -590,7 +642,7 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
                             st_cg(ex.pp->list + idx[k], v[k]);
                             st_cg(ex.pp->sig + idx[k], static_cast<u64>(0));
                             if (bits)
-                                atomicOr(bits + 2 * static_cast<u64>(v[k] >> 5) + e, 1u << (v[k] & 31));
+                                red_or_u32(bits + 2 * static_cast<u64>(v[k] >> 5) + e, 1u << (v[k] & 31));
                             if (is_contact[k]) {
                                 atomicMin(&sh.min_contact, other_idx[k]);
                                 any_contact_local = true;
@@ -693,37 +745,7 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
     }
     u64 t_total = 0;
     for (u32 c0 = fb; c0 < fe; c0 += BLOCK) {
-        const u32 i = c0 + tid;
-        u64 beg = 0, deg = 0, su = 0;
-        if (i < fe) {
-            const u32 u = ld_cg(ex.pp->list + i);
-            beg = __ldg(p.offsets + u);
-            deg = __ldg(p.offsets + u + 1) - beg;
-            su = ld_cg(ex.pp->sig + i);
-        }
-        u64 inc = deg;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const u64 t = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane_id() >= static_cast<u32>(o))
-                inc += t;
-        }
-        __syncthreads();
-        if (BLOCK > 32 && lane_id() == 31)
-            sh.red64[tid >> 5] = inc;
-        sh.c_beg[tid] = beg;
-        sh.c_sig[tid] = su;
-        if (BLOCK > 32)
-            __syncthreads();
-        u64 before = 0;
-        if (BLOCK > 32)
-            for (u32 w = 0; w < (tid >> 5); ++w)
-                before += sh.red64[w];
-        sh.c_scan[tid + 1] = before + inc;
-        if (tid == 0)
-            sh.c_scan[0] = 0;
-        __syncthreads();
-        const u64 T = sh.c_scan[BLOCK];
+        const u64 T = load_chunk<BLOCK>(p, ex.pp, c0, fe, sh.c_beg, sh.c_scan, sh.c_sig, sh.red64);
         t_total += T;
         // Software pipeline: the targets of tile i+1 are requested before the visit words of tile i,
         // so the two dependent loads of a slot (target id -> visit word) overlap across tiles.
@@ -762,9 +784,16 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
                 }
             }
         };
-        if (T > 0)
-            fetch(0, 0);
-        for (u64 t0 = 0; t0 < T; t0 += TILE) {
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) {
+            v_n[k] = 0;
+            kk_n[k] = 0;
+            owner_n[k] = 0;
+            act_n[k] = false;
+        }
+        // Iteration t0 requests tile t0 and tests the tile requested by the previous iteration (nothing in
+        // the first one); written as one loop so that the request code exists once.
+        for (u64 t0 = 0;; t0 += TILE) {
             u32 v[ITEMS], kk[ITEMS];
             int owner[ITEMS];
             bool act[ITEMS];
@@ -775,8 +804,9 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
                 owner[k] = owner_n[k];
                 act[k] = act_n[k];
             }
-            if (t0 + TILE < T)
-                fetch(t0 + TILE, owner[ITEMS - 1]);
+            const bool more = t0 < T;
+            if (more)
+                fetch(t0, owner[ITEMS - 1]);
             // Visit test.  With bitmaps one 8-byte word holds the visited bits of 32 consecutive vertices
             // for both sides; rows are ascending, so a hub row streams through the bitmap instead of
             // touching one 128-byte label line per target.
@@ -825,6 +855,8 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
                     }
                 }
             }
+            if (!more)
+                break;
         }
     }
     __syncthreads();
@@ -1246,7 +1278,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             if (tid == 0) {
                 st_cg(sh.lab + 2 * static_cast<u64>(root) + k, side[k].base);
                 if (sh.bits)
-                    atomicOr(sh.bits + 2 * static_cast<u64>(root >> 5) + k, 1u << (root & 31));
+                    red_or_u32(sh.bits + 2 * static_cast<u64>(root >> 5) + k, 1u << (root & 31));
                 st_cg(side[k].pp->list, root);
                 st_cg(side[k].pp->sig, static_cast<u64>(1));
                 st_cg(side[k].pp->lvl, 0u);
