@@ -519,9 +519,12 @@ __global__ void flush_kernel(u32 *buf, u64 count, u32 salt) {
 void launch_sample_dispatch(u32 block, u32 items, const SamplerParams &p, u32 grid, cudaStream_t stream) {
     bool done = false;
 #define EBC_LAUNCH(B, I)                                       \
-    if (!done && block == B && items == I) {                   \
-        sample_kernel<B, I><<<grid, B, 0, stream>>>(p);        \
-        done = true;                                           \
+    if (!done && block == B && items == I) {                       \
+        if (p.flags & kFlagUseBitmap)                              \
+            sample_kernel<B, I, true><<<grid, B, 0, stream>>>(p);  \
+        else                                                       \
+            sample_kernel<B, I, false><<<grid, B, 0, stream>>>(p); \
+        done = true;                                               \
     }
     EBC_FOR_EACH_SHAPE(EBC_LAUNCH)
 #undef EBC_LAUNCH
@@ -534,7 +537,7 @@ int occupancy_for(u32 block, u32 items) {
     int per_sm = -1;
 #define EBC_OCC(B, I)                                                                                   \
     if (per_sm < 0 && block == B && items == I)                                                         \
-        EBC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sample_kernel<B, I>, B, 0));
+        EBC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sample_kernel<B, I, true>, B, 0));
     EBC_FOR_EACH_SHAPE(EBC_OCC)
 #undef EBC_OCC
     if (per_sm < 0)
@@ -853,7 +856,6 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
     lap("graph upload");
 
     // ---- launch shape ----
-    m.block = opt.block_threads ? opt.block_threads : 128;
     m.flags = opt.materialize_final_level ? kFlagMaterializeFinal : 0u;
     {
         // Visited bitmaps pay off when single rows are long enough to be probed (hub graphs); on
@@ -863,12 +865,16 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
             max_degree = std::max<std::uint64_t>(max_degree, g.degree(v));
         const char *env = std::getenv("EBC_BITMAP");
         m.hub_graph = max_degree >= 1024;
-        // Adjacency slots per thread per tile.  The kernel's instruction footprint (121 KB at 2, 144 KB at
-        // 4) is a measured bottleneck -- eight CTAs per SM sit in different phases -- so 2 wins wherever
-        // levels are either long rows (hubs) or tiny (small graphs): R-MAT-20 4.19 M -> 4.51 M samples/s,
-        // config 1 14.6 M -> 17.0 M.  Large low-degree graphs expand many narrow multi-row levels whose
-        // cost is per tile (barriers, ranks), where 4 is better (config 3: 158 k vs 147 k).
-        m.items = opt.items_per_thread ? opt.items_per_thread : (m.hub_graph || m.arcs < (u64{1} << 22) ? 2 : 4);
+        // Launch shape (threads cooperating on one sample, adjacency slots per thread per tile), from
+        // sweeps over R-MAT 14/17/20/24, Erdos-Renyi 10^4 and 10^6 and grids 300^2 / 2000^2
+        // (profiles/r01_shapes.txt).  Small graphs mean little work per sample: more, smaller CTAs win
+        // (config 1: 20.0 M samples/s at 128 threads, 27.6 M at 64, 34.4 M at 32).  Four slots per thread
+        // pay once levels are long (R-MAT-20: 4.92 M vs 4.78 M; grid 2000^2: 170 k vs 150 k); on smaller
+        // inputs two are faster (R-MAT-17: 13.7 M vs 11.4 M).
+        m.block = opt.block_threads ? opt.block_threads
+                                    : (m.arcs < (u64{1} << 18) ? 32 : m.arcs < (u64{1} << 21) ? 64 : 128);
+        m.items = opt.items_per_thread ? opt.items_per_thread
+                                       : (m.arcs >= (u64{1} << (m.hub_graph ? 24 : 22)) ? 4 : 2);
         const bool want = env ? std::atoi(env) != 0 : m.hub_graph;
         if (want && !opt.materialize_final_level)
             m.flags |= kFlagUseBitmap;

@@ -65,8 +65,20 @@ __device__ __noinline__ static std::uint64_t philox_draw_device(std::uint32_t dr
     const Philox4 r = philox4x32_10(Philox4{draw, tag, i0, i1}, k0, k1);
     return static_cast<std::uint64_t>(r.x) | (static_cast<std::uint64_t>(r.y) << 32);
 }
-// (0 - bound) % bound, the rejection threshold of next_below: a 64-bit software division, kept out of line.
-__device__ __noinline__ static std::uint64_t lemire_threshold_device(std::uint64_t bound) { return (0 - bound) % bound; }
+// (0 - bound) % bound, the rejection threshold of next_below, out of line and compact.
+// Restoring division, one bit per iteration: the threshold is needed with probability bound / 2^64.
+__device__ __noinline__ static std::uint64_t lemire_threshold_device(std::uint64_t bound) {
+    const std::uint64_t a = 0 - bound;
+    std::uint64_t r = 0;
+#pragma unroll 1
+    for (int i = 63; i >= 0; --i) {
+        const bool top = (r >> 63) != 0;
+        r = (r << 1) | ((a >> i) & 1);
+        if (top || r >= bound)
+            r -= bound;
+    }
+    return r;
+}
 #endif
 
 class SampleStream {

@@ -89,15 +89,29 @@ __device__ __forceinline__ void sat_atomic_add(u64 *p, u64 add, bool small) {
 
 // uniform_below_u128 (sampler.cpp:21-30).  Executed redundantly by every thread
 // of the CTA (the stream state is uniform), so no broadcast is needed.
+// a % b for b >= 2^64 by restoring division, one bit per iteration.  Only the wide rejection sampler
+// below uses it (total weights >= 2^64); the compiler's inline 128-bit division is ~100 instructions
+// per use, and the kernel's instruction footprint is what it is short of (profiles/r01_icache.txt).
+__device__ __noinline__ u128 umod128_compact(u128 a, u128 b) {
+    u128 r = 0;
+#pragma unroll 1
+    for (int i = 127; i >= 0; --i) {
+        const bool top = static_cast<u64>(r >> 127) != 0;
+        r = (r << 1) | ((a >> i) & 1);
+        if (top || r >= b)
+            r -= b;
+    }
+    return r;
+}
 __device__ __noinline__ u128 uniform_below_wide(SampleStream &rng, u128 bound) {
     const u128 all = ~static_cast<u128>(0);
-    const u128 reject_from = all - (all % bound);
+    const u128 reject_from = all - umod128_compact(all, bound);
     for (;;) {
         const u128 hi = rng.next_u64();
         const u128 lo = rng.next_u64();
         const u128 r = (hi << 64) | lo;
         if (r < reject_from)
-            return r % bound;
+            return umod128_compact(r, bound);
     }
 }
 __device__ __forceinline__ u128 uniform_below_u128(SampleStream &rng, u128 bound) {
@@ -236,7 +250,7 @@ template <int BLOCK> __device__ __forceinline__ u64 block_sum_u64(u64 v, u64 *re
 template <int BLOCK>
 __device__ __noinline__ void block_sum_u128(u128 v, u64 &lo, u64 &hi, u64 &ovf, u64 *red) {
     u64 a = static_cast<u64>(v), b = static_cast<u64>(v >> 64), c = 0;
-#pragma unroll
+#pragma unroll 1 // (called a few times per sample: compact beats fast)
     for (int o = 16; o > 0; o >>= 1) {
         const u64 a2 = __shfl_xor_sync(0xffffffffu, a, o);
         const u64 b2 = __shfl_xor_sync(0xffffffffu, b, o);
@@ -257,7 +271,7 @@ __device__ __noinline__ void block_sum_u128(u128 v, u64 &lo, u64 &hi, u64 &ovf, 
         __syncthreads();
         u128 s = 0;
         c = 0;
-#pragma unroll
+#pragma unroll 1
         for (int w = 0; w < BLOCK / 32; ++w) {
             const u128 y = (static_cast<u128>(red[w * 3 + 1]) << 64) | red[w * 3 + 0];
             const u128 t = s + y;
@@ -282,7 +296,7 @@ __device__ __noinline__ u32 block_first_exceeding(u128 w, u128 &running, bool &r
                                                   u64 *red64, u32 *found_lane) {
     u64 a = static_cast<u64>(w), b = static_cast<u64>(w >> 64);
     u32 of = 0;
-#pragma unroll
+#pragma unroll 1
     for (int o = 1; o < 32; o <<= 1) {
         const u64 a2 = __shfl_up_sync(0xffffffffu, a, o);
         const u64 b2 = __shfl_up_sync(0xffffffffu, b, o);
@@ -308,6 +322,7 @@ __device__ __noinline__ u32 block_first_exceeding(u128 w, u128 &running, bool &r
         __syncthreads();
         u128 before = 0;
         bool before_of = false;
+#pragma unroll 1
         for (u32 k = 0; k < warp; ++k) {
             const u128 y = (static_cast<u128>(red64[k * 3 + 1]) << 64) | red64[k * 3 + 0];
             const u128 t = before + y;
@@ -409,7 +424,7 @@ __device__ __noinline__ u64 load_chunk(const SamplerParams &p, const SidePtrs *p
 // updated here (see sum_frontier_degrees).  Returns false on
 // slot-capacity overflow (the sample is then re-run in a large slot).
 // contact_n returns the number of contact vertices appended to `contact`.
-template <int BLOCK, int ITEMS>
+template <int BLOCK, int ITEMS, bool BITS>
 __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e, SideRegs &ex, const SideRegs &ot,
                              u32 *contact, u32 &contact_n, BlockShared<BLOCK, ITEMS> &sh, WorkRegs &wk, u32 &hgen) {
     constexpr int TILE = BLOCK * ITEMS;
@@ -500,7 +515,7 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
                         st_cg(lab + 2 * static_cast<u64>(v[k]) + e, ex.base + idx[k]);
                         st_cg(ex.pp->list + idx[k], v[k]);
                         st_cg(ex.pp->sig + idx[k], sig_u);
-                        if (bits)
+                        if (BITS)
                             red_or_u32(bits + 2 * static_cast<u64>(v[k] >> 5) + e, 1u << (v[k] & 31));
                         if (is_contact[k]) {
                             atomicMin(&sh.min_contact, other_idx[k]);
@@ -641,7 +656,7 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
                             st_cg(lab + 2 * static_cast<u64>(v[k]) + e, ex.base + idx[k]);
                             st_cg(ex.pp->list + idx[k], v[k]);
                             st_cg(ex.pp->sig + idx[k], static_cast<u64>(0));
-                            if (bits)
+                            if (BITS)
                                 red_or_u32(bits + 2 * static_cast<u64>(v[k] >> 5) + e, 1u << (v[k] & 31));
                             if (is_contact[k]) {
                                 atomicMin(&sh.min_contact, other_idx[k]);
@@ -731,7 +746,7 @@ __device__ __forceinline__ u64 sum_frontier_degrees(const SamplerParams &p, cons
 // (possibly > edge_cap, in which case the caller falls back to expand_level).
 // new_slots counts (per thread) the slots whose target is unvisited on this
 // side (= the level's E_lvl, sampler.cpp:97).
-template <int BLOCK, int ITEMS>
+template <int BLOCK, int ITEMS, bool BITS>
 __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bits, int e, const SideRegs &ex, const SideRegs &ot,
                            u32 *edges, u32 edge_cap, BlockShared<BLOCK, ITEMS> &sh, u64 &new_slots,
                            u64 &total_slots) {
@@ -811,7 +826,7 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
             // for both sides; rows are ascending, so a hub row streams through the bitmap instead of
             // touching one 128-byte label line per target.
             u64 both[ITEMS];
-            if (bits) {
+            if (BITS) {
                 const u64 *bits64 = reinterpret_cast<const u64 *>(bits);
 #pragma unroll
                 for (int k = 0; k < ITEMS; ++k)
@@ -826,7 +841,7 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
                 if (!act[k])
                     continue;
                 u32 oi;
-                if (bits) {
+                if (BITS) {
                     if ((half_of(both[k], e) >> (v[k] & 31)) & 1u)
                         continue; // visited before this level
                     new_slots += 1;
@@ -895,7 +910,7 @@ __device__ u32 meet_from_edges(const u32 *edges, u32 m, u32 olo, u32 ohi, u32 *m
         sum[q] = 0;
         first[q] = i < m;
     }
-#pragma unroll 2
+#pragma unroll 1
     for (u32 j = 0; j < m; ++j) {
         const u32 vj = sh.f_v[j];
         const u64 kj = sh.f_key[j], sj = sh.f_s[j];
@@ -927,7 +942,7 @@ __device__ u32 meet_from_edges(const u32 *edges, u32 m, u32 olo, u32 ohi, u32 *m
         member[q] = i < m && sh.f_o[i] - olo < ohi - olo;
         rank[q] = 0;
     }
-#pragma unroll 2
+#pragma unroll 1
     for (u32 j = 0; j < m; ++j) {
         const u64 kj = sh.f_key[j];
         const bool in_range = sh.f_o[j] - olo < ohi - olo;
@@ -1083,6 +1098,7 @@ __device__ void walk_side(const SamplerParams &p, const u32 *lab, int x, const S
                     const u32 mypos = have ? sh.pred_pos[tid] : 0xffffffffu;
                     const u64 mysig = have ? sh.pred_sig[tid] : 0;
                     u128 before = 0;
+#pragma unroll 1
                     for (u32 q = 0; q < npred; ++q)
                         if (sh.pred_pos[q] < mypos)
                             before += sh.pred_sig[q];
@@ -1143,7 +1159,9 @@ template <int BLOCK> constexpr int min_blocks_per_sm() {
     return (EBC_WARPS_PER_SM * 32) / BLOCK > 0 ? (EBC_WARPS_PER_SM * 32) / BLOCK : 1;
 }
 
-template <int BLOCK, int ITEMS>
+// BITS: the launch uses visited bitmaps (kFlagUseBitmap); a template parameter so that each kernel
+// carries only its own variant of the probe code -- the instruction footprint matters, see above.
+template <int BLOCK, int ITEMS, bool BITS>
 __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kernel(const SamplerParams p) {
     __shared__ BlockShared<BLOCK, ITEMS> sh;
     const u32 tid = threadIdx.x;
@@ -1156,7 +1174,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             u32 got = 0xffffffffu;
             while (got == 0xffffffffu) {
                 const unsigned long long h = atomicAdd(p.ring_pos, 1ull);
-                got = atomicExch(p.ring + (h % p.ring_size), 0xffffffffu);
+                got = atomicExch(p.ring + (static_cast<u32>(h) % p.ring_size), 0xffffffffu); // (any position works)
             }
             __threadfence();
             sh.bcast[2] = got;
@@ -1176,7 +1194,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
         if (tid == 0) {
             if (k == 0) {
                 sh.lab = p.lab + slot * 2 * n; // lab[2v + side]
-                sh.bits = (p.flags & kFlagUseBitmap) ? p.bits + slot * 2 * p.bit_words : nullptr;
+                sh.bits = BITS ? p.bits + slot * 2 * p.bit_words : nullptr;
                 sh.contact = p.contact + slot * 6 * p.aux_cap; // 2*aux_cap words: contacts / contact edges
                 sh.meetbuf = sh.contact + 2 * p.aux_cap;       // 4*aux_cap words: ordered meet set
             }
@@ -1277,7 +1295,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             side[k].pending = __ldg(p.offsets + root + 1) - __ldg(p.offsets + root);
             if (tid == 0) {
                 st_cg(sh.lab + 2 * static_cast<u64>(root) + k, side[k].base);
-                if (sh.bits)
+                if (BITS)
                     red_or_u32(sh.bits + 2 * static_cast<u64>(root >> 5) + k, 1u << (root & 31));
                 st_cg(side[k].pp->list, root);
                 st_cg(side[k].pp->sig, static_cast<u64>(1));
@@ -1319,7 +1337,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             if (!(p.flags & kFlagMaterializeFinal) && edge_cap() > 0 && side[e].pending >= kProbeMinSlots &&
                 static_cast<u64>(side[e].depth) + 2 <= p.aux_cap) {
                 u64 new_slots = 0, total_slots = 0;
-                edge_n = probe_level<BLOCK, ITEMS>(p, sh.lab, sh.bits, e, side[e], side[1 - e], sh.contact, edge_cap(), sh, new_slots,
+                edge_n = probe_level<BLOCK, ITEMS, BITS>(p, sh.lab, sh.bits, e, side[e], side[1 - e], sh.contact, edge_cap(), sh, new_slots,
                                                    total_slots);
                 EBC_PH(2)
                 if (edge_n > 0 && edge_n <= edge_cap()) {
@@ -1338,7 +1356,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
                 }
                 __syncthreads(); // no sh.contact (or too many sh.contact edges): expand normally
             }
-            if (!expand_level<BLOCK, ITEMS>(p, sh.lab, sh.bits, e, side[e], side[1 - e], sh.contact, contact_n, sh, wk, hgen)) {
+            if (!expand_level<BLOCK, ITEMS, BITS>(p, sh.lab, sh.bits, e, side[e], side[1 - e], sh.contact, contact_n, sh, wk, hgen)) {
                 aborted = true;
                 break;
             }
@@ -1483,7 +1501,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
         }
         if (p.records && tid == 0)
             p.records[local] = sh.rec;
-        if (sh.bits) { // clear the bitmap words of every settled vertex (both sides share the 8-byte word)
+        if (BITS) { // clear the bitmap words of every settled vertex (both sides share the 8-byte word)
             u64 *bits64 = reinterpret_cast<u64 *>(sh.bits);
 #pragma unroll 1
             for (int k = 0; k < 2; ++k) {
@@ -1546,7 +1564,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             __threadfence();
             for (;;) {
                 const unsigned long long t = atomicAdd(p.ring_pos + 1, 1ull);
-                if (atomicCAS(p.ring + (t % p.ring_size), 0xffffffffu, static_cast<u32>(slot)) == 0xffffffffu)
+                if (atomicCAS(p.ring + (static_cast<u32>(t) % p.ring_size), 0xffffffffu, static_cast<u32>(slot)) == 0xffffffffu)
                     break;
             }
         }
