@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -48,6 +49,7 @@ public:
                 idle_.erase(it);
                 idle_bytes_ -= bytes;
                 live_[p] = {dev, bytes};
+                live_bytes_ += bytes;
                 return p;
             }
         }
@@ -63,6 +65,7 @@ public:
         cuda_check(e, "cudaMalloc", __FILE__, __LINE__);
         std::lock_guard<std::mutex> lk(mu_);
         live_[p] = {dev, bytes};
+        live_bytes_ += bytes;
         return p;
     }
     void free(void *p) {
@@ -76,6 +79,7 @@ public:
         }
         const auto key = it->second;
         live_.erase(it);
+        live_bytes_ -= key.second;
         if (idle_bytes_ + key.second > kMaxIdleBytes) {
             ++frees_;
             cudaFree(p);
@@ -89,9 +93,27 @@ public:
         std::fprintf(stderr, "[ebc] pool %s: %zu cudaMalloc (%.1f MB), %zu cudaFree, idle %.1f MB in %zu buffers, live %zu\n", where,
                      mallocs_, malloc_bytes_ / 1e6, frees_, idle_bytes_ / 1e6, idle_.size(), live_.size());
     }
-    std::size_t idle_bytes() {
+    std::size_t live_bytes() {
         std::lock_guard<std::mutex> lk(mu_);
-        return idle_bytes_;
+        return live_bytes_;
+    }
+    // Device memory this process can use = free + everything the pool holds.  cudaMemGetInfo was measured
+    // at 8-90 ms per call with ~14 GB allocated -- a sixth of a whole run on a small input -- so the
+    // figure is cached per device and refreshed every few seconds (an allocation that fails because
+    // somebody else took the memory still frees the idle buffers and retries, see alloc()).
+    std::size_t capacity() {
+        int dev = 0;
+        EBC_CUDA(cudaGetDevice(&dev));
+        const auto now = std::chrono::steady_clock::now();
+        std::lock_guard<std::mutex> lk(mu_);
+        auto it = capacity_.find(dev);
+        if (it != capacity_.end() && now - it->second.first < std::chrono::seconds(5))
+            return it->second.second;
+        size_t free_b = 0, total_b = 0;
+        EBC_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        const std::size_t cap = free_b + idle_bytes_ + live_bytes_;
+        capacity_[dev] = {now, cap};
+        return cap;
     }
     void release_idle() {
         std::lock_guard<std::mutex> lk(mu_);
@@ -106,7 +128,8 @@ private:
     std::mutex mu_;
     std::map<void *, std::pair<int, std::size_t>> live_;
     std::multimap<std::pair<int, std::size_t>, void *> idle_;
-    std::size_t idle_bytes_ = 0;
+    std::size_t idle_bytes_ = 0, live_bytes_ = 0;
+    std::map<int, std::pair<std::chrono::steady_clock::time_point, std::size_t>> capacity_;
     std::size_t mallocs_ = 0, malloc_bytes_ = 0, frees_ = 0;
 };
 
@@ -308,6 +331,9 @@ __global__ void widen_kernel(const u32 *in, u64 *out, u64 words) {
 // frontier vertex, lanes stride the row; the level loop runs on the device
 // stream without host round trips (each launch reads the queue size written by
 // the previous one and exits when it is empty).
+constexpr u32 kBfsBigRow = 8192;  // adjacency entries
+constexpr u32 kBfsBigCap = 2048;  // set-aside rows per level (further ones are expanded in place)
+
 struct BfsState {
     u32 queue_size[2];
     u32 depth;
@@ -319,6 +345,10 @@ struct BfsState {
     u32 bottom_up;        // mode of the level about to run
     u32 have_queue;       // the frontier of the level about to run exists as a queue
     u32 bu_found;         // vertices settled by the bottom-up pass of this level
+    // top-down levels: frontier vertices whose row is too long for one warp are set aside and expanded
+    // by the whole grid (bfs_big_rows_kernel) -- a sweep that starts at a hub is otherwise one warp's work
+    u32 big_count;
+    u32 big[kBfsBigCap];
 };
 
 __global__ void __launch_bounds__(256) bfs_level_kernel(const u64 *offsets, const u32 *targets, u32 *dist,
@@ -335,6 +365,17 @@ __global__ void __launch_bounds__(256) bfs_level_kernel(const u64 *offsets, cons
     for (u32 i = warp; i < count; i += warps) {
         const u32 u = in[i];
         const u64 beg = offsets[u], end = offsets[u + 1];
+        if (end - beg > kBfsBigRow) {
+            u32 slot = 0;
+            if (lane == 0)
+                slot = atomicAdd(&st->big_count, 1u);
+            slot = __shfl_sync(0xffffffffu, slot, 0);
+            if (slot < kBfsBigCap) {
+                if (lane == 0)
+                    st->big[slot] = u;
+                continue;
+            }
+        }
         for (u64 k = beg + lane; k < end; k += 32) {
             const u32 v = targets[k];
             if (dist[v] == 0xffffffffu && atomicCAS(dist + v, 0xffffffffu, level + 1) == 0xffffffffu) {
@@ -347,6 +388,36 @@ __global__ void __launch_bounds__(256) bfs_level_kernel(const u64 *offsets, cons
     for (int o = 16; o > 0; o >>= 1)
         arcs += __shfl_xor_sync(0xffffffffu, arcs, o);
     if (lane == 0 && arcs)
+        atomicAdd(reinterpret_cast<unsigned long long *>(&st->frontier_arcs[(level + 1) & 1]), static_cast<unsigned long long>(arcs));
+}
+
+// Second half of a top-down level: the rows set aside by bfs_level_kernel, each spread over the whole grid.
+__global__ void __launch_bounds__(256) bfs_big_rows_kernel(const u64 *offsets, const u32 *targets, u32 *dist,
+                                                           u32 *queue0, u32 *queue1, BfsState *st, u32 level) {
+    if (st->done || st->bottom_up)
+        return;
+    const u32 rows = st->big_count < kBfsBigCap ? st->big_count : kBfsBigCap;
+    if (rows == 0)
+        return;
+    u32 *out = (level & 1) ? queue0 : queue1;
+    const u64 threads = static_cast<u64>(gridDim.x) * blockDim.x;
+    const u64 me = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x;
+    u64 arcs = 0;
+    for (u32 r = 0; r < rows; ++r) {
+        const u32 u = st->big[r];
+        const u64 beg = offsets[u], end = offsets[u + 1];
+        for (u64 k = beg + me; k < end; k += threads) {
+            const u32 v = targets[k];
+            if (dist[v] == 0xffffffffu && atomicCAS(dist + v, 0xffffffffu, level + 1) == 0xffffffffu) {
+                const u32 pos = atomicAdd(&st->queue_size[(level + 1) & 1], 1u);
+                out[pos] = v;
+                arcs += offsets[v + 1] - offsets[v];
+            }
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1)
+        arcs += __shfl_xor_sync(0xffffffffu, arcs, o);
+    if ((threadIdx.x & 31) == 0 && arcs)
         atomicAdd(reinterpret_cast<unsigned long long *>(&st->frontier_arcs[(level + 1) & 1]), static_cast<unsigned long long>(arcs));
 }
 
@@ -401,6 +472,7 @@ __global__ void bfs_advance_kernel(BfsState *st, u32 level, u64 arcs_total, u32 
     const bool next_is_queue = !st->bottom_up;
     st->queue_size[level & 1] = 0;
     st->bu_found = 0;
+    st->big_count = 0;
     st->frontier_arcs[level & 1] = 0;
     if (next == 0) {
         st->done = 1;
@@ -892,6 +964,7 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
         lap("dense numbering");
     }
     const int per_sm = occupancy_for(m.block, m.items);
+    lap("occupancy query");
     if (per_sm < 1)
         throw CudaError("sampling kernel does not fit on an SM");
     u64 cap = opt.slot_capacity ? std::min<u64>(opt.slot_capacity, g.n)
@@ -901,12 +974,13 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
     // path; measured in profiles/r01_capacity_sweep.txt.)
     cap = std::max<u64>(cap, 2);
     u64 slots = opt.slots ? opt.slots : static_cast<u64>(per_sm) * m.sm_count;
-    size_t free_b = 0, total_b = 0;
-    EBC_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const u64 capacity = pool().capacity();
+    const u64 live = pool().live_bytes();
+    lap("memory query");
     const u64 fixed = (g.n + 1) * (4 * 2 + 8 + 8 + 16 + 12) + (u64{256} << 20) + kOverflowCap * 4 +
                       (cap < g.n ? kLargeSlots * SlotArrays::bytes_per_slot(g.n, g.n) : 0);
     // Buffers cached by the pool are reusable (or released on demand), so they count as free.
-    const u64 avail = static_cast<u64>(free_b) + pool().idle_bytes();
+    const u64 avail = capacity > live ? capacity - live : 0;
     const u64 budget = avail > fixed ? (avail - fixed) / 10 * 8 : 0;
     const u64 per_slot = SlotArrays::bytes_per_slot(g.n, cap);
     if (!opt.slots && slots * per_slot > budget)
@@ -1272,15 +1346,23 @@ BfsSummary CudaSampler::bfs(std::uint32_t source, std::uint32_t *dist_out) {
     EBC_CUDA(cudaMemsetAsync(m.d_best, 0, 8, st));
     const u32 grid = static_cast<u32>(m.sm_count) * 8;
     const u32 allow_bu = m.hub_graph ? 1u : 0u; // low-degree graphs stay top-down (2 launches per level)
-    BfsState host{};
+    // Only the head of the state (done, reached) comes back per round trip; levels are enqueued in
+    // batches of 8, 16, 32, 32 ...: launches after the search is done are no-ops, but not free.
+    struct { u32 queue_size[2]; u32 depth; u32 done; u64 reached; } host{};
+    static_assert(offsetof(BfsState, reached) == 16, "BfsState head layout");
+    int batch = 8;
     for (u32 level = 0;;) {
-        for (int k = 0; k < 32; ++k, ++level) { // 32 levels per host round trip
+        for (int k = 0; k < batch; ++k, ++level) {
             if (allow_bu) {
                 bfs_rebuild_queue_kernel<<<grid, 256, 0, st>>>(m.d_dist, m.n, m.d_queue[0], m.d_queue[1], m.d_bfs, level);
                 bfs_bottom_up_kernel<<<grid, 256, 0, st>>>(m.d_offsets, m.d_targets, m.d_dist, m.n, m.d_bfs, level);
                 m.launches += 2;
             }
             bfs_level_kernel<<<grid, 256, 0, st>>>(m.d_offsets, m.d_targets, m.d_dist, m.d_queue[0], m.d_queue[1], m.d_bfs, level);
+            if (m.hub_graph) { // rows above kBfsBigRow exist only there
+                bfs_big_rows_kernel<<<grid, 256, 0, st>>>(m.d_offsets, m.d_targets, m.d_dist, m.d_queue[0], m.d_queue[1], m.d_bfs, level);
+                ++m.launches;
+            }
             bfs_advance_kernel<<<1, 1, 0, st>>>(m.d_bfs, level, m.arcs, allow_bu);
             m.launches += 2;
         }
@@ -1289,6 +1371,7 @@ BfsSummary CudaSampler::bfs(std::uint32_t source, std::uint32_t *dist_out) {
         EBC_CUDA(cudaStreamSynchronize(st));
         if (host.done)
             break;
+        batch = batch < 32 ? batch * 2 : 32;
     }
     bfs_farthest_kernel<<<grid, 256, 0, st>>>(m.d_dist, m.n, m.d_best);
     ++m.launches;
