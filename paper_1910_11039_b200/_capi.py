@@ -63,6 +63,11 @@ SIGNATURES = {
     "ebc_graph_load": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]),
     "ebc_graph_save": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int]),
     "ebc_graph_lcc": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "ebc_graph_lcc_device": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
+    "ebc_graph_from_edges_device": (C.c_int, [C.c_uint64, u64p, u64p, C.c_uint64, C.c_int, C.c_int,
+                                              C.POINTER(C.c_void_p)]),
+    "ebc_gen_rmat_device": (C.c_int, [C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_double,
+                                      C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     "ebc_graph_num_vertices": (C.c_uint64, [C.c_void_p]),
     "ebc_graph_num_edges": (C.c_uint64, [C.c_void_p]),
     "ebc_graph_offsets": (u64p, [C.c_void_p]),

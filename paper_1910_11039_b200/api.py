@@ -109,6 +109,16 @@ class Graph:
         return cls._new(_capi.load().ebc_graph_from_edges, n, _p(s, _capi.u64p), _p(d, _capi.u64p), len(s))
 
     @classmethod
+    def from_edges_device(cls, n: int, src, dst, take_lcc: bool = False, device: int = -1) -> "Graph":
+        """from_edges (and optionally the largest component) computed on the GPU; same result."""
+        s = np.ascontiguousarray(src, dtype=np.uint64)
+        d = np.ascontiguousarray(dst, dtype=np.uint64)
+        if s.shape != d.shape:
+            raise ConfigError("from_edges: src and dst differ in length")
+        return cls._new(_capi.load().ebc_graph_from_edges_device, n, _p(s, _capi.u64p), _p(d, _capi.u64p), len(s),
+                        int(take_lcc), device)
+
+    @classmethod
     def from_csr(cls, offsets, targets, original_ids=None, validate=True) -> "Graph":
         o = np.ascontiguousarray(offsets, dtype=np.uint64)
         t = np.ascontiguousarray(targets, dtype=np.uint32)
@@ -124,7 +134,10 @@ class Graph:
     def save(self, path: str, binary: bool = False) -> None:
         _check(_capi.load().ebc_graph_save(self._h, str(path).encode(), int(binary)))
 
-    def largest_connected_component(self) -> "Graph":
+    def largest_connected_component(self, device: Optional[int] = None) -> "Graph":
+        """largest_connected_component (graph.cpp:229-290); device=ordinal (or -1) computes it on the GPU."""
+        if device is not None:
+            return self._new(_capi.load().ebc_graph_lcc_device, self._h, device)
         return self._new(_capi.load().ebc_graph_lcc, self._h)
 
     @property
@@ -158,6 +171,12 @@ def gen_erdos_renyi(n: int, m: int, seed: int) -> Graph:
 def gen_rmat(scale: int, edge_factor: int = 16, a=0.57, b=0.19, c=0.19, d=0.05, seed: int = 1) -> Graph:
     """R-MAT with gen_rmat's quadrant convention (rmat.cpp:24-42)."""
     return Graph._new(_capi.load().ebc_gen_rmat, scale, edge_factor, a, b, c, d, seed)
+
+
+def gen_rmat_device(scale: int, edge_factor: int = 16, a=0.57, b=0.19, c=0.19, d=0.05, seed: int = 1,
+                    take_lcc: bool = False, device: int = -1) -> Graph:
+    """gen_rmat (and optionally the largest component) generated and canonicalised on the GPU; same graph."""
+    return Graph._new(_capi.load().ebc_gen_rmat_device, scale, edge_factor, a, b, c, d, seed, int(take_lcc), device)
 
 
 def gen_grid(width: int, height: int, delete_prob: float, shortcut_fraction: float, seed: int) -> Graph:

@@ -14,9 +14,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libebc_b200.so")
 
-SOURCES = ["capi.cpp", "cuda_sampler.cu", "host_graph.cpp", "host_stopping.cpp", "host_diameter.cpp",
+SOURCES = ["capi.cpp", "cuda_sampler.cu", "device_graph.cu", "host_graph.cpp", "host_stopping.cpp", "host_diameter.cpp",
            "epoch_driver.cpp", "host_scores.cpp"]
-HEADERS = ["cuda_sampler.hpp", "device_types.cuh", "epoch_driver.hpp", "host_common.hpp", "host_scores.hpp", "philox.cuh",
+HEADERS = ["cuda_sampler.hpp", "device_graph.hpp", "device_types.cuh", "epoch_driver.hpp", "host_common.hpp", "host_scores.hpp", "philox.cuh",
            "sampler_kernels.cuh", os.path.join("..", "..", "include", "ebc_b200.h")]
 
 

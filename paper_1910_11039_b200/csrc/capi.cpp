@@ -10,6 +10,7 @@
 #include <string>
 
 #include "cuda_sampler.hpp"
+#include "device_graph.hpp"
 #include "epoch_driver.hpp"
 #include "host_common.hpp"
 #include "host_scores.hpp"
@@ -198,6 +199,40 @@ ebc_status ebc_gen_rmat(int scale, int edge_factor, double a, double b, double c
         need(out, "ebc_gen_rmat: null out");
         auto h = std::make_unique<ebc_graph>();
         h->g = gen_rmat(scale, edge_factor, a, b, c, d, seed);
+        *out = h.release();
+    });
+}
+
+ebc_status ebc_gen_rmat_device(int scale, int edge_factor, double a, double b, double c, double d, uint64_t seed,
+                               int take_lcc, int device, ebc_graph **out) {
+    return guarded([&] {
+        need(out, "ebc_gen_rmat_device: null out");
+        auto h = std::make_unique<ebc_graph>();
+        h->g = device_gen_rmat(scale, edge_factor, a, b, c, d, seed, take_lcc != 0, device);
+        *out = h.release();
+    });
+}
+
+ebc_status ebc_graph_from_edges_device(uint64_t n, const uint64_t *src, const uint64_t *dst, uint64_t count,
+                                       int take_lcc, int device, ebc_graph **out) {
+    return guarded([&] {
+        need(out, "ebc_graph_from_edges_device: null out");
+        if (count) {
+            need(src, "ebc_graph_from_edges_device: null src");
+            need(dst, "ebc_graph_from_edges_device: null dst");
+        }
+        auto h = std::make_unique<ebc_graph>();
+        h->g = device_graph_from_edges(n, src, dst, count, take_lcc != 0, device);
+        *out = h.release();
+    });
+}
+
+ebc_status ebc_graph_lcc_device(const ebc_graph *g, int device, ebc_graph **out) {
+    return guarded([&] {
+        need(g, "ebc_graph_lcc_device: null graph");
+        need(out, "ebc_graph_lcc_device: null out");
+        auto h = std::make_unique<ebc_graph>();
+        h->g = device_graph_lcc(g->g, device);
         *out = h.release();
     });
 }

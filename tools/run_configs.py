@@ -7,12 +7,12 @@ import paper_1910_11039_b200 as ebc
 def build(c):
     t = time.time()
     if c == 1: g = ebc.gen_erdos_renyi(10000, 50000, 1); eps = 0.01
-    elif c == 2: g = ebc.gen_rmat(20, 16, seed=2); eps = 0.005
+    elif c == 2: g = ebc.gen_rmat_device(20, 16, seed=2); eps = 0.005
     elif c == 3: g = ebc.gen_grid(2000, 2000, 0.05, 0.001, 3); eps = 0.01
-    elif c == 4: g = ebc.gen_rmat(24, 16, seed=4); eps = 0.001
-    elif c == 5: g = ebc.gen_rmat(26, 16, seed=5); eps = 0.001
+    elif c == 4: g = ebc.gen_rmat_device(24, 16, seed=4); eps = 0.001
+    elif c == 5: g = ebc.gen_rmat_device(26, 16, seed=5); eps = 0.001
     t1 = time.time() - t
-    g = g.largest_connected_component()
+    g = g.largest_connected_component(device=-1 if c in (2, 4, 5) else None)  # same graphs as the host path, in seconds
     print(f"config {c}: n={g.num_vertices} m={g.num_edges} gen {t1:.1f}s lcc {time.time()-t-t1:.1f}s", flush=True)
     return g, eps
 
