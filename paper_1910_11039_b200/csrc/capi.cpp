@@ -99,6 +99,9 @@ public:
                       int bound) override {
         s_.set_stopping(eps, omega, dl, du, bound);
     }
+    void set_stopping_uniform(double eps, std::uint64_t omega, double delta_each, std::uint64_t, int bound) override {
+        s_.set_stopping_uniform(eps, omega, delta_each, bound);
+    }
     void fold_async(int frame, AllreduceHook allreduce, void *user) override {
         s_.fold_and_check_async(frame, allreduce, user);
     }

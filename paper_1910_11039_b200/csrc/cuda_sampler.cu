@@ -573,6 +573,14 @@ __global__ void __launch_bounds__(256) dense_rows_kernel(const u64 *ext_offsets,
     }
 }
 
+__global__ void __launch_bounds__(256) fill_two_kernel(double *a, double *b, u64 count, double value) {
+    for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < count;
+         i += static_cast<u64>(gridDim.x) * blockDim.x) {
+        a[i] = value;
+        b[i] = value;
+    }
+}
+
 __global__ void flush_kernel(u32 *buf, u64 count, u32 salt) {
     for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < count;
          i += static_cast<u64>(gridDim.x) * blockDim.x)
@@ -1194,6 +1202,21 @@ void CudaSampler::set_stopping(double eps, std::uint64_t omega, const double *de
     bound_log_terms(delta_upper, m.n, bound, up.data());
     EBC_CUDA(cudaMemcpy(m.d_log_lower, lo.data(), m.n * 8, cudaMemcpyHostToDevice));
     EBC_CUDA(cudaMemcpy(m.d_log_upper, up.data(), m.n * 8, cudaMemcpyHostToDevice));
+    m.stop.eps = eps;
+    m.stop.omega = omega;
+    m.stop.log_lower = m.d_log_lower;
+    m.stop.log_upper = m.d_log_upper;
+    m.stop.bound = bound;
+    m.stop.have = 1;
+}
+
+void CudaSampler::set_stopping_uniform(double eps, std::uint64_t omega, double delta_each, int bound) {
+    Impl &m = *impl_;
+    require(bound == 0 || bound == 1, "set_stopping: unknown bound kind");
+    double term = 0.0;
+    bound_log_terms(&delta_each, 1, bound, &term); // the host libm's log, as for per-vertex values
+    fill_two_kernel<<<static_cast<u32>(m.sm_count) * 4, 256, 0, m.s_agg>>>(m.d_log_lower, m.d_log_upper, m.n, term);
+    EBC_CUDA(cudaGetLastError());
     m.stop.eps = eps;
     m.stop.omega = omega;
     m.stop.log_lower = m.d_log_lower;

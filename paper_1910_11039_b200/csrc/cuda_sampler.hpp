@@ -51,6 +51,8 @@ public:
 
     void set_stopping(double eps, std::uint64_t omega, const double *delta_lower,
                       const double *delta_upper, int bound);
+    // delta_lower[v] == delta_upper[v] == delta_each for all v: the log terms are filled on the device.
+    void set_stopping_uniform(double eps, std::uint64_t omega, double delta_each, int bound);
     // Asynchronous part of fold+check on the aggregation stream; wait_fold() returns the decision.
     void fold_and_check_async(int frame, AllreduceFn allreduce, void *user);
     bool wait_fold(int frame, std::uint64_t *tau_out = nullptr);

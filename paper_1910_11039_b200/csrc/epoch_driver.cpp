@@ -82,10 +82,11 @@ RunOutput run_pipeline(const HostGraph &g, const RunConfig &cfg, SamplerBackend 
 
     // Phase 3: calibration (engine.cpp:321-357): non-adaptive samples from an
     // independent stream, blocking aggregation, failure-probability allocation.
-    std::vector<double> delta_lower(n), delta_upper(n);
     {
         const double t0 = now_s();
-        std::vector<std::uint64_t> calib(n + 1, 0);
+        // the uniform allocator uses no calibration counts (stopping.cpp:50,72-78): no arrays needed
+        const bool uniform = cfg.allocator == 0;
+        std::vector<std::uint64_t> calib(uniform ? 1 : n + 1, 0);
         if (cfg.calib_samples > 0) {
             std::uint64_t lo, cnt;
             shard_range(0, cfg.calib_samples, cfg.rank, cfg.world_size, &lo, &cnt);
@@ -93,15 +94,20 @@ RunOutput run_pipeline(const HostGraph &g, const RunConfig &cfg, SamplerBackend 
             be.fold_async(0, hook, cfg.allreduce_user);
             std::uint64_t tau = 0;
             be.wait_fold(0, &tau);
-            if (cfg.allocator == 0)
-                calib[0] = tau; // the uniform allocator uses no calibration counts (stopping.cpp:50,72-78)
+            if (uniform)
+                calib[0] = tau;
             else
                 be.read_state(calib.data());
             be.clear();
         }
         st.calibration_samples = calib[0];
-        calibrate(calib.data(), n, cfg.delta, cfg.allocator, delta_lower.data(), delta_upper.data());
-        be.set_stopping(cfg.eps, omega, delta_lower.data(), delta_upper.data(), cfg.bound);
+        if (uniform) {
+            be.set_stopping_uniform(cfg.eps, omega, calibrate_uniform_value(n, cfg.delta), n, cfg.bound);
+        } else {
+            std::vector<double> delta_lower(n), delta_upper(n);
+            calibrate(calib.data(), n, cfg.delta, cfg.allocator, delta_lower.data(), delta_upper.data());
+            be.set_stopping(cfg.eps, omega, delta_lower.data(), delta_upper.data(), cfg.bound);
+        }
         st.calibration_s = now_s() - t0;
     }
 

@@ -70,6 +70,12 @@ public:
                         int frame) = 0;
     virtual void set_stopping(double eps, std::uint64_t omega, const double *delta_lower,
                               const double *delta_upper, int bound) = 0;
+    // Same with delta_lower[v] == delta_upper[v] == delta_each for every vertex (uniform allocator);
+    // a backend may override it to skip the per-vertex arrays.
+    virtual void set_stopping_uniform(double eps, std::uint64_t omega, double delta_each, std::uint64_t n, int bound) {
+        const std::vector<double> each(n, delta_each);
+        set_stopping(eps, omega, each.data(), each.data(), bound);
+    }
     // Asynchronous: (allreduce) -> S += frame, frame := 0 -> check_stop(S).
     virtual void fold_async(int frame, AllreduceHook allreduce, void *user) = 0;
     // Completes the fold of `frame`; returns the stop decision and tau of S.

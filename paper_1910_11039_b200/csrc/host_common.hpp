@@ -82,6 +82,8 @@ void calibrate(const std::uint64_t *calib_words, std::uint64_t n, double delta, 
                double *delta_lower, double *delta_upper);
 // ln(1/delta_v) (Hoeffding) or ln(2/delta_v) (empirical Bernstein), evaluated with the host libm.
 void bound_log_terms(const double *delta_v, std::uint64_t n, int bound, double *out);
+// Per-vertex, per-side failure probability of the uniform allocator (what calibrate() writes n times).
+double calibrate_uniform_value(std::uint64_t n, double delta);
 
 // host_diameter.cpp
 struct BfsSummary {

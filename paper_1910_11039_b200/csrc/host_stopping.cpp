@@ -71,6 +71,22 @@ void calibrate(const std::uint64_t *calib, std::uint64_t n, double delta, int al
     }
 }
 
+// The value every entry of lower[] and upper[] gets from calibrate() under the uniform allocator,
+// including the budget guard (same operations in the same order, without the two arrays).
+double calibrate_uniform_value(std::uint64_t n, double delta) {
+    require(n >= 1, "calibrate: empty graph");
+    require(delta > 0 && delta < 1, "calibrate: bad delta");
+    double per_side = delta / (2.0 * static_cast<double>(n));
+    long double total = 0.0L;
+    for (std::uint64_t v = 0; v < n; ++v)
+        total += static_cast<long double>(per_side) + per_side;
+    if (total > static_cast<long double>(delta)) {
+        const double scale = static_cast<double>(static_cast<long double>(delta) / total) * (1.0 - 1e-12);
+        per_side *= scale;
+    }
+    return per_side;
+}
+
 void bound_log_terms(const double *delta_v, std::uint64_t n, int bound, double *out) {
     // Equal inputs give equal outputs, so the last (input, output) pair is reused: under the uniform
     // allocator all n values are identical and this is one log() instead of n.
