@@ -15,7 +15,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libebc_b200.so")
 
 SOURCES = ["capi.cpp", "cuda_sampler.cu", "device_graph.cu", "host_graph.cpp", "host_stopping.cpp", "host_diameter.cpp",
-           "epoch_driver.cpp", "host_scores.cpp"]
+           "epoch_driver.cpp", "host_scores.cpp", "pinned_pool.cpp"]
 HEADERS = ["cuda_sampler.hpp", "device_graph.hpp", "device_types.cuh", "epoch_driver.hpp", "host_common.hpp", "host_scores.hpp", "philox.cuh",
            "sampler_kernels.cuh", os.path.join("..", "..", "include", "ebc_b200.h")]
 

@@ -685,6 +685,7 @@ constexpr u64 kLargeSlots = 8; // full-capacity slots of the re-run pass
 void release_device_cache() {
     pool().release_idle();
     handles().release_idle();
+    pinned_release_idle();
 }
 
 struct CudaSampler::Impl {

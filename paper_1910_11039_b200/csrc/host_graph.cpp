@@ -96,6 +96,11 @@ inline std::uint64_t arc_key(std::uint64_t u, std::uint64_t v) { return (u << 32
 
 } // namespace
 
+// Host-only builds: no pinned memory (the product library links the strong definitions of pinned_pool.cpp).
+__attribute__((weak)) void *pinned_alloc(std::size_t) { return nullptr; }
+__attribute__((weak)) bool pinned_free(void *) { return false; }
+__attribute__((weak)) void pinned_release_idle() {}
+
 // Sorted unique arc keys -> CSR.  Because keys sort by (u, v), rows come out
 // ascending with no further work.
 HostGraph graph_from_arc_keys(std::uint64_t n, std::vector<std::uint64_t> &&keys_in) {
