@@ -764,64 +764,69 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
         t_total += T;
         // Software pipeline: the targets of tile i+1 are requested before the visit words of tile i,
         // so the two dependent loads of a slot (target id -> visit word) overlap across tiles.
-        u32 v_n[ITEMS], kk_n[ITEMS];
-        int owner_n[ITEMS];
-        bool act_n[ITEMS];
-        // The slots of a thread ascend (over k, then over tiles), so the owner row of a slot is searched
-        // upwards from the owner of the thread's previous slot: one shared-memory compare for the common
-        // case of a long row, a galloping + binary search otherwise.
-        auto fetch = [&](u64 t0, int hint) {
+        // A tile that lies inside one row -- the usual case behind a hub -- addresses its slots as
+        // row[j]; otherwise every slot finds its owner row by galloping upwards from the tile's first
+        // row (slots ascend with k).  Only a contact edge needs (owner, index in row) again, and looks
+        // them up on its own: the pipeline carries nothing but the target ids.
+        u32 v_n[ITEMS];
+        u32 act_n = 0; // bit k: slot k of the requested tile exists
+        int row = 0;   // owner row of the requested tile's first slot (uniform, non-decreasing)
+        auto fetch = [&](u64 t0) {
+            while (sh.c_scan[row + 1] <= t0) // c_scan[BLOCK] = T > t0
+                ++row;
+            const u64 t_end = t0 + TILE < T ? t0 + TILE : T;
+            act_n = 0;
+            if (sh.c_scan[row + 1] >= t_end) {
+                const u32 *rowp = p.targets + (sh.c_beg[row] - sh.c_scan[row]);
 #pragma unroll
-            for (int k = 0; k < ITEMS; ++k) {
-                const u64 j = t0 + static_cast<u64>(k) * BLOCK + tid;
-                act_n[k] = j < T;
-                v_n[k] = 0;
-                kk_n[k] = 0;
-                owner_n[k] = hint;
-                if (act_n[k]) {
-                    int lo = hint, hi = hint + 1, step = 1; // owner row: last r with c_scan[r] <= j; c_scan[BLOCK] = T > j
-                    while (sh.c_scan[hi] <= j) {
-                        lo = hi;
-                        hi = hi + step < BLOCK ? hi + step : BLOCK;
-                        step <<= 1;
+                for (int k = 0; k < ITEMS; ++k) {
+                    const u64 j = t0 + static_cast<u64>(k) * BLOCK + tid;
+                    v_n[k] = 0;
+                    if (j < t_end) {
+                        act_n |= 1u << k;
+                        v_n[k] = __ldg(rowp + j);
                     }
-                    while (hi - lo > 1) {
-                        const int mid = (lo + hi) >> 1;
-                        if (sh.c_scan[mid] <= j)
-                            lo = mid;
-                        else
-                            hi = mid;
+                }
+            } else {
+                int lo = row;
+#pragma unroll
+                for (int k = 0; k < ITEMS; ++k) {
+                    const u64 j = t0 + static_cast<u64>(k) * BLOCK + tid;
+                    v_n[k] = 0;
+                    if (j < t_end) {
+                        int hi = lo + 1, step = 1; // owner row: last r with c_scan[r] <= j
+                        while (sh.c_scan[hi] <= j) {
+                            lo = hi;
+                            hi = hi + step < BLOCK ? hi + step : BLOCK;
+                            step <<= 1;
+                        }
+                        while (hi - lo > 1) {
+                            const int mid = (lo + hi) >> 1;
+                            if (sh.c_scan[mid] <= j)
+                                lo = mid;
+                            else
+                                hi = mid;
+                        }
+                        act_n |= 1u << k;
+                        v_n[k] = __ldg(p.targets + sh.c_beg[lo] + (j - sh.c_scan[lo]));
                     }
-                    hint = lo;
-                    owner_n[k] = lo;
-                    kk_n[k] = static_cast<u32>(j - sh.c_scan[lo]);
-                    v_n[k] = __ldg(p.targets + sh.c_beg[lo] + kk_n[k]);
                 }
             }
         };
 #pragma unroll
-        for (int k = 0; k < ITEMS; ++k) {
+        for (int k = 0; k < ITEMS; ++k)
             v_n[k] = 0;
-            kk_n[k] = 0;
-            owner_n[k] = 0;
-            act_n[k] = false;
-        }
         // Iteration t0 requests tile t0 and tests the tile requested by the previous iteration (nothing in
         // the first one); written as one loop so that the request code exists once.
         for (u64 t0 = 0;; t0 += TILE) {
-            u32 v[ITEMS], kk[ITEMS];
-            int owner[ITEMS];
-            bool act[ITEMS];
+            u32 v[ITEMS];
+            const u32 act = act_n;
 #pragma unroll
-            for (int k = 0; k < ITEMS; ++k) {
+            for (int k = 0; k < ITEMS; ++k)
                 v[k] = v_n[k];
-                kk[k] = kk_n[k];
-                owner[k] = owner_n[k];
-                act[k] = act_n[k];
-            }
             const bool more = t0 < T;
             if (more)
-                fetch(t0, owner[ITEMS - 1]);
+                fetch(t0);
             // Visit test.  With bitmaps one 8-byte word holds the visited bits of 32 consecutive vertices
             // for both sides; rows are ascending, so a hub row streams through the bitmap instead of
             // touching one 128-byte label line per target.
@@ -830,15 +835,15 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
                 const u64 *bits64 = reinterpret_cast<const u64 *>(bits);
 #pragma unroll
                 for (int k = 0; k < ITEMS; ++k)
-                    both[k] = act[k] ? ld_cg(bits64 + (v[k] >> 5)) : 0ull;
+                    both[k] = (act >> k) & 1u ? ld_cg(bits64 + (v[k] >> 5)) : 0ull;
             } else {
 #pragma unroll
                 for (int k = 0; k < ITEMS; ++k)
-                    both[k] = act[k] ? ld_cg(lab64 + v[k]) : 0ull;
+                    both[k] = (act >> k) & 1u ? ld_cg(lab64 + v[k]) : 0ull;
             }
 #pragma unroll
             for (int k = 0; k < ITEMS; ++k) {
-                if (!act[k])
+                if (!((act >> k) & 1u))
                     continue;
                 u32 oi;
                 if (BITS) {
@@ -859,10 +864,20 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
                     atomicMin(&sh.min_contact, oi);
                     const u32 pos = atomicAdd(&sh.edge_cnt, 1u);
                     if (pos < edge_cap) {
+                        // (owner row, index in row) of this slot of the tile requested one iteration ago
+                        const u64 j = (t0 - TILE) + static_cast<u64>(k) * BLOCK + tid;
+                        int lo = 0, hi = BLOCK;
+                        while (hi - lo > 1) {
+                            const int mid = (lo + hi) >> 1;
+                            if (sh.c_scan[mid] <= j)
+                                lo = mid;
+                            else
+                                hi = mid;
+                        }
                         u32 *w = edges + 6 * static_cast<u64>(pos);
-                        const u64 sg = sh.c_sig[owner[k]];
-                        st_cg(w + 0, (c0 - fb) + static_cast<u32>(owner[k]));
-                        st_cg(w + 1, kk[k]);
+                        const u64 sg = sh.c_sig[lo];
+                        st_cg(w + 0, (c0 - fb) + static_cast<u32>(lo));
+                        st_cg(w + 1, static_cast<u32>(j - sh.c_scan[lo]));
                         st_cg(w + 2, v[k]);
                         st_cg(w + 3, oi);
                         st_cg(w + 4, static_cast<u32>(sg));
