@@ -134,6 +134,12 @@ constexpr int kPredCache = 32;
 // scanned read-only; if it touches the other side, the meet set is resolved from at most
 // FinalEdgeCap<BLOCK>::value contact edges and the level is never settled.
 constexpr u64 kProbeMinSlots = 2048;
+// Slots per thread of the probe pass relative to the expansion.  Measured on R-MAT-20: 128x4 threads x
+// slots: factor 1 4.94 M samples/s, 2 4.41 M, 4 3.35 M; 128x2: 4.82 / 5.00 / 4.60 M -- beyond four
+// probes in flight per thread the memory system, not latency, is the limit.
+#ifndef EBC_PROBE_FACTOR
+#define EBC_PROBE_FACTOR 1
+#endif
 template <int BLOCK> struct FinalEdgeCap {
     static constexpr int value = 4 * BLOCK < 512 ? 4 * BLOCK : 512;
 };
@@ -750,7 +756,10 @@ template <int BLOCK, int ITEMS, bool BITS>
 __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bits, int e, const SideRegs &ex, const SideRegs &ot,
                            u32 *edges, u32 edge_cap, BlockShared<BLOCK, ITEMS> &sh, u64 &new_slots,
                            u64 &total_slots) {
-    constexpr int TILE = BLOCK * ITEMS;
+    // The pass only reads, so it can afford more slots per thread than the expansion: fewer, longer
+    // tiles mean fewer dependent round trips per level.
+    constexpr int PI = ITEMS * EBC_PROBE_FACTOR;
+    constexpr int TILE = BLOCK * PI;
     const u32 tid = threadIdx.x;
     const u32 fb = ex.fb, fe = ex.cnt;
     const u64 *lab64 = reinterpret_cast<const u64 *>(lab);
@@ -768,7 +777,7 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
         // row[j]; otherwise every slot finds its owner row by galloping upwards from the tile's first
         // row (slots ascend with k).  Only a contact edge needs (owner, index in row) again, and looks
         // them up on its own: the pipeline carries nothing but the target ids.
-        u32 v_n[ITEMS];
+        u32 v_n[PI];
         u32 act_n = 0; // bit k: slot k of the requested tile exists
         int row = 0;   // owner row of the requested tile's first slot (uniform, non-decreasing)
         auto fetch = [&](u64 t0) {
@@ -779,7 +788,7 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
             if (sh.c_scan[row + 1] >= t_end) {
                 const u32 *rowp = p.targets + (sh.c_beg[row] - sh.c_scan[row]);
 #pragma unroll
-                for (int k = 0; k < ITEMS; ++k) {
+                for (int k = 0; k < PI; ++k) {
                     const u64 j = t0 + static_cast<u64>(k) * BLOCK + tid;
                     v_n[k] = 0;
                     if (j < t_end) {
@@ -790,7 +799,7 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
             } else {
                 int lo = row;
 #pragma unroll
-                for (int k = 0; k < ITEMS; ++k) {
+                for (int k = 0; k < PI; ++k) {
                     const u64 j = t0 + static_cast<u64>(k) * BLOCK + tid;
                     v_n[k] = 0;
                     if (j < t_end) {
@@ -814,15 +823,15 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
             }
         };
 #pragma unroll
-        for (int k = 0; k < ITEMS; ++k)
+        for (int k = 0; k < PI; ++k)
             v_n[k] = 0;
         // Iteration t0 requests tile t0 and tests the tile requested by the previous iteration (nothing in
         // the first one); written as one loop so that the request code exists once.
         for (u64 t0 = 0;; t0 += TILE) {
-            u32 v[ITEMS];
+            u32 v[PI];
             const u32 act = act_n;
 #pragma unroll
-            for (int k = 0; k < ITEMS; ++k)
+            for (int k = 0; k < PI; ++k)
                 v[k] = v_n[k];
             const bool more = t0 < T;
             if (more)
@@ -830,19 +839,19 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
             // Visit test.  With bitmaps one 8-byte word holds the visited bits of 32 consecutive vertices
             // for both sides; rows are ascending, so a hub row streams through the bitmap instead of
             // touching one 128-byte label line per target.
-            u64 both[ITEMS];
+            u64 both[PI];
             if (BITS) {
                 const u64 *bits64 = reinterpret_cast<const u64 *>(bits);
 #pragma unroll
-                for (int k = 0; k < ITEMS; ++k)
+                for (int k = 0; k < PI; ++k)
                     both[k] = (act >> k) & 1u ? ld_cg(bits64 + (v[k] >> 5)) : 0ull;
             } else {
 #pragma unroll
-                for (int k = 0; k < ITEMS; ++k)
+                for (int k = 0; k < PI; ++k)
                     both[k] = (act >> k) & 1u ? ld_cg(lab64 + v[k]) : 0ull;
             }
 #pragma unroll
-            for (int k = 0; k < ITEMS; ++k) {
+            for (int k = 0; k < PI; ++k) {
                 if (!((act >> k) & 1u))
                     continue;
                 u32 oi;
