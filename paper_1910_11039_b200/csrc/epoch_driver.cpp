@@ -87,11 +87,14 @@ RunOutput run_pipeline(const HostGraph &g, const RunConfig &cfg, SamplerBackend 
         // the uniform allocator uses no calibration counts (stopping.cpp:50,72-78): no arrays needed
         const bool uniform = cfg.allocator == 0;
         std::vector<std::uint64_t> calib(uniform ? 1 : n + 1, 0);
+        double uniform_each = 0.0;
         if (cfg.calib_samples > 0) {
             std::uint64_t lo, cnt;
             shard_range(0, cfg.calib_samples, cfg.rank, cfg.world_size, &lo, &cnt);
             be.sample(cfg.seed, kTagCalibration, lo, cnt, 0);
             be.fold_async(0, hook, cfg.allreduce_user);
+            if (uniform) // a serial long-double sum over n: done while the GPU takes the calibration samples
+                uniform_each = calibrate_uniform_value(n, cfg.delta);
             std::uint64_t tau = 0;
             be.wait_fold(0, &tau);
             if (uniform)
@@ -102,7 +105,9 @@ RunOutput run_pipeline(const HostGraph &g, const RunConfig &cfg, SamplerBackend 
         }
         st.calibration_samples = calib[0];
         if (uniform) {
-            be.set_stopping_uniform(cfg.eps, omega, calibrate_uniform_value(n, cfg.delta), n, cfg.bound);
+            if (uniform_each == 0.0)
+                uniform_each = calibrate_uniform_value(n, cfg.delta);
+            be.set_stopping_uniform(cfg.eps, omega, uniform_each, n, cfg.bound);
         } else {
             std::vector<double> delta_lower(n), delta_upper(n);
             calibrate(calib.data(), n, cfg.delta, cfg.allocator, delta_lower.data(), delta_upper.data());
