@@ -445,8 +445,8 @@ ebc_status ebc_result_write_scores(const ebc_result *r, const ebc_run_config *cf
         need(path, "ebc_result_write_scores: null path");
         ScoreTable t;
         t.meta = run_meta(cfg->eps, cfg->delta, cfg->seed, r->out.tau_total);
-        t.vertex_ids = r->out.original_ids;
-        t.scores = r->out.scores;
+        t.vertex_ids.assign(r->out.original_ids.begin(), r->out.original_ids.end());
+        t.scores.assign(r->out.scores.begin(), r->out.scores.end());
         write_scores(path, t);
     });
 }

@@ -6,6 +6,7 @@
 
 #include <chrono>
 #include <cstdio>
+#include <cstring>
 #include <cstdlib>
 
 #include "philox.cuh"
@@ -168,16 +169,17 @@ RunOutput run_pipeline(const HostGraph &g, const RunConfig &cfg, SamplerBackend 
     require(tau == applied - discarded, "sample conservation violated: tau != applied - discarded");
 
     // Result assembly (engine.cpp:391-401).
-    std::vector<std::uint64_t> words(n + 1);
+    RawVector<std::uint64_t> words(n + 1);
     be.read_state(words.data());
     require(words[0] == tau, "sample conservation violated: tau of S differs from the checked tau");
     out.tau_total = tau;
-    out.original_ids.assign(g.original_ids.begin(), g.original_ids.end());
-    out.counts.assign(words.begin() + 1, words.end());
-    out.scores.assign(n, 0.0);
-    if (tau > 0)
-        for (std::uint64_t v = 0; v < n; ++v)
-            out.scores[v] = static_cast<double>(out.counts[v]) / static_cast<double>(tau);
+    out.original_ids.resize(n);
+    out.counts.resize(n);
+    out.scores.resize(n);
+    std::memcpy(out.original_ids.data(), g.original_ids.data(), n * sizeof(std::uint64_t));
+    std::memcpy(out.counts.data(), words.data() + 1, n * sizeof(std::uint64_t));
+    for (std::uint64_t v = 0; v < n; ++v)
+        out.scores[v] = tau > 0 ? static_cast<double>(out.counts[v]) / static_cast<double>(tau) : 0.0;
     be.finish(st);
     st.wall_s = now_s() - run_start;
     if (std::getenv("EBC_TRACE"))

@@ -54,10 +54,10 @@ struct RunStats { // replaces epochbc::RunStats (engine.hpp:89-110)
 };
 
 struct RunOutput { // ApproxResult (engine.hpp:83-87) + stats
-    std::vector<double> scores;
-    std::vector<std::uint64_t> counts;
+    RawVector<double> scores; // (RawVector: pooled page-locked memory, no zero fill -- see host_common.hpp)
+    RawVector<std::uint64_t> counts;
     std::uint64_t tau_total = 0;
-    std::vector<std::uint64_t> original_ids;
+    RawVector<std::uint64_t> original_ids;
     RunStats stats;
 };
 
