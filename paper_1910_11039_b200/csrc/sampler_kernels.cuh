@@ -167,6 +167,7 @@ template <int BLOCK, int ITEMS> struct BlockShared {
     };
     u32 edge_cnt;
     SidePtrs sp[2];
+    u64 prev_pending[2]; // per side: pending edges of the level expanded last (0 before the first)
     u32 sigma_small[2]; // per side: the frontier's sigma values sum to < 2^63 (no add of the next level can wrap)
     u32 last[6]; // base / cnt / depth of both sides of the last finished sample (state dumps)
     u32 *lab, *bits, *contact, *meetbuf; // the slot's label / bitmap / contact arrays
@@ -1332,6 +1333,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             sh.ws[kW_V_set] = 2;
             sh.ws[kW_samples] = 1;
             sh.sigma_small[0] = sh.sigma_small[1] = 1; // sigma[root] = 1
+            sh.prev_pending[0] = sh.prev_pending[1] = 0;
         }
         wk.e_lvl = 0;
         wk.p_walk = 0;
@@ -1358,7 +1360,13 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             if (side[0].cnt == side[0].fb || side[1].cnt == side[1].fb)
                 break; // a frontier ran empty: t unreachable, empty sample (sampler.cpp:82-83)
             e = side[0].pending <= side[1].pending ? 0 : 1; // tie -> forward (sampler.cpp:84)
+            // A probe that finds no contact is a wasted scan of the level, so it is only tried where the
+            // level can plausibly be the last one: on a side whose frontier at least doubled.  Searches in
+            // expanding graphs (R-MAT, Erdos-Renyi) end in their widest level; on lattice-like graphs the
+            // frontier grows by a few per cent per level, almost no level is the last, and probing every wide
+            // level cost config 3 a quarter of its time.
             if (!(p.flags & kFlagMaterializeFinal) && edge_cap() > 0 && side[e].pending >= kProbeMinSlots &&
+                side[e].pending >= 2 * sh.prev_pending[e] &&
                 static_cast<u64>(side[e].depth) + 2 <= p.aux_cap) {
                 u64 new_slots = 0, total_slots = 0;
                 edge_n = probe_level<BLOCK, ITEMS, BITS>(p, sh.lab, sh.bits, e, side[e], side[1 - e], sh.contact, edge_cap(), sh, new_slots,
@@ -1386,8 +1394,11 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             }
             EBC_PH(1)
             found = sh.min_contact != 0xffffffffu;
-            if (!found) // next_pending (sampler.cpp:95,102); evaluated fused into the level it was 3 % slower
+            if (!found) { // next_pending (sampler.cpp:95,102); evaluated fused into the level it was 3 % slower
+                if (tid == 0)
+                    sh.prev_pending[e] = side[e].pending; // (read after the barriers of sum_frontier_degrees)
                 side[e].pending = sum_frontier_degrees<BLOCK>(p, side[e], sh.red64, &sh.sigma_small[e]);
+            }
             else
                 __syncthreads();
             EBC_PH(3)
