@@ -148,7 +148,7 @@ typedef struct ebc_run_config {
     uint64_t calib_samples;    /* total calibration samples (reference: 100 per worker)    */
     int diameter_sweeps;       /* RunConfig::diameter_sweeps (default 4)                   */
     uint64_t vertex_diameter_override; /* 0 = run the diameter phase                      */
-    uint64_t epoch_samples;    /* samples per epoch over ALL ranks; 0 = derive from omega  */
+    uint64_t epoch_samples;    /* samples per epoch over ALL ranks; 0 = derive from omega and the rule */
     uint64_t max_epochs;       /* safety cap; 0 = unlimited                                */
     int device;                /* CUDA device ordinal; -1 = current device                 */
     int rank, world_size;      /* this process' shard of every epoch (one process per GPU) */

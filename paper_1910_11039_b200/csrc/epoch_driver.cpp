@@ -35,13 +35,19 @@ void RunConfig::validate() const {
         throw ConfigError("run config: need at least one diameter sweep");
 }
 
-std::uint64_t default_epoch_samples(std::uint64_t omega) {
-    // k epochs of equal size, k = clamp(round(omega / 32768), 2, 16): an epoch keeps every resident CTA
-    // busy for many samples (the tail of a launch costs about one sample time) while the adaptive rule
-    // still gets at least two chances to stop before the static budget; B is rounded up to 1024 so that
-    // k * B overshoots omega by less than k * 1024 samples.
-    std::uint64_t k = (omega + 16384) / 32768;
-    k = k < 2 ? 2 : (k > 16 ? 16 : k);
+std::uint64_t default_epoch_samples(std::uint64_t omega, bool adaptive_rule) {
+    // k epochs of equal size.  Under the Hoeffding bound the width does not depend on the counters and
+    // the static budget omega fires first, so k = clamp(round(omega / 32768), 2, 16): an epoch keeps every
+    // resident CTA busy for many samples (the tail of a launch costs about one sample time).  With the
+    // empirical-Bernstein bound the run can stop long before omega, and the epoch in flight at the stop is
+    // discarded, so epochs are half as long there (k = clamp(round(omega / 16384), 3, 32); config 2 with
+    // the weighted allocator then stops at tau = 55 296 instead of 71 680; 8192-sample epochs stop a
+    // little earlier still but sample 30 % slower).  B is rounded up to 1024 so that k * B overshoots
+    // omega by less than k * 1024 samples.  Depends on omega and the rule only, never on the GPU count.
+    const std::uint64_t unit = adaptive_rule ? 16384 : 32768;
+    const std::uint64_t k_min = adaptive_rule ? 3 : 2, k_max = adaptive_rule ? 32 : 16;
+    std::uint64_t k = (omega + unit / 2) / unit;
+    k = k < k_min ? k_min : (k > k_max ? k_max : k);
     std::uint64_t b = (omega + k - 1) / k;
     b = (b + 1023) / 1024 * 1024;
     if (b < 1024)
@@ -118,7 +124,7 @@ RunOutput run_pipeline(const HostGraph &g, const RunConfig &cfg, SamplerBackend 
     }
 
     // Phase 4: adaptive sampling in epochs.
-    const std::uint64_t B = cfg.epoch_samples ? cfg.epoch_samples : default_epoch_samples(omega);
+    const std::uint64_t B = cfg.epoch_samples ? cfg.epoch_samples : default_epoch_samples(omega, cfg.bound != 0);
     st.n0 = B;
     std::uint64_t applied = 0, discarded = 0, tau = 0;
     {

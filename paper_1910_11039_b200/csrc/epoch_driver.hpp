@@ -87,8 +87,8 @@ public:
     virtual void finish(RunStats &stats) = 0;              // work counters, overflow count
 };
 
-// Samples per epoch derived from omega only (never from the GPU count).
-std::uint64_t default_epoch_samples(std::uint64_t omega);
+// Samples per epoch derived from omega and the stopping rule only (never from the GPU count).
+std::uint64_t default_epoch_samples(std::uint64_t omega, bool adaptive_rule);
 
 RunOutput run_pipeline(const HostGraph &g, const RunConfig &cfg, SamplerBackend &backend);
 
