@@ -146,25 +146,10 @@ template <int BLOCK> struct FinalEdgeCap {
 
 template <int BLOCK, int ITEMS> struct BlockShared {
     static constexpr int WARPS = BLOCK / 32;
-    // Duplicate filter of multi-row tiles: open-addressing table keyed by target vertex, one u64 per
-    // entry = generation (22 bits) | vertex (32) | TILE-1-slot (10); atomicMax keeps the LOWEST slot.
-#ifndef EBC_SMEM_DEDUPE
-#define EBC_SMEM_DEDUPE 0 // evaluated in round 1: neutral (config 2 -0.6 %, config 1 -5 %, config 3 +3 %)
-#endif
-    static constexpr bool kSmemDedupe = EBC_SMEM_DEDUPE && BLOCK * ITEMS <= 1024;
-    static constexpr int HS = kSmemDedupe ? 2 * BLOCK * ITEMS : 2;
-    union {
-        struct {
-            u64 f_key[FinalEdgeCap<BLOCK>::value]; // contact edges of a probed final level: discovery key,
-            u64 f_s[FinalEdgeCap<BLOCK>::value];   //   sigma of the parent,
-            u32 f_v[FinalEdgeCap<BLOCK>::value];   //   target vertex,
-            u32 f_o[FinalEdgeCap<BLOCK>::value];   //   its idx on the other side
-        };
-        struct {
-            unsigned long long h[HS];
-            u32 h_idx[HS]; // idx handed to the winner of an entry (read by the losing slots)
-        };
-    };
+    u64 f_key[FinalEdgeCap<BLOCK>::value]; // contact edges of a probed final level: discovery key,
+    u64 f_s[FinalEdgeCap<BLOCK>::value];   //   sigma of the parent,
+    u32 f_v[FinalEdgeCap<BLOCK>::value];   //   target vertex,
+    u32 f_o[FinalEdgeCap<BLOCK>::value];   //   its idx on the other side
     u32 edge_cnt;
     SidePtrs sp[2];
     u64 prev_pending[2]; // per side: pending edges of the level expanded last (0 before the first)
@@ -433,7 +418,7 @@ __device__ __noinline__ u64 load_chunk(const SamplerParams &p, const SidePtrs *p
 // contact_n returns the number of contact vertices appended to `contact`.
 template <int BLOCK, int ITEMS, bool BITS>
 __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e, SideRegs &ex, const SideRegs &ot,
-                             u32 *contact, u32 &contact_n, BlockShared<BLOCK, ITEMS> &sh, WorkRegs &wk, u32 &hgen) {
+                             u32 *contact, u32 &contact_n, BlockShared<BLOCK, ITEMS> &sh, WorkRegs &wk) {
     constexpr int TILE = BLOCK * ITEMS;
     const u32 tid = threadIdx.x;
     const u32 fb = ex.fb, fe = ex.cnt;
@@ -595,56 +580,15 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
                         }
                     }
                 }
-                constexpr bool kSmemDedupe = BlockShared<BLOCK, ITEMS>::kSmemDedupe;
-                constexpr u32 kHashMask = BlockShared<BLOCK, ITEMS>::HS - 1;
-                u32 ent[ITEMS];
-                if (kSmemDedupe) {
-                    // claim in shared memory: lowest slot of every distinct unvisited target wins
-                    if (hgen == (1u << 22) - 1) { // generation wrap: start over with a clean table
-                        for (u32 i = tid; i <= kHashMask; i += BLOCK)
-                            sh.h[i] = 0;
-                        hgen = 0;
-                        __syncthreads();
-                    }
-                    hgen += 1;
+                // claim: the lowest slot of every distinct unvisited target wins (see the header comment)
 #pragma unroll
-                    for (int k = 0; k < ITEMS; ++k) {
-                        ent[k] = 0;
-                        if (candidate[k]) {
-                            const unsigned long long mine = (static_cast<unsigned long long>(hgen) << 42) |
-                                                            (static_cast<unsigned long long>(v[k]) << 10) |
-                                                            static_cast<unsigned long long>(BLOCK * ITEMS - 1 - (k * BLOCK + tid));
-                            u32 at = (v[k] * 2654435761u) & kHashMask;
-                            for (;;) {
-                                const unsigned long long cur = *(volatile unsigned long long *)(sh.h + at);
-                                if ((cur >> 42) == hgen) {
-                                    if (static_cast<u32>(cur >> 10) == v[k]) {
-                                        atomicMax(sh.h + at, mine);
-                                        break;
-                                    }
-                                    at = (at + 1) & kHashMask;
-                                } else if (atomicCAS(sh.h + at, cur, mine) == cur) {
-                                    break;
-                                }
-                            }
-                            ent[k] = at;
-                        }
-                    }
-                } else {
-#pragma unroll
-                    for (int k = 0; k < ITEMS; ++k)
-                        if (candidate[k])
-                            red_max_u32(lab + 2 * static_cast<u64>(v[k]) + e, kClaimTop - (k * BLOCK + tid));
-                }
+                for (int k = 0; k < ITEMS; ++k)
+                    if (candidate[k])
+                        red_max_u32(lab + 2 * static_cast<u64>(v[k]) + e, kClaimTop - (k * BLOCK + tid));
                 __syncthreads(); // claims visible
 #pragma unroll
                 for (int k = 0; k < ITEMS; ++k) {
-                    if (kSmemDedupe)
-                        win[k] = candidate[k] && static_cast<u32>(sh.h[ent[k]] & 1023u) ==
-                                                     static_cast<u32>(BLOCK * ITEMS - 1 - (k * BLOCK + tid));
-                    else
-                        win[k] = candidate[k] &&
-                                 ld_cg(lab + 2 * static_cast<u64>(v[k]) + e) == kClaimTop - (k * BLOCK + tid);
+                    win[k] = candidate[k] && ld_cg(lab + 2 * static_cast<u64>(v[k]) + e) == kClaimTop - (k * BLOCK + tid);
                     is_contact[k] = win[k] && other_idx[k] < ot.cnt;
                 }
                 const u32 winners = block_ranks<BLOCK, ITEMS>(win, rank, sh.warp_cnt);
@@ -654,12 +598,9 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
                 for (int k = 0; k < ITEMS; ++k) {
                     if (win[k]) {
                         if (overflow) {
-                            if (!kSmemDedupe)
-                                st_cg(lab + 2 * static_cast<u64>(v[k]) + e, 0u); // undo the claim
+                            st_cg(lab + 2 * static_cast<u64>(v[k]) + e, 0u); // undo the claim
                         } else {
                             idx[k] = cnt + rank[k];
-                            if (kSmemDedupe)
-                                sh.h_idx[ent[k]] = idx[k];
                             st_cg(lab + 2 * static_cast<u64>(v[k]) + e, ex.base + idx[k]);
                             st_cg(ex.pp->list + idx[k], v[k]);
                             st_cg(ex.pp->sig + idx[k], static_cast<u64>(0));
@@ -680,7 +621,7 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
 #pragma unroll
                 for (int k = 0; k < ITEMS; ++k) {
                     if (candidate[k] && !win[k])
-                        idx[k] = kSmemDedupe ? sh.h_idx[ent[k]] : ld_cg(lab + 2 * static_cast<u64>(v[k]) + e) - ex.base;
+                        idx[k] = ld_cg(lab + 2 * static_cast<u64>(v[k]) + e) - ex.base; // the winner's label
                     if (candidate[k] || at_level[k]) {
                         sat_atomic_add(ex.pp->sig + idx[k], sig_u[k], sigma_small); // sampler.cpp:97-98
                         wk.e_lvl += 1;
@@ -1238,9 +1179,6 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
     };
     WorkRegs wk;
     u64 tot_e_lvl = 0, tot_p_walk = 0;
-    u32 hgen = 0; // generation of the duplicate filter (BlockShared::h)
-    for (u32 i = tid; i < static_cast<u32>(BlockShared<BLOCK, ITEMS>::HS); i += BLOCK)
-        sh.h[i] = 0;
     if (tid == 0)
         for (int c = 0; c < kWorkCounters; ++c)
             sh.wk[c] = 0;
@@ -1388,7 +1326,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
                 }
                 __syncthreads(); // no sh.contact (or too many sh.contact edges): expand normally
             }
-            if (!expand_level<BLOCK, ITEMS, BITS>(p, sh.lab, sh.bits, e, side[e], side[1 - e], sh.contact, contact_n, sh, wk, hgen)) {
+            if (!expand_level<BLOCK, ITEMS, BITS>(p, sh.lab, sh.bits, e, side[e], side[1 - e], sh.contact, contact_n, sh, wk)) {
                 aborted = true;
                 break;
             }
@@ -1433,12 +1371,6 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             // meet set in discovery order (sampler.cpp:109-113) -> sh.meetbuf
             const u32 meet_count = probed ? meet_from_edges<BLOCK, ITEMS>(sh.contact, edge_n, olo, ohi, sh.meetbuf, sh)
                                           : meet_from_contacts<BLOCK, ITEMS>(sh.contact, contact_n, ex, olo, ohi, sh.meetbuf, sh);
-            if (probed) { // the sh.contact-edge arrays alias the duplicate filter: hand it back empty
-                for (u32 i = tid; i < static_cast<u32>(BlockShared<BLOCK, ITEMS>::HS); i += BLOCK)
-                    sh.h[i] = 0;
-                hgen = 0;
-                __syncthreads();
-            }
 
             // total weight over the meet set (sampler.cpp:121-123), saturating at 2^128-1
             u128 wsum = 0;
