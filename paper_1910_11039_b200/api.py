@@ -288,32 +288,55 @@ def run_pipeline(g: Graph, cfg: RunConfig, scores_path: Optional[str] = None, st
     c = cfg.to_c()
     out = C.c_void_p()
     _check(L.ebc_run(g._h, C.byref(c), C.byref(out)))
-    try:
-        if scores_path is not None:
-            _check(L.ebc_result_write_scores(out, C.byref(c), str(scores_path).encode()))
-        if stats_path is not None:
-            need = C.c_uint64()
-            _check(L.ebc_result_stats_json(out, C.byref(c), None, 0, C.byref(need)))
-            buf = C.create_string_buffer(need.value)
-            _check(L.ebc_result_stats_json(out, C.byref(c), buf, need.value, None))
-            with open(stats_path, "wb") as f:
-                f.write(buf.value)
-        n = C.c_uint64()
-        sp = _capi.f64p()
-        _check(L.ebc_result_scores(out, C.byref(sp), C.byref(n)))
-        scores = np.ctypeslib.as_array(sp, shape=(n.value,)).copy()
-        cp = _capi.u64p()
-        _check(L.ebc_result_counts(out, C.byref(cp), C.byref(n)))
-        counts = np.ctypeslib.as_array(cp, shape=(n.value,)).copy()
-        ip = _capi.u64p()
-        _check(L.ebc_result_original_ids(out, C.byref(ip), C.byref(n)))
-        ids = np.ctypeslib.as_array(ip, shape=(n.value,)).copy()
-        st = _CRunStats()
-        _check(L.ebc_result_stats(out, C.byref(st)))
-        res = ApproxResult(scores, int(L.ebc_result_tau(out)), ids, counts)
-        return res, _stats_dict(st)
-    finally:
-        L.ebc_result_free(out)
+    owner = _ResultOwner(out)
+    if scores_path is not None:
+        _check(L.ebc_result_write_scores(out, C.byref(c), str(scores_path).encode()))
+    if stats_path is not None:
+        need = C.c_uint64()
+        _check(L.ebc_result_stats_json(out, C.byref(c), None, 0, C.byref(need)))
+        buf = C.create_string_buffer(need.value)
+        _check(L.ebc_result_stats_json(out, C.byref(c), buf, need.value, None))
+        with open(stats_path, "wb") as f:
+            f.write(buf.value)
+    n = C.c_uint64()
+    sp = _capi.f64p()
+    _check(L.ebc_result_scores(out, C.byref(sp), C.byref(n)))
+    scores = owner.view(sp, C.c_double, n.value)
+    cp = _capi.u64p()
+    _check(L.ebc_result_counts(out, C.byref(cp), C.byref(n)))
+    counts = owner.view(cp, C.c_uint64, n.value)
+    ip = _capi.u64p()
+    _check(L.ebc_result_original_ids(out, C.byref(ip), C.byref(n)))
+    ids = owner.view(ip, C.c_uint64, n.value)
+    st = _CRunStats()
+    _check(L.ebc_result_stats(out, C.byref(st)))
+    res = ApproxResult(scores, int(L.ebc_result_tau(out)), ids, counts)
+    return res, _stats_dict(st)
+
+
+class _ResultOwner:
+    """Keeps an ebc_result alive for as long as any array that views its buffers (the arrays are the
+    pointers the C ABI returns -- "borrowed from the result handle" -- not copies)."""
+
+    def __init__(self, handle):
+        self._h = handle
+
+    def view(self, ptr, ctype, n: int) -> np.ndarray:
+        if n == 0:
+            return np.zeros(0, dtype=np.dtype(ctype))
+        ca = (ctype * n).from_address(C.addressof(ptr.contents))
+        ca._owner = self  # numpy keeps `ca` as the array's base, `ca` keeps the handle
+        a = np.ctypeslib.as_array(ca)
+        a.flags.writeable = False
+        return a
+
+    def __del__(self):
+        try:
+            if self._h:
+                _capi.load().ebc_result_free(self._h)
+                self._h = None
+        except Exception:
+            pass
 
 
 # --------------------------------------------------------------------------- sampler
