@@ -19,6 +19,7 @@
 #include <cstdio>
 #include <string>
 
+#include "cuda_sampler.hpp"
 #include "device_graph.hpp"
 #include "philox.cuh"
 
@@ -62,7 +63,14 @@ template <typename T> struct DevBuf {
     void alloc(u64 n) {
         release();
         count = n;
-        DG_CUDA(cudaMalloc(reinterpret_cast<void **>(&p), std::max<u64>(n, 1) * sizeof(T)));
+        const size_t bytes = std::max<u64>(n, 1) * sizeof(T);
+        cudaError_t e = cudaMalloc(reinterpret_cast<void **>(&p), bytes);
+        if (e == cudaErrorMemoryAllocation) { // the samplers' buffer cache may be holding the memory
+            cudaGetLastError();
+            release_device_cache();
+            e = cudaMalloc(reinterpret_cast<void **>(&p), bytes);
+        }
+        check(e, "cudaMalloc", __LINE__);
     }
     void release() {
         if (p)
