@@ -803,7 +803,10 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
                     new_slots += 1;
                     if (!((half_of(both[k], 1 - e) >> (v[k] & 31)) & 1u))
                         continue; // not a contact
-                    oi = ld_cg(lab + 2 * static_cast<u64>(v[k]) + (1 - e)) - ot.base;
+                    // The other side's bit already says "contact"; its idx is only needed for the record and
+                    // is fetched for all contact edges at once after the scan (one round trip per level
+                    // instead of one inside every tile that has a contact).
+                    oi = 0;
                 } else {
                     const u32 rel = half_of(both[k], e) - ex.base;
                     if (rel < ex.cnt)
@@ -812,7 +815,8 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
                     oi = half_of(both[k], 1 - e) - ot.base;
                 }
                 if (oi < ot.cnt) {
-                    atomicMin(&sh.min_contact, oi);
+                    if (!BITS)
+                        atomicMin(&sh.min_contact, oi);
                     const u32 pos = atomicAdd(&sh.edge_cnt, 1u);
                     if (pos < edge_cap) {
                         // (owner row, index in row) of this slot of the tile requested one iteration ago
@@ -842,7 +846,20 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
     }
     __syncthreads();
     total_slots = t_total;
-    return sh.edge_cnt;
+    const u32 found = sh.edge_cnt;
+    if (BITS && found > 0 && found <= edge_cap) { // other-side idx of every contact edge, and their minimum
+        u32 lowest = 0xffffffffu;
+        for (u32 i = tid; i < found; i += BLOCK) {
+            u32 *w = edges + 6 * static_cast<u64>(i);
+            const u32 oi = ld_cg(lab + 2 * static_cast<u64>(ld_cg(w + 2)) + (1 - e)) - ot.base;
+            st_cg(w + 3, oi);
+            lowest = oi < lowest ? oi : lowest;
+        }
+        if (lowest != 0xffffffffu)
+            atomicMin(&sh.min_contact, lowest);
+        __syncthreads();
+    }
+    return found;
 }
 
 // Meet set of a probed final level from its m <= final_edge_cap contact edges:
