@@ -625,6 +625,10 @@ int occupancy_for(u32 block, u32 items) {
     return per_sm;
 }
 
+// 8-byte bitmap words per slot (one word = 32 vertices x 2 sides), padded to whole 32-byte sectors: the
+// kernel clears a settled vertex's bits by zeroing its sector with one 32-byte store.
+static u64 bit_words_of(u64 n) { return ((n + 31) / 32 + 3) & ~u64{3}; }
+
 struct SlotArrays {
     u32 *lab = nullptr, *list = nullptr, *lvl = nullptr, *contact = nullptr, *hdr = nullptr, *bits = nullptr;
     u64 *sig = nullptr;
@@ -640,8 +644,8 @@ struct SlotArrays {
         sig = dev_alloc<u64>(slots * 2 * cap);
         lvl = dev_alloc<u32>(slots * 2 * (aux_cap + 2));
         contact = dev_alloc<u32>(slots * 6 * aux_cap);
-        bits = dev_alloc<u32>(slots * 2 * ((n + 31) / 32));
-        EBC_CUDA(cudaMemsetAsync(bits, 0, slots * 2 * ((n + 31) / 32) * 4, stream));
+        bits = dev_alloc<u32>(slots * 2 * bit_words_of(n));
+        EBC_CUDA(cudaMemsetAsync(bits, 0, slots * 2 * bit_words_of(n) * 4, stream));
         hdr = dev_alloc<u32>(slots * kHdrWords);
         bytes = slots * bytes_per_slot(n, cap);
         EBC_CUDA(cudaMemsetAsync(lab, 0, slots * 2 * n * 4, stream));
@@ -672,7 +676,7 @@ struct SlotArrays {
     static u64 aux_cap_of(u64 cap, u64 n) { return cap >= n ? n : std::min<u64>(cap, u64{1} << 16); }
     static u64 bytes_per_slot(u64 n, u64 cap) {
         const u64 aux = aux_cap_of(cap, n);
-        return 2 * n * 4 + 2 * ((n + 31) / 32) * 4 + 2 * cap * (4 + 8) + 2 * (aux + 2) * 4 + 6 * aux * 4 + kHdrWords * 4;
+        return 2 * n * 4 + 2 * bit_words_of(n) * 4 + 2 * cap * (4 + 8) + 2 * (aux + 2) * 4 + 6 * aux * 4 + kHdrWords * 4;
     }
 };
 
@@ -749,7 +753,7 @@ struct CudaSampler::Impl {
         p.contact = a.contact;
         p.hdr = a.hdr;
         p.bits = a.bits;
-        p.bit_words = (n + 31) / 32;
+        p.bit_words = bit_words_of(n);
         p.cap = a.cap;
         p.aux_cap = a.aux_cap;
         p.work = d_work;
@@ -952,10 +956,16 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
         // (config 1: 20.0 M samples/s at 128 threads, 27.6 M at 64, 34.4 M at 32).  Four slots per thread
         // pay once levels are long (R-MAT-20: 4.92 M vs 4.78 M; grid 2000^2: 170 k vs 150 k); on smaller
         // inputs two are faster (R-MAT-17: 13.7 M vs 11.4 M).
+        // Hub graphs from 2^28 arcs on (R-MAT-24, -26): a sample scans 2..4 * 10^5 adjacency entries and every
+        // slot carries 8 bytes of labels per vertex, so 512 threads per sample serve the memory system as
+        // well as four times as many 128-thread samples with a quarter of the slot state (config 4: 558 k
+        // samples/s in 47 GB vs 509 k in 154 GB; config 5: 187 k vs 165 k; profiles/r01_shapes.txt).
+        const bool huge_hub = m.hub_graph && m.arcs >= (u64{1} << 28);
         m.block = opt.block_threads ? opt.block_threads
-                                    : (m.arcs < (u64{1} << 18) ? 32 : m.arcs < (u64{1} << 21) ? 64 : 128);
+                                    : (m.arcs < (u64{1} << 18) ? 32 : m.arcs < (u64{1} << 21) ? 64 : huge_hub ? 512 : 128);
         m.items = opt.items_per_thread ? opt.items_per_thread
-                                       : (m.arcs >= (u64{1} << (m.hub_graph ? 24 : 22)) ? 4 : 2);
+                                       : (huge_hub && m.block == 512 ? 2
+                                          : m.arcs >= (u64{1} << (m.hub_graph ? 24 : 22)) ? 4 : 2);
         const bool want = env ? std::atoi(env) != 0 : m.hub_graph;
         if (want && !opt.materialize_final_level)
             m.flags |= kFlagUseBitmap;

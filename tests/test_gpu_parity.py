@@ -175,7 +175,7 @@ def test_rmat14_counters_bit_exact():
         assert np.array_equal(paths[i, :len(want["path"])], want["path"])
 
 
-@pytest.mark.parametrize("block,items", [(32, 1), (64, 2), (128, 4), (256, 4)])
+@pytest.mark.parametrize("block,items", [(32, 1), (64, 2), (128, 4), (256, 4), (512, 2)])
 def test_final_level_probe_is_result_identical(block, items):
     """Large last levels are only scanned (contact edges -> meet set); paths, counters and the work the
     reference algorithm defines must not change.  R-MAT-15 has levels far above the probe threshold."""
