@@ -328,6 +328,29 @@ EBC_API void ebc_release_device_cache(void);
 /* L2 flush helper for benchmarks: writes a buffer larger than L2 on the sampler's stream. */
 EBC_API ebc_status ebc_sampler_flush_l2(ebc_sampler *s);
 
+/* ------------------------------------------------------- native NCCL hook --- */
+/* A ready-made ebc_allreduce_fn over NCCL (NVLink 5 / NVSwitch), so that a C or C++ host (one process
+ * per GPU) needs nothing but this library on the data path: no callback into another runtime per epoch.
+ * Replaces the reduce + broadcast of Communicator (comm.hpp:38-51; MpiCommunicator, mpi_comm.cpp) for the
+ * epoch frames.  libnccl.so.2 is resolved at run time (dlopen; a copy already loaded by the process, e.g.
+ * torch's, is reused), so the library itself has no link-time NCCL dependency.
+ *
+ *   rank 0: ebc_nccl_unique_id(id);  send the 128 bytes to every rank (MPI_Bcast, a file, a socket ...)
+ *   all   : ebc_nccl_comm_create(id, rank, world, device, &comm);
+ *           cfg.allreduce = ebc_nccl_allreduce;  cfg.allreduce_user = comm;  cfg.rank / world_size = ...
+ *           ebc_run(g, &cfg, &res);   ...   ebc_nccl_comm_free(comm);
+ */
+typedef struct ebc_nccl_comm ebc_nccl_comm;
+#define EBC_NCCL_UNIQUE_ID_BYTES 128
+EBC_API ebc_status ebc_nccl_unique_id(void *id_out /* EBC_NCCL_UNIQUE_ID_BYTES */);
+/* Collective over all `world_size` ranks (ncclCommInitRank).  device = CUDA ordinal, -1 = current. */
+EBC_API ebc_status ebc_nccl_comm_create(const void *id, int rank, int world_size, int device,
+                                        ebc_nccl_comm **out);
+/* ebc_allreduce_fn: in-place ncclAllReduce(sum, u32) of `count` words at device address `buf`, enqueued
+ * on `cuda_stream`; `user` is the ebc_nccl_comm.  Returns 0 on success (message: ebc_last_error()). */
+EBC_API int ebc_nccl_allreduce(void *user, void *buf, uint64_t count, void *cuda_stream);
+EBC_API void ebc_nccl_comm_free(ebc_nccl_comm *c);
+
 #ifdef __cplusplus
 }
 #endif

@@ -113,6 +113,10 @@ SIGNATURES = {
     "ebc_sampler_bfs": (C.c_int, [C.c_void_p, C.c_uint32, u32p, u64p]),
     "ebc_sampler_flush_l2": (C.c_int, [C.c_void_p]),
     "ebc_release_device_cache": (None, []),
+    "ebc_nccl_unique_id": (C.c_int, [C.c_void_p]),
+    "ebc_nccl_comm_create": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "ebc_nccl_allreduce": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
+    "ebc_nccl_comm_free": (None, [C.c_void_p]),
     "ebc_scores_write": (C.c_int, [C.c_char_p, u64p, f64p, C.c_uint64, C.POINTER(C.c_char_p), C.POINTER(C.c_char_p),
                                    C.c_uint64]),
     "ebc_result_write_scores": (C.c_int, [C.c_void_p, C.POINTER(RunConfig), C.c_char_p]),

@@ -242,6 +242,7 @@ class RunConfig:
     rank: int = 0
     world_size: int = 1
     allreduce: Optional[object] = None  # ctypes callback (see distributed.py)
+    allreduce_user: int = 0  # void* handed back to the callback (the ebc_nccl_comm of NativeNcclComm)
     block_threads: int = 0
     slots: int = 0
     slot_capacity: int = 0
@@ -261,6 +262,7 @@ class RunConfig:
         c.materialize_final_level = int(self.materialize_final_level)
         if self.allreduce is not None:
             c.allreduce = self.allreduce
+            c.allreduce_user = self.allreduce_user
         return c
 
 

@@ -41,7 +41,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     cmd = [nvcc_path(), "-std=c++17", "-O3", "-lineinfo",
            "-gencode", "arch=compute_100a,code=sm_100a",
            "-Xcompiler", "-fPIC,-fvisibility=hidden,-Wall,-Wextra,-Wno-unknown-pragmas",
-           "-shared", "-o", LIB] + [os.path.join(CSRC, s) for s in SOURCES] + ["-lpthread"]
+           "-shared", "-o", LIB] + [os.path.join(CSRC, s) for s in SOURCES] + ["-lpthread", "-ldl"]
     cmd[1:1] = os.environ.get("EBC_NVCC_FLAGS", "").split()
     if verbose:
         cmd.insert(1, "-Xptxas")

@@ -4,6 +4,8 @@
 // header says runs on the GPU.
 #include "../../include/ebc_b200.h"
 
+#include <dlfcn.h>
+
 #include <chrono>
 #include <cstring>
 #include <memory>
@@ -693,6 +695,115 @@ ebc_status ebc_sampler_flush_l2(ebc_sampler *s) {
         need(s, "ebc_sampler_flush_l2: null sampler");
         s->s->flush_l2();
     });
+}
+
+} // extern "C"
+
+// ---------------------------------------------------------------- native NCCL hook ----
+// The five NCCL entry points are bound at run time; the handful of types below is NCCL's stable C ABI
+// (nccl.h: ncclUniqueId is 128 opaque bytes, ncclUint32 = 3, ncclSum = 0, ncclSuccess = 0).
+namespace {
+struct NcclApi {
+    struct UniqueId {
+        char internal[EBC_NCCL_UNIQUE_ID_BYTES];
+    };
+    int (*GetUniqueId)(UniqueId *) = nullptr;
+    int (*CommInitRank)(void **, int, UniqueId, int) = nullptr;
+    int (*AllReduce)(const void *, void *, size_t, int, int, void *, void *) = nullptr;
+    int (*CommDestroy)(void *) = nullptr;
+    const char *(*GetErrorString)(int) = nullptr;
+    std::string why;
+};
+
+const NcclApi &nccl_api() {
+    static const NcclApi api = [] {
+        NcclApi a;
+        void *h = nullptr;
+        for (const char *name : {"libnccl.so.2", "libnccl.so"}) {
+            h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+            if (h)
+                break;
+        }
+        if (!h) {
+            a.why = std::string("libnccl.so.2 not found: ") + (dlerror() ? dlerror() : "");
+            return a;
+        }
+        a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+        a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+        a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(dlsym(h, "ncclAllReduce"));
+        a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+        a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+        if (!a.GetUniqueId || !a.CommInitRank || !a.AllReduce || !a.CommDestroy || !a.GetErrorString)
+            a.why = "libnccl.so.2 lacks an expected entry point";
+        return a;
+    }();
+    if (!api.why.empty())
+        throw BackendFault(api.why);
+    return api;
+}
+
+void nccl_check(const NcclApi &a, int rc, const char *what) {
+    if (rc != 0)
+        throw BackendFault(std::string(what) + ": " + a.GetErrorString(rc));
+}
+} // namespace
+
+struct ebc_nccl_comm {
+    void *comm = nullptr;
+    int rank = 0, world = 1;
+};
+
+extern "C" {
+
+ebc_status ebc_nccl_unique_id(void *id_out) {
+    return guarded([&] {
+        need(id_out, "ebc_nccl_unique_id: null id");
+        const NcclApi &a = nccl_api();
+        NcclApi::UniqueId id;
+        nccl_check(a, a.GetUniqueId(&id), "ncclGetUniqueId");
+        std::memcpy(id_out, id.internal, sizeof id.internal);
+    });
+}
+
+ebc_status ebc_nccl_comm_create(const void *id, int rank, int world_size, int device, ebc_nccl_comm **out) {
+    return guarded([&] {
+        need(id, "ebc_nccl_comm_create: null id");
+        need(out, "ebc_nccl_comm_create: null out");
+        if (world_size < 1 || rank < 0 || rank >= world_size)
+            throw ConfigError("ebc_nccl_comm_create: need 0 <= rank < world_size");
+        const NcclApi &a = nccl_api();
+        set_device_or_throw(device);
+        NcclApi::UniqueId uid;
+        std::memcpy(uid.internal, id, sizeof uid.internal);
+        auto c = std::make_unique<ebc_nccl_comm>();
+        c->rank = rank;
+        c->world = world_size;
+        nccl_check(a, a.CommInitRank(&c->comm, world_size, uid, rank), "ncclCommInitRank");
+        *out = c.release();
+    });
+}
+
+int ebc_nccl_allreduce(void *user, void *buf, uint64_t count, void *cuda_stream) {
+    const ebc_status st = guarded([&] {
+        need(user, "ebc_nccl_allreduce: null communicator");
+        need(buf, "ebc_nccl_allreduce: null buffer");
+        const NcclApi &a = nccl_api();
+        auto *c = static_cast<ebc_nccl_comm *>(user);
+        nccl_check(a, a.AllReduce(buf, buf, static_cast<size_t>(count), /*ncclUint32*/ 3, /*ncclSum*/ 0, c->comm, cuda_stream),
+                   "ncclAllReduce");
+    });
+    return st == EBC_OK ? 0 : 1;
+}
+
+void ebc_nccl_comm_free(ebc_nccl_comm *c) {
+    if (!c)
+        return;
+    try {
+        if (c->comm)
+            nccl_api().CommDestroy(c->comm);
+    } catch (...) {
+    }
+    delete c;
 }
 
 } // extern "C"

@@ -686,6 +686,18 @@ constexpr u64 kLargeSlots = 8; // full-capacity slots of the re-run pass
 
 } // namespace
 
+void set_device_or_throw(int device) {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+        throw CudaError(std::string("no CUDA device available (this library has no CPU fallback): ") +
+                        (e == cudaSuccess ? "device count is 0" : cudaGetErrorString(e)));
+    if (device >= count)
+        throw ConfigError("device ordinal out of range");
+    if (device >= 0)
+        EBC_CUDA(cudaSetDevice(device));
+}
+
 void release_device_cache() {
     pool().release_idle();
     handles().release_idle();

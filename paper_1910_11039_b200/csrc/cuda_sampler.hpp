@@ -32,6 +32,8 @@ using AllreduceFn = int (*)(void *user, void *buf, std::uint64_t count, void *cu
 
 // Frees the device buffers cached from destroyed samplers (see DevicePool in cuda_sampler.cu).
 void release_device_cache();
+// Makes `device` (>= 0) the calling thread's CUDA device; throws CudaError when there is no device at all.
+void set_device_or_throw(int device);
 
 class CudaSampler {
 public:

@@ -47,3 +47,60 @@ def make_allreduce_hook(group=None, on_error=None):
             return 1
 
     return _capi.ALLREDUCE_FN(hook)
+
+
+class NativeNcclComm:
+    """The library's own NCCL transport (ebc_nccl_*, include/ebc_b200.h): the epoch-frame all-reduce is a C
+    function inside libebc_b200.so, so no Python runs per epoch.  torch.distributed (or anything else that
+    can move 128 bytes) is only used once, to hand rank 0's NCCL unique id to the other ranks.
+
+        comm = NativeNcclComm.from_process_group(device)          # inside torchrun
+        cfg = RunConfig(..., rank=comm.rank, world_size=comm.world_size, **comm.hook())
+    """
+
+    ID_BYTES = 128
+
+    def __init__(self, unique_id: bytes, rank: int, world_size: int, device: int = -1):
+        L = _capi.load()
+        if len(unique_id) != self.ID_BYTES:
+            raise ValueError("NCCL unique id must be 128 bytes")
+        self.rank, self.world_size = rank, world_size
+        self._h = C.c_void_p()
+        buf = C.create_string_buffer(unique_id, self.ID_BYTES)
+        st = L.ebc_nccl_comm_create(buf, rank, world_size, device, C.byref(self._h))
+        if st != 0:
+            raise RuntimeError(f"ebc_nccl_comm_create failed ({st}): {L.ebc_last_error().decode()}")
+        self._fn = C.cast(L.ebc_nccl_allreduce, _capi.ALLREDUCE_FN)
+
+    @staticmethod
+    def unique_id() -> bytes:
+        L = _capi.load()
+        buf = C.create_string_buffer(NativeNcclComm.ID_BYTES)
+        st = L.ebc_nccl_unique_id(buf)
+        if st != 0:
+            raise RuntimeError(f"ebc_nccl_unique_id failed ({st}): {L.ebc_last_error().decode()}")
+        return buf.raw
+
+    @classmethod
+    def from_process_group(cls, device: int = -1, group=None):
+        """Rank 0 creates the id; it is broadcast through the (already initialised) torch process group."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        box = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0, group=group)
+        return cls(box[0], rank, world, device)
+
+    def hook(self) -> dict:
+        """Keyword arguments for RunConfig: the C all-reduce function and this communicator as its user pointer."""
+        return {"allreduce": self._fn, "allreduce_user": self._h.value}
+
+    def close(self):
+        if self._h:
+            _capi.load().ebc_nccl_comm_free(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

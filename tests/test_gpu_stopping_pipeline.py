@@ -170,6 +170,27 @@ def test_nccl_allreduce_hook_single_rank():
             dist.destroy_process_group()
 
 
+def test_native_nccl_hook_single_rank():
+    """The library's own NCCL transport (ebc_nccl_*: ncclCommInitRank / ncclAllReduce bound with dlopen, no
+    Python per epoch) with a 1-rank communicator: the frames pass through ncclAllReduce on the aggregation
+    stream and the pipeline's counters, tau and stop epoch must not change."""
+    from paper_1910_11039_b200.distributed import NativeNcclComm
+    comm = NativeNcclComm(NativeNcclComm.unique_id(), rank=0, world_size=1, device=0)
+    try:
+        g, o = _graph(3000, 10000, 5)
+        cfg = ebc.RunConfig(eps=0.03, delta=0.1, seed=SEED, epoch_samples=1024, **comm.hook())
+        res, st = ebc.run_pipeline(g, cfg)
+        ref, st2 = ebc.run_pipeline(g, ebc.RunConfig(eps=0.03, delta=0.1, seed=SEED, epoch_samples=1024))
+        assert np.array_equal(res.counts, ref.counts) and st["tau"] == st2["tau"] and st["epochs"] == st2["epochs"]
+        s = ebc.Sampler(g, cfg)
+        s.sample(SEED, 0, 2000)
+        s.fold_and_check(0)
+        assert np.array_equal(s.read_state(), o.accumulate(SEED, 0, 2000))
+        s.close()
+    finally:
+        comm.close()
+
+
 def test_pipeline_writes_reference_score_file_and_stats_json(tmp_path):
     """`run` of the reference CLI writes a score file and a stats JSON (tools/epochbc.cpp:219-224)."""
     import json

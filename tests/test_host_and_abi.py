@@ -253,3 +253,23 @@ def test_score_files_round_trip_and_compare(tmp_path):
         want = RefPlain.compare_files(pa, pe, 0.01)
         for k, v in want.items():
             assert rep[k] == v, k
+
+
+def test_native_nccl_transport_without_gpu():
+    """ebc_nccl_*: the unique id needs no device; creating a communicator without one fails loudly with the
+    CUDA status (no CPU fallback), and argument errors map to the config class."""
+    import ctypes as C
+    from paper_1910_11039_b200 import _capi
+    L = _capi.load()
+    a, b = C.create_string_buffer(128), C.create_string_buffer(128)
+    assert L.ebc_nccl_unique_id(a) == 0 and L.ebc_nccl_unique_id(b) == 0
+    assert a.raw != b.raw and a.raw != bytes(128)
+    h = C.c_void_p()
+    assert L.ebc_nccl_comm_create(a, 2, 2, -1, C.byref(h)) == 2      # rank out of range: EBC_ERR_CONFIG
+    assert b"rank" in L.ebc_last_error()
+    import torch
+    if not torch.cuda.is_available():
+        assert L.ebc_nccl_comm_create(a, 0, 1, -1, C.byref(h)) == 5  # EBC_ERR_CUDA
+        assert b"no CUDA device" in L.ebc_last_error()
+    assert L.ebc_nccl_allreduce(None, None, 0, None) == 1            # null communicator: hook reports failure
+    L.ebc_nccl_comm_free(None)
