@@ -717,6 +717,7 @@ struct CudaSampler::Impl {
     u32 block = 128;
     u32 items = 4;
     u32 flags = 0;
+    u64 probe_min_slots = 512;
     bool hub_graph = false; // max degree >= 1024: visited bitmaps, direction-optimising BFS
     SlotArrays small, big;
     u32 *d_frame[2] = {nullptr, nullptr};
@@ -766,6 +767,7 @@ struct CudaSampler::Impl {
         p.hdr = a.hdr;
         p.bits = a.bits;
         p.bit_words = bit_words_of(n);
+        p.probe_min_slots = probe_min_slots;
         p.cap = a.cap;
         p.aux_cap = a.aux_cap;
         p.work = d_work;
@@ -978,6 +980,11 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
         m.items = opt.items_per_thread ? opt.items_per_thread
                                        : (huge_hub && m.block == 512 ? 2
                                           : m.arcs >= (u64{1} << (m.hub_graph ? 24 : 22)) ? 4 : 2);
+        // Probe threshold (profiles/r01_probe_threshold.txt): with visited bitmaps a probe is cheap enough to pay
+        // from 256 adjacency slots on (R-MAT-14 +13 %, R-MAT-20 +5 % over 2048); probing through labels, from 512.
+        m.probe_min_slots = m.hub_graph ? 256 : 512;
+        if (const char *pe = std::getenv("EBC_PROBE_MIN_SLOTS")) // tuning hook (tools/sweep_probe_min.py)
+            m.probe_min_slots = std::strtoull(pe, nullptr, 0);
         const bool want = env ? std::atoi(env) != 0 : m.hub_graph;
         if (want && !opt.materialize_final_level)
             m.flags |= kFlagUseBitmap;

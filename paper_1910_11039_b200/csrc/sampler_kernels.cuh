@@ -143,10 +143,10 @@ struct SidePtrs {
 
 constexpr int kPredCache = 32;
 
-// Final-level probe (see probe_level): a level with at least kProbeMinSlots adjacency slots is first
-// scanned read-only; if it touches the other side, the meet set is resolved from at most
-// FinalEdgeCap<BLOCK>::value contact edges and the level is never settled.
-constexpr u64 kProbeMinSlots = 2048;
+// Final-level probe (see probe_level): a level with at least SamplerParams::probe_min_slots adjacency
+// slots (256 with visited bitmaps, else 512; set by the host) is first scanned read-only; if it touches
+// the other side, the meet set is resolved from at most FinalEdgeCap<BLOCK>::value contact edges and the
+// level is never settled.
 // Slots per thread of the probe pass relative to the expansion.  Measured on R-MAT-20: 128x4 threads x
 // slots: factor 1 4.94 M samples/s, 2 4.41 M, 4 3.35 M; 128x2: 4.82 / 5.00 / 4.60 M -- beyond four
 // probes in flight per thread the memory system, not latency, is the limit.
@@ -1333,7 +1333,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             // expanding graphs (R-MAT, Erdos-Renyi) end in their widest level; on lattice-like graphs the
             // frontier grows by a few per cent per level, almost no level is the last, and probing every wide
             // level cost config 3 a quarter of its time.
-            if (!(p.flags & kFlagMaterializeFinal) && edge_cap() > 0 && side[e].pending >= kProbeMinSlots &&
+            if (!(p.flags & kFlagMaterializeFinal) && edge_cap() > 0 && side[e].pending >= p.probe_min_slots &&
                 side[e].pending >= 2 * sh.prev_pending[e] &&
                 static_cast<u64>(side[e].depth) + 2 <= p.aux_cap) {
                 u64 new_slots = 0, total_slots = 0;
