@@ -68,6 +68,9 @@ __device__ __forceinline__ u64 atom_add_u64(u64 *p, u64 v) {
 __device__ __forceinline__ void red_max_u64(u64 *p, u64 v) {
     asm volatile("red.global.max.u64 [%0], %1;" ::"l"(__cvta_generic_to_global(p)), "l"(v) : "memory");
 }
+__device__ __forceinline__ void red_min_u64(u64 *p, u64 v) {
+    asm volatile("red.global.min.u64 [%0], %1;" ::"l"(__cvta_generic_to_global(p)), "l"(v) : "memory");
+}
 __device__ __forceinline__ void red_max_u32(u32 *p, u32 v) {
     asm volatile("red.global.max.u32 [%0], %1;" ::"l"(__cvta_generic_to_global(p)), "r"(v) : "memory");
 }
@@ -153,8 +156,11 @@ constexpr int kPredCache = 32;
 #ifndef EBC_PROBE_FACTOR
 #define EBC_PROBE_FACTOR 1
 #endif
+#ifndef EBC_EDGE_CAP_MAX
+#define EBC_EDGE_CAP_MAX 512
+#endif
 template <int BLOCK> struct FinalEdgeCap {
-    static constexpr int value = 4 * BLOCK < 512 ? 4 * BLOCK : 512;
+    static constexpr int value = 4 * BLOCK < EBC_EDGE_CAP_MAX ? 4 * BLOCK : EBC_EDGE_CAP_MAX;
 };
 
 template <int BLOCK, int ITEMS> struct BlockShared {
@@ -964,6 +970,109 @@ __device__ u32 meet_from_edges(const u32 *edges, u32 m, u32 olo, u32 ohi, u32 *m
     return total;
 }
 
+// The same for a probed final level with more contact edges than meet_from_edges holds in shared
+// memory (R-MAT-20: 6.5 % of the samples, R-MAT-24: 16 % -- the ones with the largest final levels, which
+// would otherwise be expanded and settled in full).  Works in the slot's global arrays:
+//  * a member's other-side idx oi is unique and lies in [olo, ohi), so oi - olo indexes two scratch
+//    arrays (unused tails of the two sides' sigma arrays): first[] = smallest discovery key among the
+//    vertex's contact edges, sum[] = saturating sum of the parents' sigma;
+//  * the edge whose key equals first[] represents its vertex; the representatives are written to
+//    meetbuf as {key hi, key lo, v, oi}, sorted by key with a bitonic network (one CTA, global memory,
+//    padded to a power of two), and rewritten in place as {v, oi, sigma lo, sigma hi}.
+template <int BLOCK, int ITEMS>
+__device__ __noinline__ u32 meet_from_edges_large(const u32 *edges, u32 m, u32 olo, u32 ohi, u32 *meetbuf, u64 *first,
+                                                  u64 *sum, BlockShared<BLOCK, ITEMS> &sh) {
+    const u32 tid = threadIdx.x;
+    const u32 L = ohi - olo;
+    for (u32 i = tid; i < m; i += BLOCK) {
+        const u32 r = ld_cg(edges + 6 * static_cast<u64>(i) + 3) - olo;
+        if (r < L) {
+            st_cg(first + r, ~0ull);
+            st_cg(sum + r, static_cast<u64>(0));
+        }
+    }
+    __syncthreads();
+    for (u32 i = tid; i < m; i += BLOCK) {
+        const u32 *w = edges + 6 * static_cast<u64>(i);
+        const u32 r = ld_cg(w + 3) - olo;
+        if (r < L) {
+            red_min_u64(first + r, (static_cast<u64>(ld_cg(w)) << 32) | ld_cg(w + 1));
+            sat_atomic_add(sum + r, static_cast<u64>(ld_cg(w + 4)) | (static_cast<u64>(ld_cg(w + 5)) << 32), false);
+        }
+    }
+    __syncthreads();
+    u32 count = 0;
+    for (u32 i0 = 0; i0 < m; i0 += BLOCK) {
+        const u32 i = i0 + tid;
+        bool rep[1] = {false};
+        u32 k_hi = 0, k_lo = 0, v = 0, oi = 0;
+        if (i < m) {
+            const u32 *w = edges + 6 * static_cast<u64>(i);
+            oi = ld_cg(w + 3);
+            if (oi - olo < L) {
+                k_hi = ld_cg(w);
+                k_lo = ld_cg(w + 1);
+                v = ld_cg(w + 2);
+                rep[0] = ld_cg(first + (oi - olo)) == ((static_cast<u64>(k_hi) << 32) | k_lo);
+            }
+        }
+        u32 rank[1];
+        const u32 tot = block_ranks<BLOCK, 1>(rep, rank, sh.warp_cnt);
+        if (rep[0]) {
+            u32 *w = meetbuf + 4 * static_cast<u64>(count + rank[0]);
+            st_cg(w + 0, k_hi);
+            st_cg(w + 1, k_lo);
+            st_cg(w + 2, v);
+            st_cg(w + 3, oi);
+        }
+        count += tot;
+        __syncthreads();
+    }
+    u32 n2 = 1;
+    while (n2 < count)
+        n2 <<= 1;
+    for (u32 i = count + tid; i < n2; i += BLOCK) { // padding sorts last
+        st_cg(meetbuf + 4 * static_cast<u64>(i), 0xffffffffu);
+        st_cg(meetbuf + 4 * static_cast<u64>(i) + 1, 0xffffffffu);
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (u32 k = 2; k <= n2; k <<= 1) {
+#pragma unroll 1
+        for (u32 j = k >> 1; j > 0; j >>= 1) {
+            for (u32 t = tid; t < (n2 >> 1); t += BLOCK) {
+                const u32 i = ((t & ~(j - 1)) << 1) | (t & (j - 1)); // t with a zero inserted at bit log2(j)
+                u32 *a = meetbuf + 4 * static_cast<u64>(i), *b = meetbuf + 4 * static_cast<u64>(i | j);
+                const u32 a0 = ld_cg(a), a1 = ld_cg(a + 1), b0 = ld_cg(b), b1 = ld_cg(b + 1);
+                const u64 ka = (static_cast<u64>(a0) << 32) | a1, kb = (static_cast<u64>(b0) << 32) | b1;
+                if ((ka > kb) == ((i & k) == 0)) {
+                    const u32 a2 = ld_cg(a + 2), a3 = ld_cg(a + 3), b2 = ld_cg(b + 2), b3 = ld_cg(b + 3);
+                    st_cg(a, b0);
+                    st_cg(a + 1, b1);
+                    st_cg(a + 2, b2);
+                    st_cg(a + 3, b3);
+                    st_cg(b, a0);
+                    st_cg(b + 1, a1);
+                    st_cg(b + 2, a2);
+                    st_cg(b + 3, a3);
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (u32 i = tid; i < count; i += BLOCK) {
+        u32 *w = meetbuf + 4 * static_cast<u64>(i);
+        const u32 v = ld_cg(w + 2), oi = ld_cg(w + 3);
+        const u64 sg = ld_cg(sum + (oi - olo));
+        st_cg(w + 0, v);
+        st_cg(w + 1, oi);
+        st_cg(w + 2, static_cast<u32>(sg));
+        st_cg(w + 3, static_cast<u32>(sg >> 32));
+    }
+    __syncthreads();
+    return count;
+}
+
 // Meet set of a normally expanded final level: the contacts (in discovery order)
 // whose other-side idx lies in [olo, ohi), written to meetbuf like meet_from_edges.
 template <int BLOCK, int ITEMS>
@@ -1203,9 +1312,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
     }
     __syncthreads();
     auto edge_cap = [&]() -> u32 { // contact edges the probe may collect (recomputed: not worth a register)
-        const u64 room = (2 * p.aux_cap) / 6;
-        return static_cast<u32>(room < static_cast<u64>(FinalEdgeCap<BLOCK>::value) ? room
-                                                                                   : static_cast<u64>(FinalEdgeCap<BLOCK>::value));
+        return static_cast<u32>((2 * p.aux_cap) / 6);
     };
     WorkRegs wk;
     u64 tot_e_lvl = 0, tot_p_walk = 0;
@@ -1340,7 +1447,17 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
                 edge_n = probe_level<BLOCK, ITEMS, BITS>(p, sh.lab, sh.bits, e, side[e], side[1 - e], sh.contact, edge_cap(), sh, new_slots,
                                                    total_slots);
                 EBC_PH(2)
-                if (edge_n > 0 && edge_n <= edge_cap()) {
+                bool resolvable = edge_n > 0 && edge_n <= edge_cap();
+                if (resolvable && edge_n > static_cast<u32>(FinalEdgeCap<BLOCK>::value)) {
+                    // meet_from_edges_large needs ohi - olo scratch words behind both sides' sigma arrays
+                    const SideRegs &ot = side[1 - e];
+                    u32 best = ot.depth;
+                    while (ld_cg(ot.pp->lvl + best) > sh.min_contact)
+                        --best;
+                    const u64 span = (best == ot.depth ? ot.cnt : ld_cg(ot.pp->lvl + best + 1)) - ld_cg(ot.pp->lvl + best);
+                    resolvable = span + side[e].cnt <= p.cap && span + ot.cnt <= p.cap;
+                }
+                if (resolvable) {
                     // final level: account its scan, open the (virtual) level for the walk, stop
                     wk.e_lvl += new_slots;
                     if (tid == 0) {
@@ -1354,6 +1471,8 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
                     found = true;
                     break;
                 }
+                if (tid == 0 && edge_n > 0)
+                    sh.rec.flags |= 4u; // the probe found more contact edges than it can resolve
                 __syncthreads(); // no sh.contact (or too many sh.contact edges): expand normally
             }
             if (!expand_level<BLOCK, ITEMS, BITS>(p, sh.lab, sh.bits, e, side[e], side[1 - e], sh.contact, contact_n, sh, wk)) {
@@ -1399,8 +1518,12 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             __syncthreads();
 
             // meet set in discovery order (sampler.cpp:109-113) -> sh.meetbuf
-            const u32 meet_count = probed ? meet_from_edges<BLOCK, ITEMS>(sh.contact, edge_n, olo, ohi, sh.meetbuf, sh)
-                                          : meet_from_contacts<BLOCK, ITEMS>(sh.contact, contact_n, ex, olo, ohi, sh.meetbuf, sh);
+            const u32 meet_count =
+                !probed ? meet_from_contacts<BLOCK, ITEMS>(sh.contact, contact_n, ex, olo, ohi, sh.meetbuf, sh)
+                : edge_n <= static_cast<u32>(FinalEdgeCap<BLOCK>::value)
+                    ? meet_from_edges<BLOCK, ITEMS>(sh.contact, edge_n, olo, ohi, sh.meetbuf, sh)
+                    : meet_from_edges_large<BLOCK, ITEMS>(sh.contact, edge_n, olo, ohi, sh.meetbuf, ex.pp->sig + ex.cnt,
+                                                          ot.pp->sig + ot.cnt, sh);
 
             // total weight over the meet set (sampler.cpp:121-123), saturating at 2^128-1
             u128 wsum = 0;
