@@ -718,6 +718,7 @@ struct CudaSampler::Impl {
     u32 items = 4;
     u32 flags = 0;
     u64 probe_min_slots = 512;
+    u64 probe_growth_x4 = 8; // the frontier's pending edges at least doubled
     bool hub_graph = false; // max degree >= 1024: visited bitmaps, direction-optimising BFS
     SlotArrays small, big;
     u32 *d_frame[2] = {nullptr, nullptr};
@@ -768,6 +769,7 @@ struct CudaSampler::Impl {
         p.bits = a.bits;
         p.bit_words = bit_words_of(n);
         p.probe_min_slots = probe_min_slots;
+        p.probe_growth_x4 = probe_growth_x4;
         p.cap = a.cap;
         p.aux_cap = a.aux_cap;
         p.work = d_work;
@@ -970,21 +972,29 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
         // (config 1: 20.0 M samples/s at 128 threads, 27.6 M at 64, 34.4 M at 32).  Four slots per thread
         // pay once levels are long (R-MAT-20: 4.92 M vs 4.78 M; grid 2000^2: 170 k vs 150 k); on smaller
         // inputs two are faster (R-MAT-17: 13.7 M vs 11.4 M).
-        // Hub graphs from 2^28 arcs on (R-MAT-24, -26): a sample scans 2..4 * 10^5 adjacency entries and every
-        // slot carries 8 bytes of labels per vertex, so 512 threads per sample serve the memory system as
-        // well as four times as many 128-thread samples with a quarter of the slot state (config 4: 558 k
-        // samples/s in 47 GB vs 509 k in 154 GB; config 5: 187 k vs 165 k; profiles/r01_shapes.txt).
-        const bool huge_hub = m.hub_graph && m.arcs >= (u64{1} << 28);
-        m.block = opt.block_threads ? opt.block_threads
-                                    : (m.arcs < (u64{1} << 18) ? 32 : m.arcs < (u64{1} << 21) ? 64 : huge_hub ? 512 : 128);
-        m.items = opt.items_per_thread ? opt.items_per_thread
-                                       : (huge_hub && m.block == 512 ? 2
-                                          : m.arcs >= (u64{1} << (m.hub_graph ? 24 : 22)) ? 4 : 2);
+        // Hub graphs (profiles/r01_shapes.txt, second table): since every large final level is resolved by the
+        // probe, no sample is much heavier than the rest and more, smaller CTAs win again -- up to the point
+        // where the slot state (8 bytes of labels per vertex and slot) no longer fits: R-MAT-14/17 32x2
+        // (42.7 / 22.3 M samples/s; 64x2 29.4 / 18.4 M), R-MAT-20 64x2 (9.0 M; 128x4 8.1 M), R-MAT-22 128x4,
+        // R-MAT-24 256x4 (2.03 M; 512x2 1.55 M), R-MAT-26 512x4 (742 k; 256x4 614 k, 263 slots either way).
+        if (m.hub_graph) {
+            const int lg = m.arcs < (u64{1} << 23) ? 0 : m.arcs < (u64{1} << 26) ? 1 : m.arcs < (u64{1} << 28) ? 2
+                           : m.arcs < (u64{1} << 30) ? 3 : 4;
+            static const u32 kBlock[5] = {32, 64, 128, 256, 512}, kItems[5] = {2, 2, 4, 4, 4};
+            m.block = opt.block_threads ? opt.block_threads : kBlock[lg];
+            m.items = opt.items_per_thread ? opt.items_per_thread : kItems[lg];
+        } else {
+            m.block = opt.block_threads ? opt.block_threads
+                                        : (m.arcs < (u64{1} << 18) ? 32 : m.arcs < (u64{1} << 21) ? 64 : 128);
+            m.items = opt.items_per_thread ? opt.items_per_thread : (m.arcs >= (u64{1} << 22) ? 4 : 2);
+        }
         // Probe threshold (profiles/r01_probe_threshold.txt): with visited bitmaps a probe is cheap enough to pay
         // from 256 adjacency slots on (R-MAT-14 +13 %, R-MAT-20 +5 % over 2048); probing through labels, from 512.
         m.probe_min_slots = m.hub_graph ? 256 : 512;
         if (const char *pe = std::getenv("EBC_PROBE_MIN_SLOTS")) // tuning hook (tools/sweep_probe_min.py)
             m.probe_min_slots = std::strtoull(pe, nullptr, 0);
+        if (const char *pe = std::getenv("EBC_PROBE_GROWTH_X4")) // tuning hook
+            m.probe_growth_x4 = std::strtoull(pe, nullptr, 0);
         const bool want = env ? std::atoi(env) != 0 : m.hub_graph;
         if (want && !opt.materialize_final_level)
             m.flags |= kFlagUseBitmap;

@@ -97,6 +97,7 @@ struct SamplerParams {
     unsigned long long *overflow_total; // persistent count of abandoned samples of this pass
     u32 flags;                  // kFlag*
     u32 *bits;                  // [slots][2 * bit_words] visited bitmaps, bits[2*(v>>5) + side]
+    u64 probe_growth_x4;        // ... and only if 4 x pending edges >= this x the pending edges of the side's previous level
     u64 probe_min_slots;        // a level with fewer adjacency slots is expanded without trying the read-only probe
     u64 bit_words;              // ceil(n / 32), rounded up to a multiple of 4 (32-byte sectors)
     // dynamic slot hand-out (main pass): ring of free slot ids, ring_pos = {head, tail}; null => slot = slot_base + blockIdx.x

@@ -1441,7 +1441,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             // frontier grows by a few per cent per level, almost no level is the last, and probing every wide
             // level cost config 3 a quarter of its time.
             if (!(p.flags & kFlagMaterializeFinal) && edge_cap() > 0 && side[e].pending >= p.probe_min_slots &&
-                side[e].pending >= 2 * sh.prev_pending[e] &&
+                4 * side[e].pending >= p.probe_growth_x4 * sh.prev_pending[e] &&
                 static_cast<u64>(side[e].depth) + 2 <= p.aux_cap) {
                 u64 new_slots = 0, total_slots = 0;
                 edge_n = probe_level<BLOCK, ITEMS, BITS>(p, sh.lab, sh.bits, e, side[e], side[1 - e], sh.contact, edge_cap(), sh, new_slots,
