@@ -719,7 +719,10 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
                            u64 &total_slots) {
     // The pass only reads, so it can afford more slots per thread than the expansion: fewer, longer
     // tiles mean fewer dependent round trips per level.
-    constexpr int PI = ITEMS * EBC_PROBE_FACTOR;
+#ifndef EBC_PROBE_MIN_PI
+#define EBC_PROBE_MIN_PI 1
+#endif
+    constexpr int PI = ITEMS * EBC_PROBE_FACTOR < EBC_PROBE_MIN_PI ? EBC_PROBE_MIN_PI : ITEMS * EBC_PROBE_FACTOR;
     constexpr int TILE = BLOCK * PI;
     const u32 tid = threadIdx.x;
     const u32 fb = ex.fb, fe = ex.cnt;
@@ -1031,6 +1034,49 @@ __device__ __noinline__ u32 meet_from_edges_large(const u32 *edges, u32 m, u32 o
     u32 n2 = 1;
     while (n2 < count)
         n2 <<= 1;
+    if (count <= static_cast<u32>(FinalEdgeCap<BLOCK>::value)) {
+        // Few members (the usual case: many contact edges, most of them to deeper levels of the other side or
+        // to the same vertices): the same network in shared memory, on the arrays of meet_from_edges.
+        for (u32 i = tid; i < n2; i += BLOCK) {
+            const u32 *w = meetbuf + 4 * static_cast<u64>(i);
+            const bool real = i < count;
+            sh.f_key[i] = real ? (static_cast<u64>(ld_cg(w)) << 32) | ld_cg(w + 1) : ~0ull;
+            sh.f_v[i] = real ? ld_cg(w + 2) : 0u;
+            sh.f_o[i] = real ? ld_cg(w + 3) : 0u;
+        }
+        __syncthreads();
+#pragma unroll 1
+        for (u32 k = 2; k <= n2; k <<= 1) {
+#pragma unroll 1
+            for (u32 j = k >> 1; j > 0; j >>= 1) {
+                for (u32 t = tid; t < (n2 >> 1); t += BLOCK) {
+                    const u32 i = ((t & ~(j - 1)) << 1) | (t & (j - 1)), q = i | j;
+                    const u64 ka = sh.f_key[i], kb = sh.f_key[q];
+                    if ((ka > kb) == ((i & k) == 0)) {
+                        sh.f_key[i] = kb;
+                        sh.f_key[q] = ka;
+                        const u32 va = sh.f_v[i], oa = sh.f_o[i];
+                        sh.f_v[i] = sh.f_v[q];
+                        sh.f_o[i] = sh.f_o[q];
+                        sh.f_v[q] = va;
+                        sh.f_o[q] = oa;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        for (u32 i = tid; i < count; i += BLOCK) {
+            u32 *w = meetbuf + 4 * static_cast<u64>(i);
+            const u32 oi = sh.f_o[i];
+            const u64 sg = ld_cg(sum + (oi - olo));
+            st_cg(w + 0, sh.f_v[i]);
+            st_cg(w + 1, oi);
+            st_cg(w + 2, static_cast<u32>(sg));
+            st_cg(w + 3, static_cast<u32>(sg >> 32));
+        }
+        __syncthreads();
+        return count;
+    }
     for (u32 i = count + tid; i < n2; i += BLOCK) { // padding sorts last
         st_cg(meetbuf + 4 * static_cast<u64>(i), 0xffffffffu);
         st_cg(meetbuf + 4 * static_cast<u64>(i) + 1, 0xffffffffu);
