@@ -209,6 +209,31 @@ def test_final_level_probe_is_result_identical(block, items):
     assert wf["V_set"] < ow["V_set"] and wf["F_chk"] < ow["F_chk"]   # last-level vertices are not settled
 
 
+@pytest.mark.parametrize("block,bitmap", [(32, "0"), (32, "1"), (128, "0"), (128, "1")])
+def test_large_contact_sets_are_resolved_without_settling(block, bitmap, monkeypatch):
+    """A probed final level with far more contact edges than the shared-memory resolver holds (7800 here)
+    goes through meet_from_edges_large: sigma sums per member by atomics in global scratch (they saturate at
+    2^64-1 here), members ordered by a bitonic sort -- in shared memory when they fit (130 <= 512 at 128
+    threads), in the meet buffer otherwise (130 > 128 at 32 threads).  Layers 40^12 -> 60 -> 130 <- 60 <- 40^12:
+    the frontier more than doubles into the middle, sigma reaches 40^12 * 60 > 2^64 there."""
+    monkeypatch.setenv("EBC_BITMAP", bitmap)
+    widths = [2] + [40] * 12 + [60, 130, 60] + [40] * 12 + [2]
+    off, tg = complete_bipartite_chain(widths)
+    core = len(off) - 1
+    n = 60000                                     # isolated padding: the contact-edge buffer scales with n
+    off = np.concatenate([off, np.full(n - core, off[-1], dtype=np.uint64)])
+    pairs = np.array([[0, core - 1], [1, core - 2], [core - 1, 0], [0, core - 2], [core - 2, 1]], dtype=np.uint32)
+    s, o = check_samples((off, tg), len(pairs), ebc.RunConfig(block_threads=block, slots=2), pairs=pairs)
+    rec, _ = s.sample_debug(SEED, 0, len(pairs), pairs=pairs)
+    assert np.all((rec["flags"] & 2) != 0) and np.all((rec["flags"] & 5) == 0)   # probed, nothing fell back
+    assert np.all(rec["meet_count"] == 130)
+    o.sample(SEED, 0, pair=(0, core - 1))
+    fs, bs = o.last_state(0)[1], o.last_state(1)[1]
+    assert max(int(fs[v]) for v in o.last_meet_set()) == 2 ** 64 - 1 or max(int(bs[v]) for v in o.last_meet_set()) == 2 ** 64 - 1
+    total = min(sum(int(fs[v]) * int(bs[v]) for v in o.last_meet_set()), 2 ** 128 - 1)
+    assert (int(rec[0]["weight_hi"]) << 64) | int(rec[0]["weight_lo"]) == total
+
+
 def test_final_level_probe_with_tiny_edge_buffer_falls_back():
     """slot_capacity so small that the contact-edge buffer overflows: expand_level / large-slot fallbacks."""
     g = ebc.gen_rmat(13, 16, seed=9).largest_connected_component()
