@@ -1034,60 +1034,67 @@ __device__ __noinline__ u32 meet_from_edges_large(const u32 *edges, u32 m, u32 o
     u32 n2 = 1;
     while (n2 < count)
         n2 <<= 1;
-    if (count <= static_cast<u32>(FinalEdgeCap<BLOCK>::value)) {
-        // Few members (the usual case: many contact edges, most of them to deeper levels of the other side or
-        // to the same vertices): the same network in shared memory, on the arrays of meet_from_edges.
-        for (u32 i = tid; i < n2; i += BLOCK) {
-            const u32 *w = meetbuf + 4 * static_cast<u64>(i);
-            const bool real = i < count;
-            sh.f_key[i] = real ? (static_cast<u64>(ld_cg(w)) << 32) | ld_cg(w + 1) : ~0ull;
-            sh.f_v[i] = real ? ld_cg(w + 2) : 0u;
-            sh.f_o[i] = real ? ld_cg(w + 3) : 0u;
-        }
-        __syncthreads();
-#pragma unroll 1
-        for (u32 k = 2; k <= n2; k <<= 1) {
-#pragma unroll 1
-            for (u32 j = k >> 1; j > 0; j >>= 1) {
-                for (u32 t = tid; t < (n2 >> 1); t += BLOCK) {
-                    const u32 i = ((t & ~(j - 1)) << 1) | (t & (j - 1)), q = i | j;
-                    const u64 ka = sh.f_key[i], kb = sh.f_key[q];
-                    if ((ka > kb) == ((i & k) == 0)) {
-                        sh.f_key[i] = kb;
-                        sh.f_key[q] = ka;
-                        const u32 va = sh.f_v[i], oa = sh.f_o[i];
-                        sh.f_v[i] = sh.f_v[q];
-                        sh.f_o[i] = sh.f_o[q];
-                        sh.f_v[q] = va;
-                        sh.f_o[q] = oa;
-                    }
-                }
-                __syncthreads();
-            }
-        }
-        for (u32 i = tid; i < count; i += BLOCK) {
-            u32 *w = meetbuf + 4 * static_cast<u64>(i);
-            const u32 oi = sh.f_o[i];
-            const u64 sg = ld_cg(sum + (oi - olo));
-            st_cg(w + 0, sh.f_v[i]);
-            st_cg(w + 1, oi);
-            st_cg(w + 2, static_cast<u32>(sg));
-            st_cg(w + 3, static_cast<u32>(sg >> 32));
-        }
-        __syncthreads();
-        return count;
-    }
     for (u32 i = count + tid; i < n2; i += BLOCK) { // padding sorts last
         st_cg(meetbuf + 4 * static_cast<u64>(i), 0xffffffffu);
         st_cg(meetbuf + 4 * static_cast<u64>(i) + 1, 0xffffffffu);
     }
     __syncthreads();
+    // Bitonic network over n2 entries.  Steps whose partner distance is below the chunk length run in shared
+    // memory (the arrays of meet_from_edges), chunk by chunk; only the few wider steps of a member set that
+    // does not fit go through global memory.  Usually n2 <= len and the whole sort is one chunk.
+    const u32 len = n2 < static_cast<u32>(FinalEdgeCap<BLOCK>::value) ? n2 : static_cast<u32>(FinalEdgeCap<BLOCK>::value);
+    auto chunk_in = [&](u32 base) {
+        for (u32 i = tid; i < len; i += BLOCK) {
+            const u32 *w = meetbuf + 4 * static_cast<u64>(base + i);
+            sh.f_key[i] = (static_cast<u64>(ld_cg(w)) << 32) | ld_cg(w + 1);
+            sh.f_v[i] = ld_cg(w + 2);
+            sh.f_o[i] = ld_cg(w + 3);
+        }
+        __syncthreads();
+    };
+    auto chunk_out = [&](u32 base) {
+        for (u32 i = tid; i < len; i += BLOCK) {
+            u32 *w = meetbuf + 4 * static_cast<u64>(base + i);
+            st_cg(w + 0, static_cast<u32>(sh.f_key[i] >> 32));
+            st_cg(w + 1, static_cast<u32>(sh.f_key[i]));
+            st_cg(w + 2, sh.f_v[i]);
+            st_cg(w + 3, sh.f_o[i]);
+        }
+        __syncthreads();
+    };
+    auto chunk_steps = [&](u32 base, u32 k, u32 j_from) { // steps j_from, j_from/2, ..., 1 of stage k on one chunk
 #pragma unroll 1
-    for (u32 k = 2; k <= n2; k <<= 1) {
+        for (u32 j = j_from; j > 0; j >>= 1) {
+            for (u32 t = tid; t < (len >> 1); t += BLOCK) {
+                const u32 i = ((t & ~(j - 1)) << 1) | (t & (j - 1)), q = i | j; // t with a zero inserted at bit log2(j)
+                const u64 ka = sh.f_key[i], kb = sh.f_key[q];
+                if ((ka > kb) == (((base + i) & k) == 0)) {
+                    sh.f_key[i] = kb;
+                    sh.f_key[q] = ka;
+                    const u32 va = sh.f_v[i], oa = sh.f_o[i];
+                    sh.f_v[i] = sh.f_v[q];
+                    sh.f_o[i] = sh.f_o[q];
+                    sh.f_v[q] = va;
+                    sh.f_o[q] = oa;
+                }
+            }
+            __syncthreads();
+        }
+    };
 #pragma unroll 1
-        for (u32 j = k >> 1; j > 0; j >>= 1) {
+    for (u32 base = 0; base < n2; base += len) { // stages 2 .. len, chunk by chunk
+        chunk_in(base);
+#pragma unroll 1
+        for (u32 k = 2; k <= len; k <<= 1)
+            chunk_steps(base, k, k >> 1);
+        chunk_out(base);
+    }
+#pragma unroll 1
+    for (u32 k = len << 1; k <= n2 && k != 0; k <<= 1) { // wider stages: global steps down to the chunk length
+#pragma unroll 1
+        for (u32 j = k >> 1; j >= len; j >>= 1) {
             for (u32 t = tid; t < (n2 >> 1); t += BLOCK) {
-                const u32 i = ((t & ~(j - 1)) << 1) | (t & (j - 1)); // t with a zero inserted at bit log2(j)
+                const u32 i = ((t & ~(j - 1)) << 1) | (t & (j - 1));
                 u32 *a = meetbuf + 4 * static_cast<u64>(i), *b = meetbuf + 4 * static_cast<u64>(i | j);
                 const u32 a0 = ld_cg(a), a1 = ld_cg(a + 1), b0 = ld_cg(b), b1 = ld_cg(b + 1);
                 const u64 ka = (static_cast<u64>(a0) << 32) | a1, kb = (static_cast<u64>(b0) << 32) | b1;
@@ -1104,6 +1111,12 @@ __device__ __noinline__ u32 meet_from_edges_large(const u32 *edges, u32 m, u32 o
                 }
             }
             __syncthreads();
+        }
+#pragma unroll 1
+        for (u32 base = 0; base < n2; base += len) {
+            chunk_in(base);
+            chunk_steps(base, k, len >> 1);
+            chunk_out(base);
         }
     }
     for (u32 i = tid; i < count; i += BLOCK) {

@@ -4,7 +4,7 @@ import sys; sys.path.insert(0, '.')
 import numpy as np, paper_1910_11039_b200 as ebc
 c = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 N = int(sys.argv[2]) if len(sys.argv) > 2 else 50000
-scale, seed = {2: (20, 2), 4: (24, 4)}[c]
+scale, seed = {2: (20, 2), 4: (24, 4), 5: (26, 5), 22: (22, 2)}[c]
 g = ebc.gen_rmat_device(scale, 16, seed=seed).largest_connected_component(device=-1)
 s = ebc.Sampler(g, ebc.RunConfig())
 rec, _ = s.sample_debug(7, 0, N, path_stride=1)
