@@ -1016,10 +1016,10 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
     if (per_sm < 1)
         throw CudaError("sampling kernel does not fit on an SM");
     u64 cap = opt.slot_capacity ? std::min<u64>(opt.slot_capacity, g.n)
-                                : std::min<u64>(g.n, std::max<u64>(u64{1} << 17, g.n / 4));
-    // (n/4 is not generous: on R-MAT graphs about 1 % of the samples settle more than n/6 vertices on one
-    // side -- a non-final level behind a hub -- and n/6 already costs 10x throughput through the re-run
-    // path; measured in profiles/r01_capacity_sweep.txt.)
+                                : std::min<u64>(g.n, std::max<u64>(u64{1} << 17, g.n / 8));
+    // (While large final levels were still settled, n/6 instead of n/4 cost 10x throughput through the re-run
+    // path on R-MAT graphs; now that they are only scanned, n/16 runs as fast as n/4 on R-MAT-20/24/26 --
+    // profiles/r01_capacity_sweep.txt.  n/8 lets config 5 keep two 512-thread CTAs per SM.)
     cap = std::max<u64>(cap, 2);
     u64 slots = opt.slots ? opt.slots : static_cast<u64>(per_sm) * m.sm_count;
     const u64 capacity = pool().capacity();
