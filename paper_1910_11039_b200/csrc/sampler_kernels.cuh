@@ -605,9 +605,15 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
                     if (candidate[k])
                         red_max_u32(lab + 2 * static_cast<u64>(v[k]) + e, kClaimTop - (k * BLOCK + tid));
                 __syncthreads(); // claims visible
+                // A candidate reads back the claim that won its target: its own (winner) or the winning slot's,
+                // through which it later finds the winner's idx in shared memory (no second look at the label).
+                static_assert(sizeof(u32) * TILE <= sizeof(sh.f_key) + sizeof(sh.f_s), "tile idx table aliases f_key/f_s");
+                u32 *tile_idx = reinterpret_cast<u32 *>(sh.f_key); // (f_key, f_s are only live in the meet phase)
+                u32 won_by[ITEMS];
 #pragma unroll
                 for (int k = 0; k < ITEMS; ++k) {
-                    win[k] = candidate[k] && ld_cg(lab + 2 * static_cast<u64>(v[k]) + e) == kClaimTop - (k * BLOCK + tid);
+                    won_by[k] = candidate[k] ? kClaimTop - ld_cg(lab + 2 * static_cast<u64>(v[k]) + e) : 0u;
+                    win[k] = candidate[k] && won_by[k] == static_cast<u32>(k * BLOCK + tid);
                     is_contact[k] = win[k] && other_idx[k] < ot.cnt;
                 }
                 const u32 winners = block_ranks<BLOCK, ITEMS>(win, rank, sh.warp_cnt);
@@ -620,6 +626,7 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
                             st_cg(lab + 2 * static_cast<u64>(v[k]) + e, 0u); // undo the claim
                         } else {
                             idx[k] = cnt + rank[k];
+                            tile_idx[k * BLOCK + tid] = idx[k];
                             st_cg(lab + 2 * static_cast<u64>(v[k]) + e, ex.base + idx[k]);
                             st_cg(ex.pp->list + idx[k], v[k]);
                             st_cg(ex.pp->sig + idx[k], static_cast<u64>(0));
@@ -640,7 +647,7 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
 #pragma unroll
                 for (int k = 0; k < ITEMS; ++k) {
                     if (candidate[k] && !win[k])
-                        idx[k] = ld_cg(lab + 2 * static_cast<u64>(v[k]) + e) - ex.base; // the winner's label
+                        idx[k] = tile_idx[won_by[k]]; // the winner's idx
                     if (candidate[k] || at_level[k]) {
                         sat_atomic_add(ex.pp->sig + idx[k], sig_u[k], sigma_small); // sampler.cpp:97-98
                         wk.e_lvl += 1;
