@@ -255,7 +255,9 @@ typedef struct ebc_sample_record {
     uint32_t meet_count;  /* |meet set|                                   */
     uint32_t draws;       /* random draws consumed                        */
     uint32_t path_len;    /* internal vertices                            */
-    uint32_t flags;       /* bit0: capacity overflow (re-run in big slot) */
+    uint32_t flags;       /* bit0: capacity overflow (re-run in big slot); bit1: the final level was resolved by the
+                           * read-only probe (not settled); bit2: a probe found contact edges it could not resolve
+                           * (buffer or scratch too small) and the level was expanded instead */
     uint64_t weight_lo, weight_hi; /* total meet weight (saturating u128) */
 } ebc_sample_record;
 
