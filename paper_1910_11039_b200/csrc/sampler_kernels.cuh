@@ -148,8 +148,9 @@ constexpr int kPredCache = 32;
 
 // Final-level probe (see probe_level): a level with at least SamplerParams::probe_min_slots adjacency
 // slots (256 with visited bitmaps, else 512; set by the host) is first scanned read-only; if it touches
-// the other side, the meet set is resolved from at most FinalEdgeCap<BLOCK>::value contact edges and the
-// level is never settled.
+// the other side, the meet set is resolved from the contact edges and the level is never settled: up to
+// FinalEdgeCap<BLOCK>::value edges in shared memory (meet_from_edges), more -- as many as the slot's
+// contact buffer holds -- in the slot's global arrays (meet_from_edges_large).
 // Slots per thread of the probe pass relative to the expansion.  Measured on R-MAT-20: 128x4 threads x
 // slots: factor 1 4.94 M samples/s, 2 4.41 M, 4 3.35 M; 128x2: 4.82 / 5.00 / 4.60 M -- beyond four
 // probes in flight per thread the memory system, not latency, is the limit.
