@@ -999,18 +999,14 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
         if (want && !opt.materialize_final_level)
             m.flags |= kFlagUseBitmap;
     }
-    {
-        // Hub-clustered numbering: on graphs with hubs most adjacency entries name a few high-degree
-        // vertices; numbering by descending degree puts their labels / visited bits next to each other
-        // (measured on R-MAT: +11 % at scale 20, +26 % at scale 24; +30..65 % when the input ids are
-        // arbitrary).  Low-degree graphs keep their own numbering, which usually is spatially coherent.
-        bool want = opt.renumber > 0 || (opt.renumber == 0 && m.hub_graph);
-        if (const char *env = std::getenv("EBC_RENUMBER"))
-            want = std::atoi(env) != 0;
-        if (want && m.arcs && m.n < (u64{1} << 31)) // (the CUB passes take 32-bit counts)
-            m.build_dense_graph();
-        lap("dense numbering");
-    }
+    // Hub-clustered numbering: on graphs with hubs most adjacency entries name a few high-degree
+    // vertices; numbering by descending degree puts their labels / visited bits next to each other
+    // (measured on R-MAT: +11 % at scale 20, +26 % at scale 24; +30..65 % when the input ids are
+    // arbitrary).  Low-degree graphs keep their own numbering, which usually is spatially coherent.
+    bool want_dense = opt.renumber > 0 || (opt.renumber == 0 && m.hub_graph);
+    if (const char *env = std::getenv("EBC_RENUMBER"))
+        want_dense = std::atoi(env) != 0;
+    want_dense = want_dense && m.arcs && m.n < (u64{1} << 31); // (the CUB passes take 32-bit counts)
     const int per_sm = occupancy_for(m.block, m.items);
     lap("occupancy query");
     if (per_sm < 1)
@@ -1026,7 +1022,8 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
     const u64 live = pool().live_bytes();
     lap("memory query");
     const u64 fixed = (g.n + 1) * (4 * 2 + 8 + 8 + 16 + 12) + (u64{256} << 20) + kOverflowCap * 4 +
-                      (cap < g.n ? kLargeSlots * SlotArrays::bytes_per_slot(g.n, g.n) : 0);
+                      (cap < g.n ? kLargeSlots * SlotArrays::bytes_per_slot(g.n, g.n) : 0) +
+                      (want_dense ? g.n * 40 + m.arcs * 4 + (u64{16} << 20) : 0); // the dense copy is built below
     // Buffers cached by the pool are reusable (or released on demand), so they count as free.
     const u64 avail = capacity > live ? capacity - live : 0;
     const u64 budget = avail > fixed ? (avail - fixed) / 10 * 8 : 0;
@@ -1035,10 +1032,15 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
         slots = budget / per_slot;
     if (slots < 1)
         throw CudaError("not enough device memory for a single sampling slot");
-    m.small.allocate(slots, cap, g.n, m.s_sample);
+    // The slot arrays are cleared on the aggregation stream while the graph is still crossing PCIe on the
+    // sampling stream (the numbering below waits for it).
+    m.small.allocate(slots, cap, g.n, m.s_agg);
     if (cap < g.n)
-        m.big.allocate(kLargeSlots, g.n, g.n, m.s_sample);
+        m.big.allocate(kLargeSlots, g.n, g.n, m.s_agg);
     lap("slot arrays");
+    if (want_dense)
+        m.build_dense_graph();
+    lap("dense numbering");
 
     // ---- frames, state, bookkeeping ----
     for (int i = 0; i < 2; ++i) {
