@@ -145,10 +145,11 @@ typedef struct ebc_run_config {
     int bound;                 /* 0 Hoeffding | 1 empirical Bernstein (stopping.hpp:18-21) */
     int allocator;             /* 0 uniform | 1 weighted (stopping.hpp:23-26)              */
     uint64_t omega_override;   /* RunConfig::omega_override; 0 = formula                   */
-    uint64_t calib_samples;    /* total calibration samples (reference: 100 per worker)    */
+    uint64_t calib_samples;    /* total calibration samples (reference: 100 per worker); < 2^32 */
     int diameter_sweeps;       /* RunConfig::diameter_sweeps (default 4)                   */
     uint64_t vertex_diameter_override; /* 0 = run the diameter phase                      */
-    uint64_t epoch_samples;    /* samples per epoch over ALL ranks; 0 = derive from omega and the rule */
+    uint64_t epoch_samples;    /* samples per epoch over ALL ranks; 0 = derive from omega and the rule; < 2^32
+                                  (epoch frames are 32-bit words), else EBC_ERR_CONFIG */
     uint64_t max_epochs;       /* safety cap; 0 = unlimited                                */
     int device;                /* CUDA device ordinal; -1 = current device                 */
     int rank, world_size;      /* this process' shard of every epoch (one process per GPU) */

@@ -123,6 +123,13 @@ class Graph:
         o = np.ascontiguousarray(offsets, dtype=np.uint64)
         t = np.ascontiguousarray(targets, dtype=np.uint32)
         ids = None if original_ids is None else np.ascontiguousarray(original_ids, dtype=np.uint64)
+        # the native side copies offsets[0..n], targets[0..offsets[n]) and ids[0..n): the buffers must hold them
+        if o.ndim != 1 or t.ndim != 1 or len(o) < 1:
+            raise ConfigError("from_csr: offsets must be a non-empty 1-d array (n + 1 entries)")
+        if int(o[-1]) != len(t):
+            raise ConfigError("from_csr: offsets[n] must equal len(targets)")
+        if ids is not None and (ids.ndim != 1 or len(ids) != len(o) - 1):
+            raise ConfigError("from_csr: original_ids must hold n entries")
         return cls._new(_capi.load().ebc_graph_from_csr, len(o) - 1, _p(o, _capi.u64p), _p(t, _capi.u32p),
                         None if ids is None else _p(ids, _capi.u64p), int(validate))
 

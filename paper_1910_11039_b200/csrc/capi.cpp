@@ -725,7 +725,8 @@ const NcclApi &nccl_api() {
                 break;
         }
         if (!h) {
-            a.why = std::string("libnccl.so.2 not found: ") + (dlerror() ? dlerror() : "");
+            const char *err = dlerror(); // (a second call would return null: the first one clears the state)
+            a.why = std::string("libnccl.so.2 not found: ") + (err ? err : "");
             return a;
         }
         a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));

@@ -17,7 +17,8 @@
 #include <mutex>
 #include <string>
 
-#include "sampler_kernels.cuh"
+#include "device_types.cuh"
+#include "sample_launch.hpp"
 
 namespace ebc {
 
@@ -587,27 +588,18 @@ __global__ void flush_kernel(u32 *buf, u64 count, u32 salt) {
         buf[i] = static_cast<u32>(i) ^ salt;
 }
 
-// (BLOCK, ITEMS) instantiations of the sampling kernel.
-#ifdef EBC_FEW_SHAPES // faster experimental builds
-#define EBC_FOR_EACH_SHAPE(X) X(32, 1) X(64, 2) X(64, 4) X(128, 2) X(128, 4) X(256, 4)
-#else
-#define EBC_FOR_EACH_SHAPE(X) \
-    X(32, 1) X(32, 2) X(32, 4) X(64, 1) X(64, 2) X(64, 4) X(128, 1) X(128, 2) X(128, 4) X(256, 1) X(256, 2) \
-    X(256, 4) X(512, 1) X(512, 2) X(512, 4)
-#endif
-
+// The (BLOCK, ITEMS) instantiations of the sampling kernel are compiled in their own translation units, one per
+// block size (sample_launch.cu, built five times with -DEBC_SHAPE_BLOCK=...), so that they compile in parallel.
 void launch_sample_dispatch(u32 block, u32 items, const SamplerParams &p, u32 grid, cudaStream_t stream) {
     bool done = false;
-#define EBC_LAUNCH(B, I)                                       \
-    if (!done && block == B && items == I) {                       \
-        if (p.flags & kFlagUseBitmap)                              \
-            sample_kernel<B, I, true><<<grid, B, 0, stream>>>(p);  \
-        else                                                       \
-            sample_kernel<B, I, false><<<grid, B, 0, stream>>>(p); \
-        done = true;                                               \
+    switch (block) {
+    case 32: done = launch_sample_b32(items, p, grid, stream); break;
+    case 64: done = launch_sample_b64(items, p, grid, stream); break;
+    case 128: done = launch_sample_b128(items, p, grid, stream); break;
+    case 256: done = launch_sample_b256(items, p, grid, stream); break;
+    case 512: done = launch_sample_b512(items, p, grid, stream); break;
+    default: break;
     }
-    EBC_FOR_EACH_SHAPE(EBC_LAUNCH)
-#undef EBC_LAUNCH
     if (!done)
         throw ConfigError("block_threads must be one of 32, 64, 128, 256, 512 and items_per_thread one of 1, 2, 4");
     EBC_CUDA(cudaGetLastError());
@@ -615,13 +607,18 @@ void launch_sample_dispatch(u32 block, u32 items, const SamplerParams &p, u32 gr
 
 int occupancy_for(u32 block, u32 items) {
     int per_sm = -1;
-#define EBC_OCC(B, I)                                                                                   \
-    if (per_sm < 0 && block == B && items == I)                                                         \
-        EBC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sample_kernel<B, I, true>, B, 0));
-    EBC_FOR_EACH_SHAPE(EBC_OCC)
-#undef EBC_OCC
-    if (per_sm < 0)
+    switch (block) {
+    case 32: per_sm = sample_occupancy_b32(items); break;
+    case 64: per_sm = sample_occupancy_b64(items); break;
+    case 128: per_sm = sample_occupancy_b128(items); break;
+    case 256: per_sm = sample_occupancy_b256(items); break;
+    case 512: per_sm = sample_occupancy_b512(items); break;
+    default: break;
+    }
+    if (per_sm == -1)
         throw ConfigError("block_threads must be one of 32, 64, 128, 256, 512 and items_per_thread one of 1, 2, 4");
+    if (per_sm < -1)
+        throw CudaError("cudaOccupancyMaxActiveBlocksPerMultiprocessor failed for the sampling kernel");
     return per_sm;
 }
 
@@ -705,6 +702,7 @@ void release_device_cache() {
 }
 
 struct CudaSampler::Impl {
+    ~Impl();
     int device = 0;
     int sm_count = 0;
     u64 n = 0, arcs = 0;
@@ -1080,8 +1078,11 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
         pool().stats("after ctor");
 }
 
-CudaSampler::~CudaSampler() {
-    Impl &m = *impl_;
+// Everything the sampler holds goes back to the process-wide caches here, in the destructor of Impl, so that a
+// constructor that throws half way (out of memory, kernel does not fit, ...) returns what it had taken:
+// impl_ is a complete member by then and is destroyed during unwinding.  Null handles are skipped.
+CudaSampler::Impl::~Impl() {
+    Impl &m = *this;
     const bool trace = std::getenv("EBC_TRACE") != nullptr;
     const auto t0 = std::chrono::steady_clock::now();
     cudaDeviceSynchronize();
@@ -1133,6 +1134,8 @@ CudaSampler::~CudaSampler() {
         std::fprintf(stderr, "[ebc] ~CudaSampler: total %.3f ms\n",
                      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
 }
+
+CudaSampler::~CudaSampler() = default;
 
 std::uint64_t CudaSampler::n() const { return impl_->n; }
 std::uint64_t CudaSampler::overflow_samples() const {
@@ -1242,8 +1245,11 @@ void CudaSampler::set_stopping(double eps, std::uint64_t omega, const double *de
     std::vector<double> lo(m.n), up(m.n);
     bound_log_terms(delta_lower, m.n, bound, lo.data());
     bound_log_terms(delta_upper, m.n, bound, up.data());
-    EBC_CUDA(cudaMemcpy(m.d_log_lower, lo.data(), m.n * 8, cudaMemcpyHostToDevice));
-    EBC_CUDA(cudaMemcpy(m.d_log_upper, up.data(), m.n * 8, cudaMemcpyHostToDevice));
+    // (on the stream that reads them; a pageable cudaMemcpy only orders against the legacy stream, which the
+    // sampler's non-blocking streams do not synchronise with)
+    EBC_CUDA(cudaMemcpyAsync(m.d_log_lower, lo.data(), m.n * 8, cudaMemcpyHostToDevice, m.s_agg));
+    EBC_CUDA(cudaMemcpyAsync(m.d_log_upper, up.data(), m.n * 8, cudaMemcpyHostToDevice, m.s_agg));
+    EBC_CUDA(cudaStreamSynchronize(m.s_agg)); // lo / up go out of scope
     m.stop.eps = eps;
     m.stop.omega = omega;
     m.stop.log_lower = m.d_log_lower;
@@ -1325,25 +1331,28 @@ void CudaSampler::read_frame(int which, std::uint64_t *words_out) {
 void CudaSampler::write_state(const std::uint64_t *words) {
     Impl &m = *impl_;
     m.sync_sampling();
+    EBC_CUDA(cudaMemcpyAsync(m.d_S, words, (m.n + 1) * 8, cudaMemcpyHostToDevice, m.s_agg));
     EBC_CUDA(cudaStreamSynchronize(m.s_agg));
-    EBC_CUDA(cudaMemcpy(m.d_S, words, (m.n + 1) * 8, cudaMemcpyHostToDevice));
 }
 
 void CudaSampler::clear() {
     Impl &m = *impl_;
     m.sync_sampling();
-    EBC_CUDA(cudaStreamSynchronize(m.s_agg));
+    // All streams are idle here; the memsets run on the aggregation stream and are complete on return, so
+    // whatever the caller launches next (on any of the sampler's streams) is ordered behind them.
     for (int i = 0; i < 2; ++i)
-        EBC_CUDA(cudaMemset(m.d_frame[i], 0, (m.n + 1) * 4));
-    EBC_CUDA(cudaMemset(m.d_S, 0, (m.n + 1) * 8));
+        EBC_CUDA(cudaMemsetAsync(m.d_frame[i], 0, (m.n + 1) * 4, m.s_agg));
+    EBC_CUDA(cudaMemsetAsync(m.d_S, 0, (m.n + 1) * 8, m.s_agg));
+    EBC_CUDA(cudaStreamSynchronize(m.s_agg));
 }
 
 void CudaSampler::work(std::uint64_t *out, bool reset) {
     Impl &m = *impl_;
     m.sync_sampling();
-    EBC_CUDA(cudaMemcpy(out, m.d_work, kWorkCounters * 8, cudaMemcpyDeviceToHost));
+    EBC_CUDA(cudaMemcpyAsync(out, m.d_work, kWorkCounters * 8, cudaMemcpyDeviceToHost, m.s_sample));
     if (reset)
-        EBC_CUDA(cudaMemset(m.d_work, 0, kWorkCounters * 8));
+        EBC_CUDA(cudaMemsetAsync(m.d_work, 0, kWorkCounters * 8, m.s_sample));
+    EBC_CUDA(cudaStreamSynchronize(m.s_sample)); // both lanes are idle: the next launch on either sees the reset
 }
 
 void CudaSampler::mark(int event) {

@@ -33,6 +33,10 @@ void RunConfig::validate() const {
         throw ConfigError("unknown allocator kind");
     if (diameter_sweeps < 1)
         throw ConfigError("run config: need at least one diameter sweep");
+    // Epoch frames are u32 (word 0 = the epoch's tau, hub counters <= tau): an epoch or a calibration batch
+    // must stay below 2^32 samples or the words wrap.
+    if (epoch_samples >= (std::uint64_t{1} << 32) || calib_samples >= (std::uint64_t{1} << 32))
+        throw ConfigError("run config: epoch_samples and calib_samples must be below 2^32 (epoch frames are 32-bit)");
 }
 
 std::uint64_t default_epoch_samples(std::uint64_t omega, bool adaptive_rule) {

@@ -180,9 +180,11 @@ HostGraph graph_from_csr(std::uint64_t n, const std::uint64_t *offsets, const st
                 g.original_ids[v] = v;
     });
     if (validate) {
+        // Offsets first, all of them: nothing below may index targets (or offsets[v]) through an unchecked value.
+        for (std::uint64_t u = 0; u < n; ++u)
+            if (g.offsets[u + 1] < g.offsets[u] || g.offsets[u + 1] > arcs)
+                throw ConfigError("graph_from_csr: offsets not monotone or beyond offsets[n]");
         for (std::uint64_t u = 0; u < n; ++u) {
-            if (g.offsets[u + 1] < g.offsets[u])
-                throw ConfigError("graph_from_csr: offsets not monotone");
             for (std::uint64_t i = g.offsets[u]; i < g.offsets[u + 1]; ++i) {
                 const std::uint32_t v = g.targets[i];
                 if (v >= n)

@@ -1,0 +1,49 @@
+// Instantiations of the sampling kernel for ONE block size (EBC_SHAPE_BLOCK, set by the build) and 1, 2 or 4
+// adjacency slots per thread, with and without visited bitmaps.  Compiled once per block size so that the
+// fifteen shapes build in parallel; nothing here but the launches.
+#include "sample_launch.hpp"
+#include "sampler_kernels.cuh"
+
+#ifndef EBC_SHAPE_BLOCK
+#error "compile with -DEBC_SHAPE_BLOCK=32|64|128|256|512"
+#endif
+
+namespace ebc {
+
+#define EBC_CAT2(a, b) a##b
+#define EBC_CAT(a, b) EBC_CAT2(a, b)
+
+template <int ITEMS> static void launch_one(const SamplerParams &p, u32 grid, cudaStream_t stream) {
+    if (p.flags & kFlagUseBitmap)
+        sample_kernel<EBC_SHAPE_BLOCK, ITEMS, true><<<grid, EBC_SHAPE_BLOCK, 0, stream>>>(p);
+    else
+        sample_kernel<EBC_SHAPE_BLOCK, ITEMS, false><<<grid, EBC_SHAPE_BLOCK, 0, stream>>>(p);
+}
+
+bool EBC_CAT(launch_sample_b, EBC_SHAPE_BLOCK)(u32 items, const SamplerParams &p, u32 grid, cudaStream_t stream) {
+    switch (items) {
+    case 1: launch_one<1>(p, grid, stream); return true;
+    case 2: launch_one<2>(p, grid, stream); return true;
+    case 4: launch_one<4>(p, grid, stream); return true;
+    default: return false;
+    }
+}
+
+template <int ITEMS> static int occupancy_one() {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sample_kernel<EBC_SHAPE_BLOCK, ITEMS, true>, EBC_SHAPE_BLOCK, 0) !=
+        cudaSuccess)
+        return -2;
+    return per_sm;
+}
+
+int EBC_CAT(sample_occupancy_b, EBC_SHAPE_BLOCK)(u32 items) {
+    switch (items) {
+    case 1: return occupancy_one<1>();
+    case 2: return occupancy_one<2>();
+    case 4: return occupancy_one<4>();
+    default: return -1;
+    }
+}
+
+} // namespace ebc

@@ -108,7 +108,7 @@ __device__ __forceinline__ void sat_atomic_add(u64 *p, u64 add, bool small) {
 // a % b for b >= 2^64 by restoring division, one bit per iteration.  Only the wide rejection sampler
 // below uses it (total weights >= 2^64); the compiler's inline 128-bit division is ~100 instructions
 // per use, and the kernel's instruction footprint is what it is short of (profiles/r01_icache.txt).
-__device__ __noinline__ u128 umod128_compact(u128 a, u128 b) {
+static __device__ __noinline__ u128 umod128_compact(u128 a, u128 b) {
     u128 r = 0;
 #pragma unroll 1
     for (int i = 127; i >= 0; --i) {
@@ -119,7 +119,7 @@ __device__ __noinline__ u128 umod128_compact(u128 a, u128 b) {
     }
     return r;
 }
-__device__ __noinline__ u128 uniform_below_wide(SampleStream &rng, u128 bound) {
+static __device__ __noinline__ u128 uniform_below_wide(SampleStream &rng, u128 bound) {
     const u128 all = ~static_cast<u128>(0);
     const u128 reject_from = all - umod128_compact(all, bound);
     for (;;) {

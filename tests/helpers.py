@@ -78,3 +78,21 @@ def largest_component(offsets, targets):
     rows = np.repeat(np.arange(n), np.diff(offsets.astype(np.int64)))
     mask = (lab[rows] == best)
     return csr_from_edges(len(keep), remap[rows[mask]], remap[targets[mask].astype(np.int64)]), keep
+
+
+def oracle_frame(offsets, targets, seed, first, count, workers=None, tag=0):
+    """Frame (u64[n+1]) of sample indices [first, first+count) from the CPU oracle, the index range split
+    over worker threads (each with its own Oracle state; ctypes drops the GIL; frames are sums)."""
+    import concurrent.futures as cf
+    import os
+    from oracle import Oracle
+    workers = max(1, min(workers or os.cpu_count() or 1, 32, count // 64 or 1))
+    cuts = [first + count * w // workers for w in range(workers + 1)]
+
+    def job(w):
+        o = Oracle(offsets, targets)
+        return o.accumulate(seed, cuts[w], cuts[w + 1] - cuts[w], tag=tag)
+
+    with cf.ThreadPoolExecutor(workers) as ex:
+        parts = list(ex.map(job, range(workers)))
+    return np.sum(parts, axis=0, dtype=np.uint64)
