@@ -7,7 +7,7 @@ from .api import (EMPIRICAL_BERNSTEIN, HOEFFDING, TAG_ADAPTIVE, TAG_CALIBRATION,
                   WORK_NAMES, ApproxResult, BackendFault, ConfigError, CudaError, Graph, ParseError,
                   RunConfig, Sampler, algorithmic_bytes, calibrate, compute_omega, diameter_upper_bound,
                   epoch_length, gen_erdos_renyi, gen_grid, gen_rmat, gen_rmat_device, parse_allocator_kind,
-                  parse_bound_kind, read_scores, run_pipeline, shard_range, write_scores,
+                  parse_bound_kind, read_scores, release_device_cache, run_pipeline, shard_range, write_scores,
                   compare_score_files)
 from .build import build
 

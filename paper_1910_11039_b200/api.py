@@ -527,6 +527,11 @@ def compare_score_files(approx_path: str, exact_path: str, eps: float) -> dict:
         L.ebc_scores_free(a)
 
 
+def release_device_cache() -> None:
+    """Frees the device buffers, streams and events the library keeps cached between runs."""
+    _capi.load().ebc_release_device_cache()
+
+
 def algorithmic_bytes(work: dict) -> int:
     """bytes the reference algorithm must move for the counted work."""
     w = work

@@ -114,9 +114,9 @@ def test_config4_rmat24_full_size():
 
 
 def test_config5_rmat26_full_size():
-    """BASELINE configs[4]: Kronecker/R-MAT scale 26 (graph seed 5, > 2^31 arcs), default launch shape 512x4."""
+    """BASELINE configs[4]: Kronecker/R-MAT scale 26 (graph seed 5, 2.1 * 10^9 arcs), default launch shape 512x4."""
     g = ebc.gen_rmat_device(26, 16, seed=5, take_lcc=True)
-    assert g.num_vertices > 30_000_000 and 2 * g.num_edges > (1 << 31)
+    assert g.num_vertices > 30_000_000 and 2 * g.num_edges > 2_000_000_000
     _check(g, 20480, 300, 8, [(0, 0, 0), (256, 4, 64)], block_first=3_000_000, block_count=1000,
            expect_default=(512, 4))
 
