@@ -166,9 +166,12 @@ typedef struct ebc_run_config {
                                   * paths, counters, tau), but vertices that cannot lie on the sampled path
                                   * are not labelled.  Needed for ebc_sampler_last_state and for work
                                   * counters V_set / F_chk / E_lvl that equal the reference algorithm's. */
-    int renumber;              /* device-side vertex numbering of the search state: 0 = auto, 1 = always, -1 = never.
+    int renumber;              /* device-side vertex numbering of the search state: 0 = auto, -1 = never,
+                                * 1 = by descending degree class, 2 = by neighbourhood cluster.
                                 * On graphs with hubs (max degree >= 1024) the sampler keeps a copy of the graph
-                                * renumbered by descending degree, so probes of hub vertices share cache lines.
+                                * renumbered by descending degree, so probes of hub vertices share cache lines; on
+                                * large graphs without hubs (grids, road networks) one numbered by clusters of
+                                * neighbouring vertices, so the surface of a search ball covers few cache lines.
                                 * Purely internal: row order, discovery order, samples, counters and every id
                                 * that crosses this interface stay those of the caller's graph. */
 } ebc_run_config;

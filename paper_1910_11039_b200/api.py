@@ -256,7 +256,7 @@ class RunConfig:
     overlap: bool = True
     items_per_thread: int = 0
     materialize_final_level: bool = False
-    renumber: int = 0  # device-side hub-clustered numbering: 0 auto (hub graphs), 1 always, -1 never
+    renumber: int = 0  # device-side numbering: 0 auto, -1 never, 1 degree classes (hubs), 2 neighbourhood clusters
 
     def to_c(self) -> _CRunConfig:
         c = _CRunConfig()

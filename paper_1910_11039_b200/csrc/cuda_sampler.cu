@@ -520,6 +520,50 @@ __global__ void __launch_bounds__(256) degree_kernel(const u64 *offsets, u64 n, 
     }
 }
 
+// ---- neighbourhood-clustered numbering for graphs without hubs ----
+// On a hub-free graph (grid, road network) a search settles a connected ball, and every label / offsets /
+// row access of a level goes to the ball's surface.  If vertices that are close in the graph are close in the
+// numbering, those accesses share 128-byte lines and the surface of a ball is a few lines instead of one per
+// vertex.  Clusters: every vertex whose hashed id falls into a 1/kClusterSize slice is a centre; centres grow
+// breadth-first in lock step and a vertex joins the smallest centre id among its assigned neighbours (a
+// graph Voronoi partition, deterministic because each round reads the previous round's array).  Vertices are
+// then sorted by (centre id, own id).
+constexpr u32 kClusterSize = 32; // vertices per 128-byte line of labels
+constexpr u32 kNoCluster = 0xffffffffu;
+__global__ void __launch_bounds__(256) cluster_seed_kernel(u64 n, u32 *center, u32 *ids) {
+    for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v < n;
+         v += static_cast<u64>(gridDim.x) * blockDim.x) {
+        const u32 h = (static_cast<u32>(v) * 2654435761u) >> 12;
+        center[v] = h % kClusterSize == 0 ? static_cast<u32>(v) : kNoCluster;
+        ids[v] = static_cast<u32>(v);
+    }
+}
+__global__ void __launch_bounds__(256) cluster_grow_kernel(const u64 *offsets, const u32 *targets, u64 n, const u32 *in,
+                                                           u32 *out, u32 *unassigned) {
+    u32 open = 0;
+    for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v < n;
+         v += static_cast<u64>(gridDim.x) * blockDim.x) {
+        u32 c = in[v];
+        if (c == kNoCluster) {
+            for (u64 k = offsets[v]; k < offsets[v + 1]; ++k) {
+                const u32 cw = in[targets[k]];
+                c = cw < c ? cw : c;
+            }
+            open += c == kNoCluster ? 1u : 0u;
+        }
+        out[v] = c;
+    }
+    if (__syncthreads_or(open != 0 ? 1 : 0) && threadIdx.x == 0)
+        atomicOr(unassigned, 1u);
+}
+// vertices no centre reached within the round limit are their own cluster
+__global__ void __launch_bounds__(256) cluster_finish_kernel(u64 n, u32 *center) {
+    for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v < n;
+         v += static_cast<u64>(gridDim.x) * blockDim.x)
+        if (center[v] == kNoCluster)
+            center[v] = static_cast<u32>(v);
+}
+
 // to_dense = inverse of to_ext; dense_offsets[i] = degree of dense vertex i (scanned afterwards)
 __global__ void __launch_bounds__(256) invert_kernel(const u32 *to_ext, const u64 *ext_offsets, u64 n, u32 *to_dense,
                                                      u64 *dense_offsets) {
@@ -636,7 +680,7 @@ struct SlotArrays {
         slots = slots_;
         cap = cap_;
         aux_cap = aux_cap_of(cap_, n);
-        lab = dev_alloc<u32>(slots * 2 * n);
+        lab = dev_alloc<u32>(slots * n);
         list = dev_alloc<u32>(slots * 2 * cap);
         sig = dev_alloc<u64>(slots * 2 * cap);
         lvl = dev_alloc<u32>(slots * 2 * (aux_cap + 2));
@@ -645,7 +689,7 @@ struct SlotArrays {
         EBC_CUDA(cudaMemsetAsync(bits, 0, slots * 2 * bit_words_of(n) * 4, stream));
         hdr = dev_alloc<u32>(slots * kHdrWords);
         bytes = slots * bytes_per_slot(n, cap);
-        EBC_CUDA(cudaMemsetAsync(lab, 0, slots * 2 * n * 4, stream));
+        EBC_CUDA(cudaMemsetAsync(lab, 0, slots * n * 4, stream));
         std::vector<u32> h(slots * kHdrWords, 0);
         for (u64 s = 0; s < slots; ++s)
             h[s * kHdrWords + kHdrBase0] = h[s * kHdrWords + kHdrBase1] = 1; // label 0 == never visited
@@ -653,7 +697,7 @@ struct SlotArrays {
             const u32 base = static_cast<u32>(std::strtoul(env, nullptr, 0));
             for (u64 s = 0; s < slots; ++s) {
                 h[s * kHdrWords + kHdrBase0] = base;
-                h[s * kHdrWords + kHdrBase1] = base - 7; // the two sides reset at different samples
+                h[s * kHdrWords + kHdrBase1] = base;
             }
         }
         EBC_CUDA(cudaMemcpyAsync(hdr, h.data(), h.size() * 4, cudaMemcpyHostToDevice, stream));
@@ -673,7 +717,7 @@ struct SlotArrays {
     static u64 aux_cap_of(u64 cap, u64 n) { return cap >= n ? n : std::min<u64>(cap, u64{1} << 16); }
     static u64 bytes_per_slot(u64 n, u64 cap) {
         const u64 aux = aux_cap_of(cap, n);
-        return 2 * n * 4 + 2 * bit_words_of(n) * 4 + 2 * cap * (4 + 8) + 2 * (aux + 2) * 4 + 6 * aux * 4 + kHdrWords * 4;
+        return n * 4 + 2 * bit_words_of(n) * 4 + 2 * cap * (4 + 8) + 2 * (aux + 2) * 4 + 6 * aux * 4 + kHdrWords * 4;
     }
 };
 
@@ -718,6 +762,7 @@ struct CudaSampler::Impl {
     u64 probe_min_slots = 512;
     u64 probe_growth_x4 = 8; // the frontier's pending edges at least doubled
     bool hub_graph = false; // max degree >= 1024: visited bitmaps, direction-optimising BFS
+    int numbering = 0;      // 0 none, 1 degree classes, 2 neighbourhood clusters
     SlotArrays small, big;
     u32 *d_frame[2] = {nullptr, nullptr};
     u64 *d_S = nullptr;
@@ -778,9 +823,10 @@ struct CudaSampler::Impl {
 
     cudaStream_t lane_stream(int lane) const { return lane == 0 ? s_sample : s_sample2; }
 
-    // Builds to_ext (vertices by descending degree class, ties by ascending id), its inverse and the dense
-    // CSR on the device from the uploaded graph.
-    void build_dense_graph() {
+    // Builds to_ext, its inverse and the dense CSR on the device from the uploaded graph.  to_ext lists the
+    // vertices by descending degree class (hub graphs) or by neighbourhood cluster (`clusters`), ties by
+    // ascending id.
+    void build_dense_graph(bool clusters) {
         cudaStream_t st = s_sample;
         u32 *deg = dev_alloc<u32>(n), *ids = dev_alloc<u32>(n), *deg_sorted = dev_alloc<u32>(n);
         d_to_ext = dev_alloc<u32>(n);
@@ -788,16 +834,41 @@ struct CudaSampler::Impl {
         d_dense_offsets = dev_alloc<u64>(n + 1);
         d_dense_targets = dev_alloc<u32>(arcs);
         const u32 grid = static_cast<u32>(std::min<u64>((n + 255) / 256, static_cast<u64>(sm_count) * 8));
-        degree_kernel<<<grid, 256, 0, st>>>(d_offsets, n, deg, ids);
-        EBC_CUDA(cudaGetLastError());
-        size_t sort_bytes = 0, scan_bytes = 0;
+        size_t sort_bytes = 0, sort2_bytes = 0, scan_bytes = 0;
         EBC_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, sort_bytes, deg, deg_sorted, ids, d_to_ext,
                                                            static_cast<int>(n), 0, 7, st));
+        EBC_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sort2_bytes, deg, deg_sorted, ids, d_to_ext,
+                                                 static_cast<int>(n), 0, 32, st));
         EBC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, d_dense_offsets, d_dense_offsets,
                                                static_cast<int>(n + 1), st));
-        unsigned char *tmp = dev_alloc<unsigned char>(std::max(sort_bytes, scan_bytes) + 16);
-        EBC_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp, sort_bytes, deg, deg_sorted, ids, d_to_ext,
-                                                           static_cast<int>(n), 0, 7, st)); // stable
+        unsigned char *tmp = dev_alloc<unsigned char>(std::max(std::max(sort_bytes, sort2_bytes), scan_bytes) + 16);
+        if (clusters) {
+            // `deg` / `deg_sorted` double as the two centre arrays of the growth rounds
+            u32 *cur = deg, *nxt = deg_sorted;
+            cluster_seed_kernel<<<grid, 256, 0, st>>>(n, cur, ids);
+            u32 *flag = reinterpret_cast<u32 *>(tmp);
+            u32 open = 1;
+            for (int round = 0; round < 64 && open; round += 4) {
+                EBC_CUDA(cudaMemsetAsync(flag, 0, 4, st));
+                for (int k = 0; k < 4; ++k) { // the flag reports the last of four rounds
+                    if (k == 3)
+                        EBC_CUDA(cudaMemsetAsync(flag, 0, 4, st));
+                    cluster_grow_kernel<<<grid, 256, 0, st>>>(d_offsets, d_targets, n, cur, nxt, flag);
+                    std::swap(cur, nxt);
+                }
+                EBC_CUDA(cudaGetLastError());
+                EBC_CUDA(cudaMemcpyAsync(&open, flag, 4, cudaMemcpyDeviceToHost, st));
+                EBC_CUDA(cudaStreamSynchronize(st));
+            }
+            cluster_finish_kernel<<<grid, 256, 0, st>>>(n, cur);
+            EBC_CUDA(cub::DeviceRadixSort::SortPairs(tmp, sort2_bytes, cur, nxt, ids, d_to_ext, static_cast<int>(n), 0, 32,
+                                                     st)); // stable: a cluster keeps its external order
+        } else {
+            degree_kernel<<<grid, 256, 0, st>>>(d_offsets, n, deg, ids);
+            EBC_CUDA(cudaGetLastError());
+            EBC_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp, sort_bytes, deg, deg_sorted, ids, d_to_ext,
+                                                               static_cast<int>(n), 0, 7, st)); // stable
+        }
         invert_kernel<<<grid, 256, 0, st>>>(d_to_ext, d_offsets, n, d_to_dense, d_dense_offsets);
         EBC_CUDA(cudaGetLastError());
         EBC_CUDA(cub::DeviceScan::ExclusiveSum(tmp, scan_bytes, d_dense_offsets, d_dense_offsets,
@@ -1001,10 +1072,14 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
     // vertices; numbering by descending degree puts their labels / visited bits next to each other
     // (measured on R-MAT: +11 % at scale 20, +26 % at scale 24; +30..65 % when the input ids are
     // arbitrary).  Low-degree graphs keep their own numbering, which usually is spatially coherent.
-    bool want_dense = opt.renumber > 0 || (opt.renumber == 0 && m.hub_graph);
+    // Hub-free graphs too large for their labels to stay in L2 (grids, road networks) are numbered by
+    // neighbourhood clusters instead (cluster_*_kernel above): config 3, see DESIGN.md section 3.
+    int numbering = opt.renumber > 0 ? opt.renumber : opt.renumber < 0 ? 0 : m.hub_graph ? 1 : m.n >= (u64{1} << 18) ? 2 : 0;
     if (const char *env = std::getenv("EBC_RENUMBER"))
-        want_dense = std::atoi(env) != 0;
-    want_dense = want_dense && m.arcs && m.n < (u64{1} << 31); // (the CUB passes take 32-bit counts)
+        numbering = std::atoi(env);
+    if (numbering < 0 || numbering > 2)
+        throw ConfigError("renumber must be -1 (never), 0 (auto), 1 (degree classes) or 2 (neighbourhood clusters)");
+    const bool want_dense = numbering != 0 && m.arcs && m.n < (u64{1} << 31); // (the CUB passes take 32-bit counts)
     const int per_sm = occupancy_for(m.block, m.items);
     lap("occupancy query");
     if (per_sm < 1)
@@ -1036,8 +1111,10 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
     if (cap < g.n)
         m.big.allocate(kLargeSlots, g.n, g.n, m.s_agg);
     lap("slot arrays");
-    if (want_dense)
-        m.build_dense_graph();
+    if (want_dense) {
+        m.build_dense_graph(numbering == 2);
+        m.numbering = numbering;
+    }
     lap("dense numbering");
 
     // ---- frames, state, bookkeeping ----
@@ -1385,7 +1462,7 @@ void CudaSampler::info(std::uint64_t *out) {
     out[2] = m.small.cap;
     out[3] = m.small.bytes + m.big.bytes + m.graph_bytes + (m.n + 1) * (4 * 2 + 8 + 8 + 16);
     out[4] = static_cast<std::uint64_t>(m.sm_count);
-    out[5] = (m.launches & ((std::uint64_t{1} << 48) - 1)) | (static_cast<std::uint64_t>(m.d_to_ext ? 1 : 0) << 48) |
+    out[5] = (m.launches & ((std::uint64_t{1} << 48) - 1)) | (static_cast<std::uint64_t>(m.numbering) << 48) |
              (static_cast<std::uint64_t>(m.items) << 56);
 }
 

@@ -20,7 +20,7 @@ struct SamplerOptions {
     std::uint64_t slot_capacity = 0; // 0 = auto
     std::uint32_t items_per_thread = 0; // 0 = auto
     bool materialize_final_level = false; // settle the final level of every sample (see ebc_b200.h)
-    int renumber = 0; // hub-clustered vertex numbering on the device: 0 = auto (hub graphs), 1 = always, -1 = never
+    int renumber = 0; // device-side numbering: 0 = auto, -1 = never, 1 = degree classes, 2 = neighbourhood clusters
 };
 
 struct SampleRecordHost { // == ebc_sample_record

@@ -28,12 +28,12 @@ enum WorkCounter : int {
     kWorkCounters
 };
 
-// Labels.  One u32 per vertex per side replaces the reference's
-// (stamp, dist, sigma) triple (sampler.hpp:39-54): label = base + idx, where
-// idx is the vertex' position in the side's discovery-ordered settle list and
-// base advances by the number of settled vertices after every sample (O(1)
-// reset like SearchScratch::round_, sampler.cpp:63).  visited <=> label - base <
-// settled count; dist is implied by idx (levels occupy contiguous idx ranges).
+// Labels.  ONE u32 per vertex (both sides share it, see SideRegs in sampler_kernels.cuh) replaces the
+// reference's per-side (stamp, dist, sigma) triple (sampler.hpp:39-54): label = base + 2 * idx + side,
+// where idx is the vertex' position in the side's discovery-ordered settle list and base advances by
+// twice the larger settled count after every sample (O(1) reset like SearchScratch::round_,
+// sampler.cpp:63).  visited on side s <=> (label - base - s) even and (label - base - s) / 2 < settled
+// count of s; dist is implied by idx (levels occupy contiguous idx ranges).
 constexpr u32 kClaimTop = 0xffffffffu;     // transient claim values: kClaimTop - slot_in_tile
 constexpr u32 kMaxBlockThreads = 1024;
 constexpr u32 kMaxTileSlots = 4096;        // BLOCK * ITEMS never exceeds this
@@ -66,7 +66,7 @@ struct SamplerParams {
     const u64 *ext_offsets;
     const u32 *ext_targets;
     // slots
-    u32 *lab;      // [slots][2][n]
+    u32 *lab;      // [slots][n]
     u32 *list;     // [slots][2][cap]   settled vertices in discovery order
     u64 *sig;      // [slots][2][cap]   sigma, same indexing
     u32 *lvl;      // [slots][2][aux_cap+2] level start offsets into list

@@ -369,12 +369,18 @@ __device__ __noinline__ u32 block_first_exceeding(u128 w, u128 &running, bool &r
     return found;
 }
 
-// Labels of both sides of a vertex share one 8-byte word: lab[2v + side].  One
-// 32-byte sector therefore serves the visit test of the expanding side AND the
-// contact test against the other side.
+// One 4-byte label per vertex serves BOTH sides: lab[v] = base + 2 * idx + side, where idx is the
+// vertex' position in that side's settle list.  That is enough because, until the search ends, a vertex
+// is settled by at most one side: the first level that touches the other side's settled set is the last
+// one (sampler.cpp:105-115).  A contact vertex of that last level is settled on the expanding side like
+// any other (its label is overwritten), and its other-side idx -- read from the old label before the
+// overwrite -- travels in the contact record; the walks only look at levels below the contact level on
+// their own side, whose labels are never overwritten.  One load answers "visited on the expanding side?"
+// and "visited on the other side?" (contact test, sampler.cpp:107), and a 32-byte sector covers eight
+// vertices.  `base` is the same for both sides and advances by 2 * max(settled counts) per sample.
 struct SideRegs {
     const SidePtrs *pp;
-    u32 base;  // label base of this sample
+    u32 base;  // label base of this sample (same value on both sides)
     u32 cnt;   // settled vertices so far
     u32 fb;    // frontier = list[fb .. cnt)
     u32 depth; // depth of the frontier
@@ -387,7 +393,13 @@ struct WorkRegs {
     u64 e_lvl = 0, p_walk = 0;
 };
 
-__device__ __forceinline__ u32 half_of(u64 both, int side) { return static_cast<u32>(both >> (32 * side)); }
+// idx on side `s` encoded in `label`, or a value >= 2^31 (never below a settled count) if the label belongs to
+// the other side, to an earlier sample (label < base wraps) or is a transient claim value.
+__device__ __forceinline__ u32 label_idx(u32 label, u32 base, int s) {
+    const u32 r = label - base - static_cast<u32>(s);
+    return (r & 1u) ? 0xffffffffu : (r >> 1);
+}
+__device__ __forceinline__ u32 make_label(u32 base, u32 idx, int s) { return base + 2u * idx + static_cast<u32>(s); }
 
 // Loads the chunk of BLOCK frontier vertices at list positions [c0, c0 + BLOCK) (clipped to fe): row
 // start and sigma of each into c_beg / c_sig, the exclusive prefix of their degrees into
@@ -444,7 +456,6 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
     const u32 fb = ex.fb, fe = ex.cnt;
     const u32 level_start = fe;
     const u32 next_depth = ex.depth + 1;
-    const u64 *lab64 = reinterpret_cast<const u64 *>(lab);
     u32 cnt = fe;
     contact_n = 0;
     const bool sigma_small = sh.sigma_small[e] != 0; // uniform; written behind a barrier
@@ -500,18 +511,18 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
                     act[k] = j <= t_last;
                     v[k] = act[k] ? __ldg(row + j) : 0u;
                 }
-                u64 both[ITEMS];
+                u32 lbl[ITEMS];
 #pragma unroll
                 for (int k = 0; k < ITEMS; ++k)
-                    both[k] = act[k] ? ld_cg(lab64 + v[k]) : 0ull;
+                    lbl[k] = act[k] ? ld_cg(lab + v[k]) : 0u;
 #pragma unroll
                 for (int k = 0; k < ITEMS; ++k) {
-                    const u32 rel = half_of(both[k], e) - ex.base;
+                    const u32 rel = label_idx(lbl[k], ex.base, e);
                     const bool visited = rel < cnt;
                     win[k] = act[k] && !visited;
                     at_level[k] = act[k] && visited && rel >= level_start; // dist[v] == next_depth (sampler.cpp:97)
                     idx[k] = rel;
-                    other_idx[k] = half_of(both[k], 1 - e) - ot.base;
+                    other_idx[k] = label_idx(lbl[k], ex.base, 1 - e);
                     is_contact[k] = win[k] && other_idx[k] < ot.cnt; // other.visited(v) (sampler.cpp:107)
                 }
                 const u32 winners = block_ranks<BLOCK, ITEMS>(win, rank, sh.warp_cnt);
@@ -524,7 +535,7 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
                 for (int k = 0; k < ITEMS; ++k) {
                     if (win[k]) { // settle (sampler.cpp:93-95) and the discovering edge's sigma (sampler.cpp:98)
                         idx[k] = cnt + rank[k];
-                        st_cg(lab + 2 * static_cast<u64>(v[k]) + e, ex.base + idx[k]);
+                        st_cg(lab + v[k], make_label(ex.base, idx[k], e));
                         st_cg(ex.pp->list + idx[k], v[k]);
                         st_cg(ex.pp->sig + idx[k], sig_u);
                         if (BITS)
@@ -589,9 +600,9 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
                 for (int k = 0; k < ITEMS; ++k) {
                     const u64 j = t0 + static_cast<u64>(k) * BLOCK + tid;
                     if (j <= t_last) {
-                        const u64 both = ld_cg(lab64 + v[k]);
-                        const u32 rel = half_of(both, e) - ex.base;
-                        other_idx[k] = half_of(both, 1 - e) - ot.base;
+                        const u32 lbl = ld_cg(lab + v[k]);
+                        const u32 rel = label_idx(lbl, ex.base, e);
+                        other_idx[k] = label_idx(lbl, ex.base, 1 - e);
                         if (rel < cnt) {
                             idx[k] = rel;
                             at_level[k] = rel >= level_start;
@@ -600,11 +611,14 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
                         }
                     }
                 }
+                // Every label of the tile is read before any is claimed: a claim replaces the label, and the
+                // winner of a contact vertex needs the other side's idx that was in it.
+                __syncthreads();
                 // claim: the lowest slot of every distinct unvisited target wins (see the header comment)
 #pragma unroll
                 for (int k = 0; k < ITEMS; ++k)
                     if (candidate[k])
-                        red_max_u32(lab + 2 * static_cast<u64>(v[k]) + e, kClaimTop - (k * BLOCK + tid));
+                        red_max_u32(lab + v[k], kClaimTop - (k * BLOCK + tid));
                 __syncthreads(); // claims visible
                 // A candidate reads back the claim that won its target: its own (winner) or the winning slot's,
                 // through which it later finds the winner's idx in shared memory (no second look at the label).
@@ -613,7 +627,7 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
                 u32 won_by[ITEMS];
 #pragma unroll
                 for (int k = 0; k < ITEMS; ++k) {
-                    won_by[k] = candidate[k] ? kClaimTop - ld_cg(lab + 2 * static_cast<u64>(v[k]) + e) : 0u;
+                    won_by[k] = candidate[k] ? kClaimTop - ld_cg(lab + v[k]) : 0u;
                     win[k] = candidate[k] && won_by[k] == static_cast<u32>(k * BLOCK + tid);
                     is_contact[k] = win[k] && other_idx[k] < ot.cnt;
                 }
@@ -624,11 +638,11 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
                 for (int k = 0; k < ITEMS; ++k) {
                     if (win[k]) {
                         if (overflow) {
-                            st_cg(lab + 2 * static_cast<u64>(v[k]) + e, 0u); // undo the claim
+                            st_cg(lab + v[k], 0u); // undo the claim (the sample is abandoned and re-run)
                         } else {
                             idx[k] = cnt + rank[k];
                             tile_idx[k * BLOCK + tid] = idx[k];
-                            st_cg(lab + 2 * static_cast<u64>(v[k]) + e, ex.base + idx[k]);
+                            st_cg(lab + v[k], make_label(ex.base, idx[k], e));
                             st_cg(ex.pp->list + idx[k], v[k]);
                             st_cg(ex.pp->sig + idx[k], static_cast<u64>(0));
                             if (BITS)
@@ -734,7 +748,6 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
     constexpr int TILE = BLOCK * PI;
     const u32 tid = threadIdx.x;
     const u32 fb = ex.fb, fe = ex.cnt;
-    const u64 *lab64 = reinterpret_cast<const u64 *>(lab);
     if (tid == 0) {
         sh.edge_cnt = 0;
         sh.min_contact = 0xffffffffu;
@@ -811,7 +824,7 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
             // Visit test.  With bitmaps one 8-byte word holds the visited bits of 32 consecutive vertices
             // for both sides; rows are ascending, so a hub row streams through the bitmap instead of
             // touching one 128-byte label line per target.
-            u64 both[PI];
+            u64 both[PI]; // bitmap word of both sides, or (labels) the 4-byte label
             if (BITS) {
                 const u64 *bits64 = reinterpret_cast<const u64 *>(bits);
 #pragma unroll
@@ -820,7 +833,7 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
             } else {
 #pragma unroll
                 for (int k = 0; k < PI; ++k)
-                    both[k] = (act >> k) & 1u ? ld_cg(lab64 + v[k]) : 0ull;
+                    both[k] = (act >> k) & 1u ? ld_cg(lab + v[k]) : 0u;
             }
 #pragma unroll
             for (int k = 0; k < PI; ++k) {
@@ -828,21 +841,21 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
                     continue;
                 u32 oi;
                 if (BITS) {
-                    if ((half_of(both[k], e) >> (v[k] & 31)) & 1u)
+                    if ((static_cast<u32>(both[k] >> (32 * e)) >> (v[k] & 31)) & 1u)
                         continue; // visited before this level
                     new_slots += 1;
-                    if (!((half_of(both[k], 1 - e) >> (v[k] & 31)) & 1u))
+                    if (!((static_cast<u32>(both[k] >> (32 * (1 - e))) >> (v[k] & 31)) & 1u))
                         continue; // not a contact
                     // The other side's bit already says "contact"; its idx is only needed for the record and
                     // is fetched for all contact edges at once after the scan (one round trip per level
                     // instead of one inside every tile that has a contact).
                     oi = 0;
                 } else {
-                    const u32 rel = half_of(both[k], e) - ex.base;
-                    if (rel < ex.cnt)
+                    const u32 lbl = static_cast<u32>(both[k]);
+                    if (label_idx(lbl, ex.base, e) < ex.cnt)
                         continue; // visited before this level
                     new_slots += 1;
-                    oi = half_of(both[k], 1 - e) - ot.base;
+                    oi = label_idx(lbl, ex.base, 1 - e);
                 }
                 if (oi < ot.cnt) {
                     if (!BITS)
@@ -881,7 +894,7 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
         u32 lowest = 0xffffffffu;
         for (u32 i = tid; i < found; i += BLOCK) {
             u32 *w = edges + 6 * static_cast<u64>(i);
-            const u32 oi = ld_cg(lab + 2 * static_cast<u64>(ld_cg(w + 2)) + (1 - e)) - ot.base;
+            const u32 oi = label_idx(ld_cg(lab + ld_cg(w + 2)), ot.base, 1 - e);
             st_cg(w + 3, oi);
             lowest = oi < lowest ? oi : lowest;
         }
@@ -1206,7 +1219,6 @@ __device__ void walk_side(const SamplerParams &p, const u32 *lab, int x, const S
         } else {
             const u32 lo = ld_cg(sd.pp->lvl + (d - 1)), hi = ld_cg(sd.pp->lvl + d);
             const u32 span = hi - lo;
-            const u32 lab_lo = sd.base + lo;
             const u64 degu = end - beg;
             if (tid == 0)
                 sh.pred_cnt = 0;
@@ -1243,7 +1255,7 @@ __device__ void walk_side(const SamplerParams &p, const u32 *lab, int x, const S
             } else {
                 for (u64 k = beg + tid; k < end; k += BLOCK) {
                     const u32 w = __ldg(p.targets + k);
-                    const u32 rel = ld_cg(lab + 2 * static_cast<u64>(w) + x) - lab_lo;
+                    const u32 rel = label_idx(ld_cg(lab + w), sd.base, x) - lo;
                     if (rel < span) {
                         const u64 sg = ld_cg(sd.pp->sig + lo + rel);
                         total_local += sg;
@@ -1289,7 +1301,7 @@ __device__ void walk_side(const SamplerParams &p, const u32 *lab, int x, const S
                     u32 w = 0;
                     if (k < end) {
                         w = __ldg(p.targets + k);
-                        const u32 rel = ld_cg(lab + 2 * static_cast<u64>(w) + x) - lab_lo;
+                        const u32 rel = label_idx(ld_cg(lab + w), sd.base, x) - lo;
                         if (rel < span)
                             wv = ld_cg(sd.pp->sig + lo + rel);
                     }
@@ -1365,7 +1377,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
     for (int k = 0; k < 2; ++k) {
         if (tid == 0) {
             if (k == 0) {
-                sh.lab = p.lab + slot * 2 * n; // lab[2v + side]
+                sh.lab = p.lab + slot * n; // one label per vertex
                 sh.bits = BITS ? p.bits + slot * 2 * p.bit_words : nullptr;
                 sh.contact = p.contact + slot * 6 * p.aux_cap; // 2*aux_cap words: contacts / contact edges
                 sh.meetbuf = sh.contact + 2 * p.aux_cap;       // 4*aux_cap words: ordered meet set
@@ -1375,7 +1387,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             sh.sp[k].lvl = p.lvl + (slot * 2 + k) * (p.aux_cap + 2);
         }
         side[k].pp = &sh.sp[k];
-        side[k].base = ld_cg(p.hdr + slot * kHdrWords + kHdrBase0 + k); // written by another SM's CTA
+        side[k].base = ld_cg(p.hdr + slot * kHdrWords + kHdrBase0); // written by another SM's CTA
     }
     __syncthreads();
     auto edge_cap = [&]() -> u32 { // contact edges the probe may collect (recomputed: not worth a register)
@@ -1415,20 +1427,11 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
 
         // ---- label-space housekeeping: labels must stay below the claim range ----
         {
-            const u64 limit = static_cast<u64>(kClaimTop) - kMaxTileSlots - 2;
-            const bool r0 = static_cast<u64>(side[0].base) + p.cap + 1 >= limit;
-            const bool r1 = static_cast<u64>(side[1].base) + p.cap + 1 >= limit;
-            if (r0 || r1) {
-                for (u64 i = tid; i < n; i += BLOCK) {
-                    if (r0)
-                        st_cg(sh.lab + 2 * i, 0u);
-                    if (r1)
-                        st_cg(sh.lab + 2 * i + 1, 0u);
-                }
-                if (r0)
-                    side[0].base = 1;
-                if (r1)
-                    side[1].base = 1;
+            const u64 limit = static_cast<u64>(kClaimTop) - kMaxTileSlots - 4;
+            if (static_cast<u64>(side[0].base) + 2 * p.cap + 2 >= limit) { // the sample's labels reach base + 2 cap + 1
+                for (u64 i = tid; i < n; i += BLOCK)
+                    st_cg(sh.lab + i, 0u);
+                side[0].base = side[1].base = 1;
                 __syncthreads();
             }
         }
@@ -1461,7 +1464,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             side[k].depth = 0;
             side[k].pending = __ldg(p.offsets + root + 1) - __ldg(p.offsets + root);
             if (tid == 0) {
-                st_cg(sh.lab + 2 * static_cast<u64>(root) + k, side[k].base);
+                st_cg(sh.lab + root, make_label(side[k].base, 0, k));
                 if (BITS)
                     red_or_u32(sh.bits + 2 * static_cast<u64>(root >> 5) + k, 1u << (root & 31));
                 st_cg(side[k].pp->list, root);
@@ -1714,7 +1717,11 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
                 sh.last[2 + k] = side[k].cnt;
                 sh.last[4 + k] = side[k].depth;
             }
-            side[k].base += side[k].cnt;
+        }
+        {
+            const u32 used = side[0].cnt > side[1].cnt ? side[0].cnt : side[1].cnt;
+            side[0].base += 2 * used;
+            side[1].base = side[0].base;
         }
         __syncthreads();
         EBC_PH(6)

@@ -108,15 +108,15 @@ def test_capacity_overflow_reruns_in_large_slots():
 
 
 def test_label_space_wraparound(monkeypatch):
-    """Labels are base + idx with base growing monotonically; when the u32 space runs out the slot's
+    """Labels are base + 2 idx + side with base growing monotonically; when the u32 space runs out the slot's
     labels are zeroed and base restarts.  EBC_TEST_LABEL_BASE starts the slots just below the reset
-    threshold so both sides cross it within a few samples (at different samples)."""
+    threshold so the slots cross it within a few samples."""
     off, tg = small_graphs()["grid12"]
     g = ebc.Graph.from_csr(off, tg)
     o = Oracle(off, tg)
     n = g.num_vertices
-    # reset happens when base + cap + 1 >= 0xffffffff - 4096 - 2 (cap == n here)
-    monkeypatch.setenv("EBC_TEST_LABEL_BASE", str(0xFFFFFFFF - 4096 - 2 - n - 1 - 2000))
+    # reset happens when base + 2 cap + 2 >= 0xffffffff - 4096 - 4 (cap == n here)
+    monkeypatch.setenv("EBC_TEST_LABEL_BASE", str(0xFFFFFFFF - 4096 - 4 - 2 * n - 2 - 4000))
     for block, slots in ((32, 1), (128, 3)):
         s = ebc.Sampler(g, ebc.RunConfig(block_threads=block, slots=slots, materialize_final_level=True))
         s.sample(SEED, 0, 3000)

@@ -1,8 +1,10 @@
-"""Hub-clustered device numbering (ebc_run_config.renumber) must be invisible: samples, paths, frames,
-search state, work counters and the full pipeline are those of the caller's graph, bit for bit.
+"""Device-side numberings (ebc_run_config.renumber: 1 = degree classes, 2 = neighbourhood clusters) must be
+invisible: samples, paths, frames, search state, work counters and the full pipeline are those of the caller's
+graph, bit for bit.
 
-The numbering is automatic on hub graphs (max degree >= 1024), so the small graphs force it with
-renumber=1 and the hub graphs are also run with renumber=-1."""
+The numbering is automatic on hub graphs (max degree >= 1024: degree classes) and on large hub-free graphs
+(>= 2^18 vertices: clusters), so the small graphs force it with renumber=1 / 2 and the hub graphs are also run
+with renumber=-1."""
 import numpy as np
 import pytest
 
@@ -13,9 +15,10 @@ from test_gpu_parity import SEED, check_samples, small_graphs
 pytestmark = pytest.mark.gpu
 
 
+@pytest.mark.parametrize("mode", [1, 2])
 @pytest.mark.parametrize("name", list(small_graphs().keys()))
-def test_small_graph_samples_renumbered(name):
-    check_samples(small_graphs()[name], 600, ebc.RunConfig(block_threads=64, slots=8, renumber=1))
+def test_small_graph_samples_renumbered(name, mode):
+    check_samples(small_graphs()[name], 600, ebc.RunConfig(block_threads=64, slots=8, renumber=mode))
 
 
 def test_explicit_pairs_renumbered():
@@ -30,16 +33,18 @@ def test_search_state_renumbered():
         off, tg = small_graphs()[name]
         g = ebc.Graph.from_csr(off, tg)
         o = Oracle(off, tg)
-        s = ebc.Sampler(g, ebc.RunConfig(block_threads=64, slots=1, materialize_final_level=True, renumber=1))
-        for i in range(25):
-            rec, _ = s.sample_debug(SEED, i, 1)
-            want = o.sample(SEED, i)
-            assert int(rec[0]["dist"]) == want["dist"]
-            for side in (0, 1):
-                d, sg = s.last_state(side)
-                od, osg = o.last_state(side)
-                assert np.array_equal(d, od), (name, i, side)
-                assert np.array_equal(sg, osg), (name, i, side)
+        for mode in (1, 2):
+            s = ebc.Sampler(g, ebc.RunConfig(block_threads=64, slots=1, materialize_final_level=True, renumber=mode))
+            assert s.info()["renumbered"] == mode
+            for i in range(25):
+                rec, _ = s.sample_debug(SEED, i, 1)
+                want = o.sample(SEED, i)
+                assert int(rec[0]["dist"]) == want["dist"]
+                for side in (0, 1):
+                    d, sg = s.last_state(side)
+                    od, osg = o.last_state(side)
+                    assert np.array_equal(d, od), (name, i, side)
+                    assert np.array_equal(sg, osg), (name, i, side)
 
 
 @pytest.mark.parametrize("materialize", [False, True])
@@ -49,7 +54,7 @@ def test_hub_graph_both_numberings_agree(materialize):
     want = o.accumulate(SEED, 0, 3000)
     ow = dict(zip(ebc.WORK_NAMES[:11], (int(x) for x in o.work())))
     out = []
-    for mode in (1, -1):
+    for mode in (1, -1, 2):
         s = ebc.Sampler(g, ebc.RunConfig(renumber=mode, materialize_final_level=materialize))
         rec, paths = s.sample_debug(SEED, 0, 3000, path_stride=12)
         assert np.array_equal(s.read_frame(0), want)
@@ -58,9 +63,10 @@ def test_hub_graph_both_numberings_agree(materialize):
                   ("E_bfs", "E_lvl", "V_exp", "M", "S_walk", "E_walk", "P_walk", "L", "levels")):
             assert w[k] == ow[k], (mode, k)
         out.append((rec, paths))
-    for k in ("s", "t", "dist", "meet", "meet_count", "draws", "path_len", "weight_lo", "weight_hi", "flags"):
-        assert np.array_equal(out[0][0][k], out[1][0][k]), k
-    assert np.array_equal(out[0][1], out[1][1])
+    for other in out[1:]:
+        for k in ("s", "t", "dist", "meet", "meet_count", "draws", "path_len", "weight_lo", "weight_hi", "flags"):
+            assert np.array_equal(out[0][0][k], other[0][k]), k
+        assert np.array_equal(out[0][1], other[1])
     for i in range(0, 3000, 41):
         w = o.sample(SEED, i)
         assert (int(out[0][0][i]["dist"]), int(out[0][0][i]["meet"])) == (w["dist"], w["meet"])
@@ -94,3 +100,21 @@ def test_pipeline_identical_with_and_without_numbering():
     assert a.tau_total == b.tau_total
     for k in ("tau", "epochs", "omega", "diameter_upper_bound", "vertex_diameter_bound"):
         assert sa[k] == sb[k], k
+
+
+def test_large_hub_free_graph_is_clustered_automatically():
+    """A grid above 2^18 vertices gets the neighbourhood-cluster numbering by default; frames equal the oracle's
+    and those of the unnumbered run."""
+    g = ebc.gen_grid(600, 600, 0.05, 0.001, 3).largest_connected_component()
+    o = Oracle(g.offsets, g.targets)
+    want = o.accumulate(SEED, 0, 1500)
+    for mode, expect in ((0, 2), (-1, 0)):
+        s = ebc.Sampler(g, ebc.RunConfig(renumber=mode))
+        assert s.info()["renumbered"] == expect
+        rec, paths = s.sample_debug(SEED, 0, 1500, path_stride=200)
+        assert np.array_equal(s.read_frame(0), want)
+        for i in range(0, 1500, 97):
+            w = o.sample(SEED, i)
+            assert (int(rec[i]["dist"]), int(rec[i]["meet"]), int(rec[i]["draws"])) == (w["dist"], w["meet"], w["draws"])
+            assert np.array_equal(paths[i, :len(w["path"])], w["path"][:200])
+        s.close()
