@@ -139,9 +139,12 @@ def load():
     """Loads (building first if the sources are newer) libebc_b200.so.  Raises if unavailable."""
     global _lib
     if _lib is None:
-        if not os.path.exists(_build.LIB) or (_build.is_stale() and _have_nvcc()):
-            _build.build()
-        L = C.CDLL(_build.LIB)
+        path = os.environ.get("EBC_LIB")  # experiment hook: an alternative build of the same library (A/B runs)
+        if not path:
+            if not os.path.exists(_build.LIB) or (_build.is_stale() and _have_nvcc()):
+                _build.build()
+            path = _build.LIB
+        L = C.CDLL(path)
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(L, name)  # AttributeError if a declared symbol is not exported
             fn.restype = res

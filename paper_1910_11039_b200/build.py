@@ -59,8 +59,10 @@ def is_stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not is_stale():
+def build(force: bool = False, verbose: bool = False, out: str = LIB) -> str:
+    """`out` other than LIB (with EBC_NVCC_FLAGS) builds an experimental variant next to the product library;
+    load it with EBC_LIB=<path>."""
+    if not force and out == LIB and not is_stale():
         return LIB
     extra = os.environ.get("EBC_NVCC_FLAGS", "").split()
     nvcc = nvcc_path()
@@ -79,11 +81,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with cf.ThreadPoolExecutor(max(1, min(os.cpu_count() or 1, len(units)))) as ex:
         list(ex.map(compile_one, units))
-    subprocess.run([nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB] + [u[0] for u in units] +
+    subprocess.run([nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", out] + [u[0] for u in units] +
                    ["-lpthread", "-ldl"], check=True)
-    return LIB
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    outs = [a for a in sys.argv[1:] if a.endswith(".so")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, out=os.path.abspath(outs[0]) if outs else LIB))

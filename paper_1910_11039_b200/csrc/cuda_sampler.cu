@@ -832,7 +832,7 @@ struct CudaSampler::Impl {
         d_to_ext = dev_alloc<u32>(n);
         d_to_dense = dev_alloc<u32>(n);
         d_dense_offsets = dev_alloc<u64>(n + 1);
-        d_dense_targets = dev_alloc<u32>(arcs);
+        d_dense_targets = dev_alloc<u32>(arcs + 4); // (+4: the probe reads whole 16-byte groups)
         const u32 grid = static_cast<u32>(std::min<u64>((n + 255) / 256, static_cast<u64>(sm_count) * 8));
         size_t sort_bytes = 0, sort2_bytes = 0, scan_bytes = 0;
         EBC_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, sort_bytes, deg, deg_sorted, ids, d_to_ext,
@@ -1017,7 +1017,7 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
 
     // ---- graph: replicated CSR, u64 offsets + u32 targets ----
     m.d_offsets = dev_alloc<u64>(g.n + 1);
-    m.d_targets = dev_alloc<u32>(m.arcs);
+    m.d_targets = dev_alloc<u32>(m.arcs + 4); // (+4: the probe reads whole 16-byte groups)
     // (a staged copy through pinned buffers was measured slower than the driver's pageable path here)
     EBC_CUDA(cudaMemcpyAsync(m.d_offsets, g.offsets.data(), (g.n + 1) * 8, cudaMemcpyHostToDevice, m.s_sample));
     if (m.arcs)

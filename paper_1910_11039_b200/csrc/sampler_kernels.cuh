@@ -151,12 +151,6 @@ constexpr int kPredCache = 32;
 // the other side, the meet set is resolved from the contact edges and the level is never settled: up to
 // FinalEdgeCap<BLOCK>::value edges in shared memory (meet_from_edges), more -- as many as the slot's
 // contact buffer holds -- in the slot's global arrays (meet_from_edges_large).
-// Slots per thread of the probe pass relative to the expansion.  Measured on R-MAT-20: 128x4 threads x
-// slots: factor 1 4.94 M samples/s, 2 4.41 M, 4 3.35 M; 128x2: 4.82 / 5.00 / 4.60 M -- beyond four
-// probes in flight per thread the memory system, not latency, is the limit.
-#ifndef EBC_PROBE_FACTOR
-#define EBC_PROBE_FACTOR 1
-#endif
 #ifndef EBC_EDGE_CAP_MAX
 #define EBC_EDGE_CAP_MAX 512
 #endif
@@ -401,6 +395,25 @@ __device__ __forceinline__ u32 label_idx(u32 label, u32 base, int s) {
 }
 __device__ __forceinline__ u32 make_label(u32 base, u32 idx, int s) { return base + 2u * idx + static_cast<u32>(s); }
 
+// Visited filter (hub graphs, BITS kernels): an approximate copy of the visited set of BOTH sides together in
+// shared memory, one bit per position h = v mod kPositions.  A clear bit means "certainly not visited by either
+// side": the probe of a final level, whose targets are overwhelmingly unvisited, then needs no global access
+// for that slot at all.  A set bit (a visited vertex, or another one that shares its position) is looked up
+// in the global bitmap.  Under the degree-class numbering small ids are the hubs, so the hubs -- the vertices
+// most often visited -- have positions of their own.  Set when a vertex is settled, cleared once per sample.
+template <int BLOCK> struct VisitedFilter {
+    // 64 bytes of filter per thread, at most 16 KB; 1 KB for one-warp CTAs (32 of them share an SM's shared memory)
+    static constexpr u32 kPositions = BLOCK <= 32 ? 8192u : 512u * (BLOCK < 256 ? BLOCK : 256);
+    static constexpr u32 kWords = kPositions / 32;
+};
+template <int BLOCK> __device__ __forceinline__ void filter_insert(u32 *vf, u32 v) {
+    const u32 h = v & (VisitedFilter<BLOCK>::kPositions - 1);
+    atomicOr(vf + (h >> 5), 1u << (h & 31));
+}
+
+// 16-byte load of four consecutive adjacency entries (SASS: LDG.E.128 through the read-only path).
+__device__ __forceinline__ uint4 ldg_targets4(const u32 *p) { return __ldg(reinterpret_cast<const uint4 *>(p)); }
+
 // Loads the chunk of BLOCK frontier vertices at list positions [c0, c0 + BLOCK) (clipped to fe): row
 // start and sigma of each into c_beg / c_sig, the exclusive prefix of their degrees into
 // c_scan[0..BLOCK]; returns the chunk's number of adjacency slots.  Starts with a barrier (the previous
@@ -449,7 +462,7 @@ __device__ __noinline__ u64 load_chunk(const SamplerParams &p, const SidePtrs *p
 // slot-capacity overflow (the sample is then re-run in a large slot).
 // contact_n returns the number of contact vertices appended to `contact`.
 template <int BLOCK, int ITEMS, bool BITS>
-__device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e, SideRegs &ex, const SideRegs &ot,
+__device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, u32 *vf, int e, SideRegs &ex, const SideRegs &ot,
                              u32 *contact, u32 &contact_n, BlockShared<BLOCK, ITEMS> &sh, WorkRegs &wk) {
     constexpr int TILE = BLOCK * ITEMS;
     const u32 tid = threadIdx.x;
@@ -538,8 +551,10 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
                         st_cg(lab + v[k], make_label(ex.base, idx[k], e));
                         st_cg(ex.pp->list + idx[k], v[k]);
                         st_cg(ex.pp->sig + idx[k], sig_u);
-                        if (BITS)
+                        if (BITS) {
                             red_or_u32(bits + 2 * static_cast<u64>(v[k] >> 5) + e, 1u << (v[k] & 31));
+                            filter_insert<BLOCK>(vf, v[k]);
+                        }
                         if (is_contact[k]) {
                             atomicMin(&sh.min_contact, other_idx[k]);
                             any_contact_local = true;
@@ -645,8 +660,10 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, int e,
                             st_cg(lab + v[k], make_label(ex.base, idx[k], e));
                             st_cg(ex.pp->list + idx[k], v[k]);
                             st_cg(ex.pp->sig + idx[k], static_cast<u64>(0));
-                            if (BITS)
+                            if (BITS) {
                                 red_or_u32(bits + 2 * static_cast<u64>(v[k] >> 5) + e, 1u << (v[k] & 31));
+                                filter_insert<BLOCK>(vf, v[k]);
+                            }
                             if (is_contact[k]) {
                                 atomicMin(&sh.min_contact, other_idx[k]);
                                 any_contact_local = true;
@@ -721,8 +738,8 @@ __device__ __forceinline__ u64 sum_frontier_degrees(const SamplerParams &p, cons
 }
 
 // Read-only scan of the level that is about to be expanded on side `e`: every
-// adjacency slot is visited (its target's label is probed exactly as in
-// expand_level) but nothing is written.  Each slot whose target is unvisited on
+// adjacency slot is visited (its target is tested exactly as in expand_level)
+// but nothing is written.  Each slot whose target is unvisited on
 // this side and visited on the other side is a CONTACT EDGE; it is appended
 // (unordered) to `edges` as 6 words {frontier position, index in row, target,
 // other-side idx, sigma[u] lo, hi}.  If the level has at least one contact edge
@@ -735,158 +752,179 @@ __device__ __forceinline__ u64 sum_frontier_degrees(const SamplerParams &p, cons
 // (possibly > edge_cap, in which case the caller falls back to expand_level).
 // new_slots counts (per thread) the slots whose target is unvisited on this
 // side (= the level's E_lvl, sampler.cpp:97).
-template <int BLOCK, int ITEMS, bool BITS>
-__device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bits, int e, const SideRegs &ex, const SideRegs &ot,
-                           u32 *edges, u32 edge_cap, BlockShared<BLOCK, ITEMS> &sh, u64 &new_slots,
-                           u64 &total_slots) {
-    // The pass only reads, so it can afford more slots per thread than the expansion: fewer, longer
-    // tiles mean fewer dependent round trips per level.
-#ifndef EBC_PROBE_MIN_PI
-#define EBC_PROBE_MIN_PI 1
+//
+// The scan is unordered (a contact edge carries its own discovery key), so the rows are streamed: a row is
+// cut into items of G lanes x 4 consecutive entries, aligned to 16 bytes; a group of G lanes takes item after
+// item (one 128-bit load per lane, the next item's entries requested before the current one's are tested) and
+// finds an item's row with one search per group instead of one per slot.  G = 32 on hub graphs (rows of 10^3..10^5
+// entries), 4 otherwise.  Entries a 16-byte group shares with the neighbouring rows are masked out.
+#ifndef EBC_PROBE_G
+#define EBC_PROBE_G 8
 #endif
-    constexpr int PI = ITEMS * EBC_PROBE_FACTOR < EBC_PROBE_MIN_PI ? EBC_PROBE_MIN_PI : ITEMS * EBC_PROBE_FACTOR;
-    constexpr int TILE = BLOCK * PI;
+// Appends one contact edge (see probe_level); out of line, it runs a few dozen times per sample.
+static __device__ __noinline__ void record_contact_edge(u32 *edges, u32 pos, u32 frontier_pos, u32 index_in_row, u32 v, u32 oi,
+                                                        u64 sg) {
+    u32 *w = edges + 6 * static_cast<u64>(pos);
+    st_cg(w + 0, frontier_pos);
+    st_cg(w + 1, index_in_row);
+    st_cg(w + 2, v);
+    st_cg(w + 3, oi);
+    st_cg(w + 4, static_cast<u32>(sg));
+    st_cg(w + 5, static_cast<u32>(sg >> 32));
+}
+
+template <int BLOCK, int ITEMS, bool BITS>
+__device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bits, const u32 *vf, int e, const SideRegs &ex,
+                           const SideRegs &ot, u32 *edges, u32 edge_cap, BlockShared<BLOCK, ITEMS> &sh, u64 &new_slots,
+                           u64 &total_slots) {
+    constexpr u32 G = BITS ? EBC_PROBE_G : 4; // lanes per item
+    constexpr u32 NG = BLOCK / G;             // groups per CTA
+    constexpr u32 kItemLen = 4 * G;           // adjacency entries per item
     const u32 tid = threadIdx.x;
+    const u32 gid = tid / G, q = tid % G;
     const u32 fb = ex.fb, fe = ex.cnt;
     if (tid == 0) {
         sh.edge_cnt = 0;
         sh.min_contact = 0xffffffffu;
     }
     u64 t_total = 0;
+    u32 fresh = 0; // slots whose target is unvisited on this side (< 2^32 per thread and level)
     for (u32 c0 = fb; c0 < fe; c0 += BLOCK) {
-        const u64 T = load_chunk<BLOCK>(p, ex.pp, c0, fe, sh.c_beg, sh.c_scan, sh.c_sig, sh.red64);
-        t_total += T;
-        // Software pipeline: the targets of tile i+1 are requested before the visit words of tile i,
-        // so the two dependent loads of a slot (target id -> visit word) overlap across tiles.
-        // A tile that lies inside one row -- the usual case behind a hub -- addresses its slots as
-        // row[j]; otherwise every slot finds its owner row by galloping upwards from the tile's first
-        // row (slots ascend with k).  Only a contact edge needs (owner, index in row) again, and looks
-        // them up on its own: the pipeline carries nothing but the target ids.
-        u32 v_n[PI];
-        u32 act_n = 0; // bit k: slot k of the requested tile exists
-        int row = 0;   // owner row of the requested tile's first slot (uniform, non-decreasing)
-        auto fetch = [&](u64 t0) {
-            while (sh.c_scan[row + 1] <= t0) // c_scan[BLOCK] = T > t0
-                ++row;
-            const u64 t_end = t0 + TILE < T ? t0 + TILE : T;
-            act_n = 0;
-            if (sh.c_scan[row + 1] >= t_end) {
-                const u32 *rowp = p.targets + (sh.c_beg[row] - sh.c_scan[row]);
+        t_total += load_chunk<BLOCK>(p, ex.pp, c0, fe, sh.c_beg, sh.c_scan, sh.c_sig, sh.red64);
+        // items per row (thread tid owns row tid of the chunk), exclusive prefix -> l_scan[0..BLOCK]
+        // (in f_key, which is only live in the meet phase and in expand_level's multi-row tiles)
+        static_assert(2 * FinalEdgeCap<BLOCK>::value >= BLOCK + 1, "l_scan aliases f_key");
+        u32 *l_scan = reinterpret_cast<u32 *>(sh.f_key);
+        {
+            const u64 deg = sh.c_scan[tid + 1] - sh.c_scan[tid];
+            const u32 items = deg ? static_cast<u32>(((sh.c_beg[tid] & 3) + deg + kItemLen - 1) / kItemLen) : 0u;
+            u32 inc = items;
 #pragma unroll
-                for (int k = 0; k < PI; ++k) {
-                    const u64 j = t0 + static_cast<u64>(k) * BLOCK + tid;
-                    v_n[k] = 0;
-                    if (j < t_end) {
-                        act_n |= 1u << k;
-                        v_n[k] = __ldg(rowp + j);
-                    }
-                }
-            } else {
-                int lo = row;
-#pragma unroll
-                for (int k = 0; k < PI; ++k) {
-                    const u64 j = t0 + static_cast<u64>(k) * BLOCK + tid;
-                    v_n[k] = 0;
-                    if (j < t_end) {
-                        int hi = lo + 1, step = 1; // owner row: last r with c_scan[r] <= j
-                        while (sh.c_scan[hi] <= j) {
-                            lo = hi;
-                            hi = hi + step < BLOCK ? hi + step : BLOCK;
-                            step <<= 1;
-                        }
-                        while (hi - lo > 1) {
-                            const int mid = (lo + hi) >> 1;
-                            if (sh.c_scan[mid] <= j)
-                                lo = mid;
-                            else
-                                hi = mid;
-                        }
-                        act_n |= 1u << k;
-                        v_n[k] = __ldg(p.targets + sh.c_beg[lo] + (j - sh.c_scan[lo]));
-                    }
-                }
+            for (int o = 1; o < 32; o <<= 1) {
+                const u32 t = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane_id() >= static_cast<u32>(o))
+                    inc += t;
             }
-        };
-#pragma unroll
-        for (int k = 0; k < PI; ++k)
-            v_n[k] = 0;
-        // Iteration t0 requests tile t0 and tests the tile requested by the previous iteration (nothing in
+            if (BLOCK > 32) {
+                if (lane_id() == 31)
+                    sh.warp_cnt[tid >> 5] = inc;
+                __syncthreads();
+                u32 before = 0;
+                for (u32 w = 0; w < (tid >> 5); ++w)
+                    before += sh.warp_cnt[w];
+                inc += before;
+            }
+            l_scan[tid + 1] = inc;
+            if (tid == 0)
+                l_scan[0] = 0;
+            __syncthreads();
+        }
+        const u32 n_items = l_scan[BLOCK];
+        // Iteration i requests the entries of item i and tests those requested by iteration i - 1 (nothing in
         // the first one); written as one loop so that the request code exists once.
-        for (u64 t0 = 0;; t0 += TILE) {
-            u32 v[PI];
-            const u32 act = act_n;
-#pragma unroll
-            for (int k = 0; k < PI; ++k)
-                v[k] = v_n[k];
-            const bool more = t0 < T;
-            if (more)
-                fetch(t0);
-            // Visit test.  With bitmaps one 8-byte word holds the visited bits of 32 consecutive vertices
-            // for both sides; rows are ascending, so a hub row streams through the bitmap instead of
-            // touching one 128-byte label line per target.
-            u64 both[PI]; // bitmap word of both sides, or (labels) the 4-byte label
-            if (BITS) {
-                const u64 *bits64 = reinterpret_cast<const u64 *>(bits);
-#pragma unroll
-                for (int k = 0; k < PI; ++k)
-                    both[k] = (act >> k) & 1u ? ld_cg(bits64 + (v[k] >> 5)) : 0ull;
-            } else {
-#pragma unroll
-                for (int k = 0; k < PI; ++k)
-                    both[k] = (act >> k) & 1u ? ld_cg(lab + v[k]) : 0u;
-            }
-#pragma unroll
-            for (int k = 0; k < PI; ++k) {
-                if (!((act >> k) & 1u))
-                    continue;
-                u32 oi;
-                if (BITS) {
-                    if ((static_cast<u32>(both[k] >> (32 * e)) >> (v[k] & 31)) & 1u)
-                        continue; // visited before this level
-                    new_slots += 1;
-                    if (!((static_cast<u32>(both[k] >> (32 * (1 - e))) >> (v[k] & 31)) & 1u))
-                        continue; // not a contact
-                    // The other side's bit already says "contact"; its idx is only needed for the record and
-                    // is fetched for all contact edges at once after the scan (one round trip per level
-                    // instead of one inside every tile that has a contact).
-                    oi = 0;
-                } else {
-                    const u32 lbl = static_cast<u32>(both[k]);
-                    if (label_idx(lbl, ex.base, e) < ex.cnt)
-                        continue; // visited before this level
-                    new_slots += 1;
-                    oi = label_idx(lbl, ex.base, 1 - e);
+        int row = 0;              // row of the item requested last (items ascend per group)
+        u32 row_c = 0, deg_c = 0; // ... of the item under test: row, its degree,
+        int rel0_c = 0;           //     index in the row of the item's first entry (negative: 16-byte alignment)
+        bool have_c = false;
+        uint4 cur = make_uint4(0, 0, 0, 0);
+        for (u32 item = gid;; item += NG) {
+            const bool have_n = item < n_items;
+            uint4 nxt = make_uint4(0, 0, 0, 0);
+            u32 deg_n = 0;
+            int rel0_n = 0;
+            if (have_n) {
+                // row = last r with l_scan[r] <= item: gallop upwards from the previous item's row, then bisect
+                int lo = row, hi = lo + 1, step = 1;
+                while (hi < BLOCK && l_scan[hi] <= item) {
+                    lo = hi;
+                    hi = hi + step < BLOCK ? hi + step : BLOCK;
+                    step <<= 1;
                 }
-                if (oi < ot.cnt) {
-                    if (!BITS)
-                        atomicMin(&sh.min_contact, oi);
-                    const u32 pos = atomicAdd(&sh.edge_cnt, 1u);
-                    if (pos < edge_cap) {
-                        // (owner row, index in row) of this slot of the tile requested one iteration ago
-                        const u64 j = (t0 - TILE) + static_cast<u64>(k) * BLOCK + tid;
-                        int lo = 0, hi = BLOCK;
-                        while (hi - lo > 1) {
-                            const int mid = (lo + hi) >> 1;
-                            if (sh.c_scan[mid] <= j)
-                                lo = mid;
-                            else
-                                hi = mid;
+                while (hi - lo > 1) {
+                    const int mid = (lo + hi) >> 1;
+                    if (l_scan[mid] <= item)
+                        lo = mid;
+                    else
+                        hi = mid;
+                }
+                row = lo;
+                const u64 beg = sh.c_beg[lo];
+                const u64 first = (beg & ~u64{3}) + static_cast<u64>(item - l_scan[lo]) * kItemLen + 4 * q; // 16-byte aligned
+                rel0_n = static_cast<int>(static_cast<long long>(first) - static_cast<long long>(beg));
+                deg_n = static_cast<u32>(sh.c_scan[lo + 1] - sh.c_scan[lo]);
+                nxt = ldg_targets4(p.targets + first);
+            }
+            if (have_c) {
+                const u32 vv[4] = {cur.x, cur.y, cur.z, cur.w};
+                // entries [lo_k, hi_k) of the four belong to the row
+                const int lo_k = rel0_c < 0 ? -rel0_c : 0;
+                const int left = static_cast<int>(deg_c) - rel0_c;
+                const int hi_k = left < 4 ? left : 4;
+                u32 need = 0; // bit k: entry k must be looked up in global memory
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (k < lo_k || k >= hi_k)
+                        continue;
+                    if (BITS) {
+                        const u32 h = vv[k] & (VisitedFilter<BLOCK>::kPositions - 1);
+                        if (((vf[h >> 5] >> (h & 31)) & 1u) == 0) { // certainly unvisited on both sides
+                            fresh += 1;
+                            continue;
                         }
-                        u32 *w = edges + 6 * static_cast<u64>(pos);
-                        const u64 sg = sh.c_sig[lo];
-                        st_cg(w + 0, (c0 - fb) + static_cast<u32>(lo));
-                        st_cg(w + 1, static_cast<u32>(j - sh.c_scan[lo]));
-                        st_cg(w + 2, v[k]);
-                        st_cg(w + 3, oi);
-                        st_cg(w + 4, static_cast<u32>(sg));
-                        st_cg(w + 5, static_cast<u32>(sg >> 32));
+                    }
+                    need |= 1u << k;
+                }
+                if (need) {
+                    u64 both[4]; // bitmap word of both sides, or (labels) the 4-byte label
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        both[k] = 0;
+                        if ((need >> k) & 1u)
+                            both[k] = BITS ? ld_cg(reinterpret_cast<const u64 *>(bits) + (vv[k] >> 5))
+                                           : static_cast<u64>(ld_cg(lab + vv[k]));
+                    }
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        if (!((need >> k) & 1u))
+                            continue;
+                        u32 oi;
+                        if (BITS) {
+                            if ((static_cast<u32>(both[k] >> (32 * e)) >> (vv[k] & 31)) & 1u)
+                                continue; // visited before this level
+                            fresh += 1;
+                            if (!((static_cast<u32>(both[k] >> (32 * (1 - e))) >> (vv[k] & 31)) & 1u))
+                                continue; // not a contact
+                            // The other side's bit already says "contact"; its idx is only needed for the record
+                            // and is fetched for all contact edges at once after the scan.
+                            oi = 0;
+                        } else {
+                            const u32 lbl = static_cast<u32>(both[k]);
+                            if (label_idx(lbl, ex.base, e) < ex.cnt)
+                                continue; // visited before this level
+                            fresh += 1;
+                            oi = label_idx(lbl, ex.base, 1 - e);
+                        }
+                        if (oi < ot.cnt) {
+                            if (!BITS)
+                                atomicMin(&sh.min_contact, oi);
+                            const u32 pos = atomicAdd(&sh.edge_cnt, 1u);
+                            if (pos < edge_cap)
+                                record_contact_edge(edges, pos, (c0 - fb) + row_c, static_cast<u32>(rel0_c + k), vv[k], oi,
+                                                    sh.c_sig[row_c]);
+                        }
                     }
                 }
             }
-            if (!more)
+            if (!have_n)
                 break;
+            cur = nxt;
+            row_c = static_cast<u32>(row);
+            deg_c = deg_n;
+            rel0_c = rel0_n;
+            have_c = true;
         }
     }
+    new_slots += fresh;
     __syncthreads();
     total_slots = t_total;
     const u32 found = sh.edge_cnt;
@@ -1348,7 +1386,11 @@ template <int BLOCK> constexpr int min_blocks_per_sm() {
 template <int BLOCK, int ITEMS, bool BITS>
 __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kernel(const SamplerParams p) {
     __shared__ BlockShared<BLOCK, ITEMS> sh;
+    __shared__ u32 vf[BITS ? VisitedFilter<BLOCK>::kWords : 1]; // visited filter of the sample in flight
     const u32 tid = threadIdx.x;
+    if (BITS)
+        for (u32 i = tid; i < VisitedFilter<BLOCK>::kWords; i += BLOCK)
+            vf[i] = 0;
     // Slot hand-out.  Launches of consecutive epochs overlap on two streams, so a CTA cannot own
     // slot blockIdx.x: it takes a free slot id from a ring (at most ring_size CTAs are resident, each
     // holds one slot, so a free one is always there or about to be returned) and puts it back at exit.
@@ -1465,8 +1507,10 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             side[k].pending = __ldg(p.offsets + root + 1) - __ldg(p.offsets + root);
             if (tid == 0) {
                 st_cg(sh.lab + root, make_label(side[k].base, 0, k));
-                if (BITS)
+                if (BITS) {
                     red_or_u32(sh.bits + 2 * static_cast<u64>(root >> 5) + k, 1u << (root & 31));
+                    filter_insert<BLOCK>(vf, root);
+                }
                 st_cg(side[k].pp->list, root);
                 st_cg(side[k].pp->sig, static_cast<u64>(1));
                 st_cg(side[k].pp->lvl, 0u);
@@ -1514,8 +1558,8 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
                 4 * side[e].pending >= p.probe_growth_x4 * sh.prev_pending[e] &&
                 static_cast<u64>(side[e].depth) + 2 <= p.aux_cap) {
                 u64 new_slots = 0, total_slots = 0;
-                edge_n = probe_level<BLOCK, ITEMS, BITS>(p, sh.lab, sh.bits, e, side[e], side[1 - e], sh.contact, edge_cap(), sh, new_slots,
-                                                   total_slots);
+                edge_n = probe_level<BLOCK, ITEMS, BITS>(p, sh.lab, sh.bits, vf, e, side[e], side[1 - e], sh.contact, edge_cap(), sh,
+                                                         new_slots, total_slots);
                 EBC_PH(2)
                 bool resolvable = edge_n > 0 && edge_n <= edge_cap();
                 if (resolvable && edge_n > static_cast<u32>(FinalEdgeCap<BLOCK>::value)) {
@@ -1545,7 +1589,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
                     sh.rec.flags |= 4u; // the probe found more contact edges than it can resolve
                 __syncthreads(); // no sh.contact (or too many sh.contact edges): expand normally
             }
-            if (!expand_level<BLOCK, ITEMS, BITS>(p, sh.lab, sh.bits, e, side[e], side[1 - e], sh.contact, contact_n, sh, wk)) {
+            if (!expand_level<BLOCK, ITEMS, BITS>(p, sh.lab, sh.bits, vf, e, side[e], side[1 - e], sh.contact, contact_n, sh, wk)) {
                 aborted = true;
                 break;
             }
@@ -1691,7 +1735,9 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
         }
         if (p.records && tid == 0)
             p.records[local] = sh.rec;
-        if (BITS) { // clear the bitmap words of every settled vertex (both sides share the 8-byte word)
+        if (BITS) { // clear the bitmap words of every settled vertex (both sides share the 8-byte word), and the filter
+            for (u32 i = tid; i < VisitedFilter<BLOCK>::kWords; i += BLOCK)
+                vf[i] = 0;
             u64 *bits64 = reinterpret_cast<u64 *>(sh.bits);
 #pragma unroll 1
             for (int k = 0; k < 2; ++k) {

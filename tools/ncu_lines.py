@@ -6,10 +6,17 @@ rep, so, kern = sys.argv[1:4]
 top = int(sys.argv[4]) if len(sys.argv) > 4 and sys.argv[4].isdigit() else 40
 tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(so)], cwd=tmp, capture_output=True)
-cub = [f for f in os.listdir(tmp) if f.endswith(".cubin") and "cuda_sampler" in f and "-" not in f][0]
-dis = subprocess.run(["nvdisasm", "-g", os.path.join(tmp, cub)], capture_output=True, text=True).stdout.splitlines()
-# locate the kernel's text section
-start = next(i for i, l in enumerate(dis) if l.strip().startswith(".section") and (".text." + kern) in l)
+# locate the cubin and text section that hold the kernel (one cubin per translation unit)
+dis, start = None, None
+for cub in sorted(f for f in os.listdir(tmp) if f.endswith(".cubin")):
+    if kern.encode() not in open(os.path.join(tmp, cub), "rb").read():
+        continue
+    d = subprocess.run(["nvdisasm", "-g", os.path.join(tmp, cub)], capture_output=True, text=True).stdout.splitlines()
+    st = next((i for i, l in enumerate(d) if l.strip().startswith(".section") and (".text." + kern) in l), None)
+    if st is not None:
+        dis, start = d, st
+        break
+assert dis is not None, "kernel not found in any cubin of " + so
 line_of = {}
 cur = None
 for l in dis[start + 1:]:

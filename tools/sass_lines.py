@@ -6,9 +6,15 @@ so, kern = sys.argv[1:3]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 30
 tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(so)], cwd=tmp, capture_output=True)
-cub = [f for f in os.listdir(tmp) if f.endswith(".cubin") and "cuda_sampler" in f and "-" not in f][0]
-dis = subprocess.run(["nvdisasm", "-g", os.path.join(tmp, cub)], capture_output=True, text=True).stdout.splitlines()
-start = next(i for i, l in enumerate(dis) if l.strip().startswith(".section") and (".text." + kern) in l)
+dis, start = None, None  # (pass the object file of the kernel's translation unit: build/obj/sample_launch_b<BLOCK>.*.o)
+for cub in sorted(f for f in os.listdir(tmp) if f.endswith(".cubin")):
+    if kern.encode() not in open(os.path.join(tmp, cub), "rb").read():
+        continue
+    d = subprocess.run(["nvdisasm", "-g", os.path.join(tmp, cub)], capture_output=True, text=True).stdout.splitlines()
+    st = next((i for i, l in enumerate(d) if l.strip().startswith(".section") and (".text." + kern) in l), None)
+    if st is not None:
+        dis, start = d, st
+        break
 per_line = collections.Counter(); cur = None; total = 0
 for l in dis[start + 1:]:
     if l.strip().startswith(".section"):
