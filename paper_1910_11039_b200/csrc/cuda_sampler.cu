@@ -618,6 +618,33 @@ __global__ void __launch_bounds__(256) dense_rows_kernel(const u64 *ext_offsets,
     }
 }
 
+// Fixed-stride rows (SamplerParams::ell): row v = its entries in row order, each with the target's degree - 1 in
+// the upper three bits, padded with kEllEmpty.  *bad is raised if a degree does not fit (a row above kEllWidth
+// entries, or a target without entries of its own -- an asymmetric input); the sampler then runs without them.
+__global__ void __launch_bounds__(256) ell_rows_kernel(const u64 *offsets, const u32 *targets, u64 n, u32 *ell, u32 *bad) {
+    for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v < n;
+         v += static_cast<u64>(gridDim.x) * blockDim.x) {
+        const u64 beg = offsets[v], deg = offsets[v + 1] - beg;
+        u32 row[kEllWidth];
+#pragma unroll
+        for (u32 k = 0; k < kEllWidth; ++k) {
+            row[k] = kEllEmpty;
+            if (k < deg) {
+                const u32 w = targets[beg + k];
+                const u64 dw = offsets[w + 1] - offsets[w];
+                if (dw < 1 || dw > kEllWidth)
+                    *bad = 1;
+                row[k] = w | (static_cast<u32>(dw - 1) << kEllDegShift);
+            }
+        }
+        if (deg > kEllWidth)
+            *bad = 1;
+        uint4 *out = reinterpret_cast<uint4 *>(ell) + 2 * v;
+        out[0] = make_uint4(row[0], row[1], row[2], row[3]);
+        out[1] = make_uint4(row[4], row[5], row[6], row[7]);
+    }
+}
+
 __global__ void __launch_bounds__(256) fill_two_kernel(double *a, double *b, u64 count, double value) {
     for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < count;
          i += static_cast<u64>(gridDim.x) * blockDim.x) {
@@ -755,6 +782,7 @@ struct CudaSampler::Impl {
     u64 *d_dense_offsets = nullptr; // hub-clustered copy the sampling kernel searches on (null: not renumbered)
     u32 *d_dense_targets = nullptr;
     u32 *d_to_dense = nullptr, *d_to_ext = nullptr;
+    u32 *d_ell = nullptr; // fixed-stride rows of the graph the kernel searches on (null: maximum degree above kEllWidth)
     std::vector<u32> h_to_ext; // fetched on demand (last_state)
     u32 block = 128;
     u32 items = 4;
@@ -803,6 +831,7 @@ struct CudaSampler::Impl {
         p.to_ext = d_to_ext;
         p.ext_offsets = d_offsets;
         p.ext_targets = d_targets;
+        p.ell = d_ell;
         p.lab = a.lab;
         p.list = a.list;
         p.sig = a.sig;
@@ -884,6 +913,28 @@ struct CudaSampler::Impl {
         dev_free(deg_sorted);
         dev_free(tmp);
         graph_bytes += (n + 1) * 8 + arcs * 4 + n * 8;
+    }
+
+    // Fixed-stride rows of the graph the kernel searches on (the dense copy if there is one).
+    void build_fixed_rows() {
+        cudaStream_t st = s_sample;
+        d_ell = dev_alloc<u32>(n * kEllWidth);
+        u32 *bad = dev_alloc<u32>(1);
+        EBC_CUDA(cudaMemsetAsync(bad, 0, 4, st));
+        const u32 grid = static_cast<u32>(std::min<u64>((n + 255) / 256, static_cast<u64>(sm_count) * 8));
+        ell_rows_kernel<<<grid, 256, 0, st>>>(d_dense_offsets ? d_dense_offsets : d_offsets,
+                                              d_dense_targets ? d_dense_targets : d_targets, n, d_ell, bad);
+        EBC_CUDA(cudaGetLastError());
+        u32 h_bad = 0;
+        EBC_CUDA(cudaMemcpyAsync(&h_bad, bad, 4, cudaMemcpyDeviceToHost, st));
+        EBC_CUDA(cudaStreamSynchronize(st));
+        dev_free(bad);
+        if (h_bad) {
+            dev_free(d_ell);
+            d_ell = nullptr;
+        } else {
+            graph_bytes += n * kEllWidth * 4;
+        }
     }
 
     // Launches the main pass and the re-run pass for [first, first+count), count <= kOverflowCap, on the
@@ -1027,10 +1078,10 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
 
     // ---- launch shape ----
     m.flags = opt.materialize_final_level ? kFlagMaterializeFinal : 0u;
+    std::uint64_t max_degree = 0;
     {
         // Visited bitmaps pay off when single rows are long enough to be probed (hub graphs); on
         // low-degree graphs they would only add an atomic per settled vertex.
-        std::uint64_t max_degree = 0;
         for (std::uint64_t v = 0; v < g.n; ++v)
             max_degree = std::max<std::uint64_t>(max_degree, g.degree(v));
         const char *env = std::getenv("EBC_BITMAP");
@@ -1080,6 +1131,10 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
     if (numbering < 0 || numbering > 2)
         throw ConfigError("renumber must be -1 (never), 0 (auto), 1 (degree classes) or 2 (neighbourhood clusters)");
     const bool want_dense = numbering != 0 && m.arcs && m.n < (u64{1} << 31); // (the CUB passes take 32-bit counts)
+    // Fixed-stride rows (expand_level_ell): lattice-like graphs, where a sample is a long chain of small levels.
+    bool want_ell = !m.hub_graph && max_degree <= kEllWidth && m.arcs && m.n < kEllIdMask && m.block <= 128;
+    if (const char *env = std::getenv("EBC_ELL"))
+        want_ell = want_ell && std::atoi(env) != 0;
     const int per_sm = occupancy_for(m.block, m.items);
     lap("occupancy query");
     if (per_sm < 1)
@@ -1096,7 +1151,8 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
     lap("memory query");
     const u64 fixed = (g.n + 1) * (4 * 2 + 8 + 8 + 16 + 12) + (u64{256} << 20) + kOverflowCap * 4 +
                       (cap < g.n ? kLargeSlots * SlotArrays::bytes_per_slot(g.n, g.n) : 0) +
-                      (want_dense ? g.n * 40 + m.arcs * 4 + (u64{16} << 20) : 0); // the dense copy is built below
+                      (want_dense ? g.n * 40 + m.arcs * 4 + (u64{16} << 20) : 0) + // the dense copy is built below
+                      (want_ell ? g.n * kEllWidth * 4 : 0);
     // Buffers cached by the pool are reusable (or released on demand), so they count as free.
     const u64 avail = capacity > live ? capacity - live : 0;
     const u64 budget = avail > fixed ? (avail - fixed) / 10 * 8 : 0;
@@ -1116,6 +1172,9 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
         m.numbering = numbering;
     }
     lap("dense numbering");
+    if (want_ell)
+        m.build_fixed_rows();
+    lap("fixed-stride rows");
 
     // ---- frames, state, bookkeeping ----
     for (int i = 0; i < 2; ++i) {
@@ -1174,6 +1233,7 @@ CudaSampler::Impl::~Impl() {
     dev_free(m.d_dense_targets);
     dev_free(m.d_to_dense);
     dev_free(m.d_to_ext);
+    dev_free(m.d_ell);
     for (int i = 0; i < 2; ++i) {
         dev_free(m.d_frame[i]);
         handles().give_words(m.h_result[i]);

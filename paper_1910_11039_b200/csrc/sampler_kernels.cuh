@@ -737,6 +737,242 @@ __device__ __forceinline__ u64 sum_frontier_degrees(const SamplerParams &p, cons
     return r;
 }
 
+// expand_level for graphs with fixed-stride rows (SamplerParams::ell: maximum degree <= kEllWidth -- grids, road
+// networks).  Such searches are long chains of small levels (config 3: 86 levels of ~450 vertices per sample): what
+// a level costs is its number of DEPENDENT memory round trips and the instructions issued around them, not its
+// bytes.  Per chunk of BLOCK frontier vertices there are three trips: list/sigma of the chunk (coalesced) -> the rows
+// (one 32-byte sector each, no offsets look-up) -> the labels of their targets.  Everything else stays on the SM:
+//  * thread t owns frontier vertex c0 + t and its (at most eight) entries, key = 8 t + k = discovery order
+//    (sampler.cpp:90-95: frontier order, then row order).  Entries are handled in two groups of four, the second
+//    only by warps that hold a row of more than four entries (the loops over groups are not unrolled: the code
+//    of a chunk is what sixteen CTAs per SM in different phases have to share the instruction cache for);
+//  * the unvisited targets of the chunk are deduplicated in a shared-memory hash table instead of being claimed in
+//    their labels: every candidate does atomicMin(table[h(v) + round], key); after a barrier the slot holds the
+//    lowest key that arrived.  A candidate that reads its own key back has won its vertex; one that finds a
+//    winner with the same vertex (kv[winner key] == v) has lost to it and keeps the winner's key; one that finds
+//    another vertex moves to the next slot in the next round.  All candidates of a vertex start at the same slot
+//    and are displaced together, so they always meet; a slot's value only decreases, and a key can be read as a
+//    slot's owner only if it won there.  On a grid a chunk has ~130 candidates in 8 BLOCK slots: one round,
+//    rarely two;
+//  * winners are ranked by a scan over the threads (keys ascend with the thread index, then k), settle their
+//    vertex (label, list, sigma = sigma[u]: sampler.cpp:93-98) and publish idx in kv[key]; the other discoverers
+//    add their sigma[u] after the barrier (sampler.cpp:97-98).  kv is double-buffered over the chunks, so a chunk
+//    costs three barriers;
+//  * the degree of a settled vertex travels in the upper bits of the entry that discovered it, so the next
+//    frontier's pending edges (sampler.cpp:95,102) and the bound behind `sigma_small` are sums over registers:
+//    sum_frontier_degrees -- two more dependent round trips per level -- is not needed.
+// Sets ex.pending, sh.prev_pending[e] and sh.sigma_small[e] itself.
+template <int BLOCK, int ITEMS>
+__device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRegs &ex, const SideRegs &ot, u32 *contact,
+                                 u32 &contact_n, BlockShared<BLOCK, ITEMS> &sh, WorkRegs &wk) {
+    constexpr u32 W = kEllWidth;
+    constexpr u32 KEYS = BLOCK * W; // candidates per chunk, at most; also the number of hash slots
+    constexpr u32 HBITS = BLOCK == 32 ? 8 : BLOCK == 64 ? 9 : 10;
+    constexpr int WARPS = BLOCK / 32;
+    static_assert((1u << HBITS) == KEYS && W == 8, "hash table size; a row is two 16-byte loads");
+    static_assert(sizeof(u32) * 3 * KEYS <= sizeof(sh.f_key) + sizeof(sh.f_s) + sizeof(sh.f_v) + sizeof(sh.f_o),
+                  "dedup tables alias the contact-edge arrays (only live in the meet phase)");
+    u32 *kv = reinterpret_cast<u32 *>(sh.f_key); // [2][KEYS] by key: the candidate's vertex; then a loser's winner key / a winner's idx
+    u32 *ht = kv + 2 * KEYS;                     // [KEYS] hash table: lowest key that arrived at the slot
+    u32 kv_flip = KEYS;                          // kv alternates between its halves from chunk to chunk
+    const u32 tid = threadIdx.x;
+    const u32 fb = ex.fb, fe = ex.cnt;
+    const u32 level_start = fe;
+    const u32 next_depth = ex.depth + 1;
+    u32 cnt = fe;
+    contact_n = 0;
+    const bool sigma_small = sh.sigma_small[e] != 0;
+    if (static_cast<u64>(next_depth) + 1 > p.aux_cap)
+        return false;
+    if (tid == 0) {
+        st_cg(ex.pp->lvl + next_depth, level_start);
+        sh.min_contact = 0xffffffffu;
+        sh.ws[kW_V_exp] += fe - fb;
+        sh.ws[kW_levels] += 1;
+        sh.ws[kW_E_bfs] += ex.pending; // the frontier's adjacency entries
+    }
+    const uint4 empty4 = make_uint4(kEllEmpty, kEllEmpty, kEllEmpty, kEllEmpty);
+    uint4 *ht_mine = reinterpret_cast<uint4 *>(ht) + 2 * tid; // the eight slots this thread clears
+    ht_mine[0] = empty4;
+    ht_mine[1] = empty4;
+    __syncthreads();
+    const u32 key0 = tid * W;
+    u32 pend = 0;  // degrees of the vertices this thread settled
+    u64 gsum = 0;  // saturating sum of sigma[u] over this thread's level edges (= its share of the new sigmas)
+    u32 n_lvl = 0;
+    for (u32 c0 = fb; c0 < fe; c0 += BLOCK, kv += kv_flip, kv_flip = 0u - kv_flip) {
+        // ---- trips 1 and 2: the chunk's vertices, their rows ----
+        const u32 i = c0 + tid;
+        uint4 a = empty4, b = empty4;
+        u64 sig_u = 0;
+        if (i < fe) {
+            const u32 u = ld_cg(ex.pp->list + i);
+            sig_u = ld_cg(ex.pp->sig + i);
+            const uint4 *row = reinterpret_cast<const uint4 *>(p.ell) + 2 * static_cast<u64>(u);
+            a = __ldg(row);
+            b = __ldg(row + 1);
+        }
+        const int ng = __any_sync(0xffffffffu, b.x != kEllEmpty) ? 2 : 1;
+        // ---- trip 3: labels; candidates enter the hash table (round 0) ----
+        u32 cand = 0, ccand = 0; // bit k: entry k is unvisited on this side / and visited on the other one
+        u32 n_edges = 0;         // level edges of this thread in this chunk
+#pragma unroll 1
+        for (int g = 0; g < ng; ++g) {
+            const u32 en[4] = {g ? b.x : a.x, g ? b.y : a.y, g ? b.z : a.z, g ? b.w : a.w};
+            u32 lb[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                lb[q] = en[q] != kEllEmpty ? ld_cg(lab + (en[q] & kEllIdMask)) : 0u;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (en[q] == kEllEmpty)
+                    continue;
+                const u32 v = en[q] & kEllIdMask;
+                const u32 d = lb[q] - ex.base, idx = d >> 1; // label = base + 2 idx + side (stale labels: idx >= 2^30)
+                const bool here = ((d ^ static_cast<u32>(e)) & 1u) == 0;
+                if (here && idx < cnt) {
+                    if (idx >= level_start) { // dist[v] == next_depth (sampler.cpp:97), settled by an earlier chunk
+                        sat_atomic_add(ex.pp->sig + idx, sig_u, sigma_small);
+                        ++n_edges;
+                    }
+                    continue;
+                }
+                const u32 key = key0 + 4 * g + q;
+                cand |= 1u << (4 * g + q);
+                kv[key] = v;
+                atomicMin(ht + ((v * 2654435761u) >> (32 - HBITS)), key);
+                if (!here && idx < ot.cnt) // other.visited(v) (sampler.cpp:107)
+                    ccand |= 1u << (4 * g + q);
+            }
+        }
+        n_edges += __popc(cand);
+        n_lvl += n_edges;
+        {
+            u64 add = sig_u * n_edges;
+            if (__umul64hi(sig_u, n_edges))
+                add = ~0ull;
+            gsum = gsum > ~0ull - add ? ~0ull : gsum + add;
+        }
+        // ---- deduplication rounds ----
+        u32 open = cand, win = 0;
+        u32 packed, incl;
+        for (u32 round = 0;; ++round) {
+            if (round) {
+#pragma unroll 1
+                for (int g = 0; g < ng; ++g) {
+                    const u32 en[4] = {g ? b.x : a.x, g ? b.y : a.y, g ? b.z : a.z, g ? b.w : a.w};
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if ((open >> (4 * g + q)) & 1u)
+                            atomicMin(ht + (((((en[q] & kEllIdMask) * 2654435761u) >> (32 - HBITS)) + round) & (KEYS - 1)),
+                                      key0 + 4 * g + q);
+                }
+            }
+            __syncthreads(); // this round's arrivals (and kv) are visible
+            if (open) {
+#pragma unroll 1
+                for (int g = 0; g < ng; ++g) {
+                    const u32 en[4] = {g ? b.x : a.x, g ? b.y : a.y, g ? b.z : a.z, g ? b.w : a.w};
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if ((open >> (4 * g + q)) & 1u) {
+                            const u32 v = en[q] & kEllIdMask, key = key0 + 4 * g + q;
+                            const u32 w = ht[(((v * 2654435761u) >> (32 - HBITS)) + round) & (KEYS - 1)];
+                            if (w == key) {
+                                win |= 1u << (4 * g + q);
+                                open &= ~(1u << (4 * g + q));
+                            } else if (kv[w] == v) {
+                                kv[key] = w; // (a loser's key is never read as an owner)
+                                open &= ~(1u << (4 * g + q));
+                            }
+                        }
+                }
+            }
+            // rank the winners: inclusive scan over the threads of (winners, contact winners); valid if this was the last round
+            packed = __popc(win) | (__popc(win & ccand) << 16);
+            incl = packed;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const u32 t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane_id() >= static_cast<u32>(o))
+                    incl += t;
+            }
+            if (WARPS > 1 && lane_id() == 31)
+                sh.warp_cnt[tid >> 5] = incl;
+            if (!__syncthreads_or(open != 0 ? 1 : 0))
+                break;
+        }
+        u32 totals = WARPS > 1 ? 0u : __shfl_sync(0xffffffffu, incl, 31);
+        if (WARPS > 1) {
+#pragma unroll
+            for (int w = 0; w < WARPS; ++w) {
+                const u32 c = sh.warp_cnt[w];
+                totals += c;
+                if (static_cast<u32>(w) < (tid >> 5))
+                    incl += c;
+            }
+        }
+        const u32 winners = totals & 0xffffu, ctot = totals >> 16;
+        if (static_cast<u64>(cnt) + winners > p.cap || (ctot && static_cast<u64>(contact_n) + ctot > p.aux_cap)) {
+            ex.cnt = cnt; // nothing of this chunk was written
+            return false;
+        }
+        if (win) {
+            u32 my_idx = cnt + ((incl - packed) & 0xffffu), my_c = contact_n + ((incl - packed) >> 16);
+#pragma unroll 1
+            for (int g = 0; g < ng; ++g) {
+                const u32 en[4] = {g ? b.x : a.x, g ? b.y : a.y, g ? b.z : a.z, g ? b.w : a.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if ((win >> (4 * g + q)) & 1u) {
+                        const u32 v = en[q] & kEllIdMask;
+                        if ((ccand >> (4 * g + q)) & 1u) { // contact (sampler.cpp:105-108); the label still holds the other side's idx
+                            const u32 oi = (ld_cg(lab + v) - ex.base) >> 1;
+                            atomicMin(&sh.min_contact, oi);
+                            st_cg(contact + 2 * static_cast<u64>(my_c), my_idx);
+                            st_cg(contact + 2 * static_cast<u64>(my_c) + 1, oi);
+                            ++my_c;
+                        }
+                        st_cg(lab + v, make_label(ex.base, my_idx, e)); // settle (sampler.cpp:93-95)
+                        st_cg(ex.pp->list + my_idx, v);
+                        st_cg(ex.pp->sig + my_idx, sig_u); // the discovering edge's sigma (sampler.cpp:98)
+                        kv[key0 + 4 * g + q] = my_idx;
+                        pend += (en[q] >> kEllDegShift) + 1;
+                        ++my_idx;
+                    }
+            }
+        }
+        ht_mine[0] = empty4; // (no reader of the table is left behind the last round's barrier)
+        ht_mine[1] = empty4;
+        __syncthreads(); // settled vertices, kv and the cleared table are visible
+        if (cand & ~win) {
+#pragma unroll 1
+            for (int g = 0; g < ng; ++g)
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (((cand & ~win) >> (4 * g + q)) & 1u) // later discoverers of a vertex settled in this chunk (sampler.cpp:97-98)
+                        sat_atomic_add(ex.pp->sig + kv[kv[key0 + 4 * g + q]], sig_u, sigma_small);
+        }
+        cnt += winners;
+        contact_n += ctot;
+    }
+    wk.e_lvl += n_lvl;
+    const u64 pending = block_sum_u64<BLOCK>(pend, sh.red64);
+    const int big = __syncthreads_or(gsum >= (1ull << 63) / BLOCK ? 1 : 0);
+    if (tid == 0) {
+        sh.ws[kW_V_set] += cnt - level_start;
+        sh.ws[kW_F_chk] += cnt - level_start;
+        sh.prev_pending[e] = ex.pending;
+        sh.sigma_small[e] = big ? 0u : 1u;
+    }
+    ex.pending = pending;
+    ex.fb = level_start; // sampler.cpp:101-103
+    ex.cnt = cnt;
+    ex.depth = next_depth;
+    __syncthreads();
+    return true;
+}
+
 // Read-only scan of the level that is about to be expanded on side `e`: every
 // adjacency slot is visited (its target is tested exactly as in expand_level)
 // but nothing is written.  Each slot whose target is unvisited on
@@ -1589,13 +1825,23 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
                     sh.rec.flags |= 4u; // the probe found more contact edges than it can resolve
                 __syncthreads(); // no sh.contact (or too many sh.contact edges): expand normally
             }
-            if (!expand_level<BLOCK, ITEMS, BITS>(p, sh.lab, sh.bits, vf, e, side[e], side[1 - e], sh.contact, contact_n, sh, wk)) {
+            bool fixed_rows = false; // (the fixed-stride path also takes the new frontier's pending edges)
+            if constexpr (!BITS && BLOCK <= 128)
+                fixed_rows = p.ell != nullptr;
+            bool ok;
+            if constexpr (!BITS && BLOCK <= 128)
+                ok = fixed_rows ? expand_level_ell<BLOCK, ITEMS>(p, sh.lab, e, side[e], side[1 - e], sh.contact, contact_n, sh, wk)
+                                : expand_level<BLOCK, ITEMS, BITS>(p, sh.lab, sh.bits, vf, e, side[e], side[1 - e], sh.contact,
+                                                                   contact_n, sh, wk);
+            else
+                ok = expand_level<BLOCK, ITEMS, BITS>(p, sh.lab, sh.bits, vf, e, side[e], side[1 - e], sh.contact, contact_n, sh, wk);
+            if (!ok) {
                 aborted = true;
                 break;
             }
             EBC_PH(1)
             found = sh.min_contact != 0xffffffffu;
-            if (!found) { // next_pending (sampler.cpp:95,102); evaluated fused into the level it was 3 % slower
+            if (!found && !fixed_rows) { // next_pending (sampler.cpp:95,102); evaluated fused into the level it was 3 % slower
                 if (tid == 0)
                     sh.prev_pending[e] = side[e].pending; // (read after the barriers of sum_frontier_degrees)
                 side[e].pending = sum_frontier_degrees<BLOCK>(p, side[e], sh.red64, &sh.sigma_small[e]);

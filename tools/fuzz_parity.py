@@ -10,7 +10,7 @@ cases = int(sys.argv[1]) if len(sys.argv) > 1 else 100
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
 t0 = time.time(); bad = 0
 for c in range(cases):
-    kind = rng.integers(0, 6)
+    kind = rng.integers(0, 8)
     if kind == 0:
         n = int(rng.integers(5, 400)); csr = random_graph(n, int(rng.integers(n // 2, 6 * n)), int(rng.integers(1 << 30)))
     elif kind == 1:
@@ -23,6 +23,10 @@ for c in range(cases):
         csr = (g0.offsets.copy(), g0.targets.copy())
     elif kind == 4:
         csr = star_graph(int(rng.integers(3, 3000)))
+    elif kind == 6:  # low maximum degree: the fixed-stride-row path (expand_level_ell)
+        n = int(rng.integers(20, 3000)); csr = random_graph(n, int(rng.integers(n // 2, 3 * n // 2)), int(rng.integers(1 << 30)))
+    elif kind == 7:
+        csr = grid_graph(int(rng.integers(20, 90)), int(rng.integers(20, 90)), float(rng.uniform(0, 0.15)), int(rng.integers(1 << 30)))
     else:
         n = int(rng.integers(1200, 4000)); csr = random_graph(n, int(rng.integers(2 * n, 12 * n)), int(rng.integers(1 << 30)))
     off, tg = csr
@@ -32,7 +36,7 @@ for c in range(cases):
     n = g.num_vertices
     block = int(rng.choice([32, 64, 128, 256, 512])); items = int(rng.choice([1, 2, 4]))
     cfg = ebc.RunConfig(block_threads=block, items_per_thread=items, slots=int(rng.choice([1, 3, 16, 0])),
-                        renumber=int(rng.choice([-1, 0, 1])), materialize_final_level=bool(rng.integers(0, 2)),
+                        renumber=int(rng.choice([-1, 0, 1, 2])), materialize_final_level=bool(rng.integers(0, 2)),
                         slot_capacity=int(rng.choice([0, 0, max(2, n // 7), 8])))
     seed = int(rng.integers(1 << 40)); first = int(rng.integers(1 << 20)); count = int(rng.integers(50, 1500))
     o = Oracle(off, tg)

@@ -35,7 +35,7 @@ hdr = rows[1]; ci = {h: i for i, h in enumerate(hdr)}
 data = rows[2:]
 base = int(data[0][ci["Address"]], 16) if data[0][ci["Address"]].startswith("0x") else int(data[0][ci["Address"]])
 agg = collections.defaultdict(lambda: [0.0, 0.0, 0.0, 0.0, 0.0])
-sort_col = 4 if '--noinst' in sys.argv else 0
+sort_col = 4 if "--noinst" in sys.argv else 3 if "--byinst" in sys.argv else 0
 tot = 0.0
 for r in data:
     a = r[ci["Address"]]; a = int(a, 16) if a.startswith("0x") else int(a)
