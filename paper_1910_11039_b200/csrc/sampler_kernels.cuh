@@ -746,18 +746,17 @@ __device__ __forceinline__ u64 sum_frontier_degrees(const SamplerParams &p, cons
 //    (sampler.cpp:90-95: frontier order, then row order).  Entries are handled in two groups of four, the second
 //    only by warps that hold a row of more than four entries (the loops over groups are not unrolled: the code
 //    of a chunk is what sixteen CTAs per SM in different phases have to share the instruction cache for);
-//  * the unvisited targets of the chunk are deduplicated in a shared-memory hash table instead of being claimed in
-//    their labels: every candidate does atomicMin(table[h(v) + round], key); after a barrier the slot holds the
-//    lowest key that arrived.  A candidate that reads its own key back has won its vertex; one that finds a
-//    winner with the same vertex (kv[winner key] == v) has lost to it and keeps the winner's key; one that finds
-//    another vertex moves to the next slot in the next round.  All candidates of a vertex start at the same slot
-//    and are displaced together, so they always meet; a slot's value only decreases, and a key can be read as a
-//    slot's owner only if it won there.  On a grid a chunk has ~130 candidates in 8 BLOCK slots: one round,
-//    rarely two;
+//  * the unvisited targets of the chunk are deduplicated in a shared-memory hash set instead of being claimed in
+//    their labels: a candidate inserts its vertex with linear probing (atomicCAS(hv[slot], empty, v) until the
+//    slot is empty or already holds v -- slots are never emptied while a chunk inserts, so all candidates of a
+//    vertex end in the same slot) and then does atomicMin(hk[slot], key).  After one barrier the candidate whose
+//    key is in hk[slot] has won the vertex, the others have lost to that key (first version: lock-step rounds
+//    of atomicMin(table[h(v) + round], key) with two barriers per round -- three to five rounds per chunk,
+//    as many as the longest probe sequence);
 //  * winners are ranked by a scan over the threads (keys ascend with the thread index, then k), settle their
 //    vertex (label, list, sigma = sigma[u]: sampler.cpp:93-98) and publish idx in kv[key]; the other discoverers
-//    add their sigma[u] after the barrier (sampler.cpp:97-98).  kv is double-buffered over the chunks, so a chunk
-//    costs three barriers;
+//    keep their winner's key in kv[own key] and add their sigma[u] after the barrier (sampler.cpp:97-98).  A
+//    chunk costs three barriers;
 //  * the degree of a settled vertex travels in the upper bits of the entry that discovered it, so the next
 //    frontier's pending edges (sampler.cpp:95,102) and the bound behind `sigma_small` are sums over registers:
 //    sum_frontier_degrees -- two more dependent round trips per level -- is not needed.
@@ -772,9 +771,9 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
     static_assert((1u << HBITS) == KEYS && W == 8, "hash table size; a row is two 16-byte loads");
     static_assert(sizeof(u32) * 3 * KEYS <= sizeof(sh.f_key) + sizeof(sh.f_s) + sizeof(sh.f_v) + sizeof(sh.f_o),
                   "dedup tables alias the contact-edge arrays (only live in the meet phase)");
-    u32 *kv = reinterpret_cast<u32 *>(sh.f_key); // [2][KEYS] by key: the candidate's vertex; then a loser's winner key / a winner's idx
-    u32 *ht = kv + 2 * KEYS;                     // [KEYS] hash table: lowest key that arrived at the slot
-    u32 kv_flip = KEYS;                          // kv alternates between its halves from chunk to chunk
+    u32 *kv = reinterpret_cast<u32 *>(sh.f_key); // [KEYS] by key: a loser's winner key / a winner's idx
+    u32 *hv = kv + KEYS;                         // [KEYS] hash set: the slot's vertex ...
+    u32 *hk = hv + KEYS;                         // [KEYS] ... and the lowest key that brought it
     const u32 tid = threadIdx.x;
     const u32 fb = ex.fb, fe = ex.cnt;
     const u32 level_start = fe;
@@ -792,15 +791,16 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
         sh.ws[kW_E_bfs] += ex.pending; // the frontier's adjacency entries
     }
     const uint4 empty4 = make_uint4(kEllEmpty, kEllEmpty, kEllEmpty, kEllEmpty);
-    uint4 *ht_mine = reinterpret_cast<uint4 *>(ht) + 2 * tid; // the eight slots this thread clears
-    ht_mine[0] = empty4;
-    ht_mine[1] = empty4;
+    uint4 *h_mine = reinterpret_cast<uint4 *>(hv) + tid; // this thread clears h_mine[0], [BLOCK], [2 BLOCK], [3 BLOCK] (hv and hk)
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        h_mine[q * BLOCK] = empty4;
     __syncthreads();
     const u32 key0 = tid * W;
     u32 pend = 0;  // degrees of the vertices this thread settled
     u64 gsum = 0;  // saturating sum of sigma[u] over this thread's level edges (= its share of the new sigmas)
     u32 n_lvl = 0;
-    for (u32 c0 = fb; c0 < fe; c0 += BLOCK, kv += kv_flip, kv_flip = 0u - kv_flip) {
+    for (u32 c0 = fb; c0 < fe; c0 += BLOCK) {
         // ---- trips 1 and 2: the chunk's vertices, their rows ----
         const u32 i = c0 + tid;
         uint4 a = empty4, b = empty4;
@@ -813,7 +813,7 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
             b = __ldg(row + 1);
         }
         const int ng = __any_sync(0xffffffffu, b.x != kEllEmpty) ? 2 : 1;
-        // ---- trip 3: labels; candidates enter the hash table (round 0) ----
+        // ---- trip 3: labels; candidates enter the hash set ----
         u32 cand = 0, ccand = 0; // bit k: entry k is unvisited on this side / and visited on the other one
         u32 n_edges = 0;         // level edges of this thread in this chunk
 #pragma unroll 1
@@ -839,8 +839,14 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
                 }
                 const u32 key = key0 + 4 * g + q;
                 cand |= 1u << (4 * g + q);
-                kv[key] = v;
-                atomicMin(ht + ((v * 2654435761u) >> (32 - HBITS)), key);
+                u32 slot = (v * 2654435761u) >> (32 - HBITS);
+                for (;;) { // (a chunk has at most KEYS distinct candidates: there is a slot for each)
+                    const u32 prev = atomicCAS(hv + slot, kEllEmpty, v);
+                    if (prev == kEllEmpty || prev == v)
+                        break;
+                    slot = (slot + 1) & (KEYS - 1);
+                }
+                atomicMin(hk + slot, key);
                 if (!here && idx < ot.cnt) // other.visited(v) (sampler.cpp:107)
                     ccand |= 1u << (4 * g + q);
             }
@@ -853,54 +859,40 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
                 add = ~0ull;
             gsum = gsum > ~0ull - add ? ~0ull : gsum + add;
         }
-        // ---- deduplication rounds ----
-        u32 open = cand, win = 0;
-        u32 packed, incl;
-        for (u32 round = 0;; ++round) {
-            if (round) {
+        // ---- winners; rank them: inclusive scan over the threads of (winners, contact winners) ----
+        __syncthreads(); // the hash set is complete
+        u32 win = 0;
+        if (cand) {
 #pragma unroll 1
-                for (int g = 0; g < ng; ++g) {
-                    const u32 en[4] = {g ? b.x : a.x, g ? b.y : a.y, g ? b.z : a.z, g ? b.w : a.w};
+            for (int g = 0; g < ng; ++g) {
+                const u32 en[4] = {g ? b.x : a.x, g ? b.y : a.y, g ? b.z : a.z, g ? b.w : a.w};
 #pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        if ((open >> (4 * g + q)) & 1u)
-                            atomicMin(ht + (((((en[q] & kEllIdMask) * 2654435761u) >> (32 - HBITS)) + round) & (KEYS - 1)),
-                                      key0 + 4 * g + q);
-                }
+                for (int q = 0; q < 4; ++q)
+                    if ((cand >> (4 * g + q)) & 1u) {
+                        const u32 v = en[q] & kEllIdMask, key = key0 + 4 * g + q;
+                        u32 slot = (v * 2654435761u) >> (32 - HBITS);
+                        while (hv[slot] != v)
+                            slot = (slot + 1) & (KEYS - 1);
+                        const u32 w = hk[slot];
+                        if (w == key)
+                            win |= 1u << (4 * g + q);
+                        else
+                            kv[key] = w;
+                    }
             }
-            __syncthreads(); // this round's arrivals (and kv) are visible
-            if (open) {
-#pragma unroll 1
-                for (int g = 0; g < ng; ++g) {
-                    const u32 en[4] = {g ? b.x : a.x, g ? b.y : a.y, g ? b.z : a.z, g ? b.w : a.w};
+        }
+        const u32 packed = __popc(win) | (__popc(win & ccand) << 16);
+        u32 incl = packed;
 #pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        if ((open >> (4 * g + q)) & 1u) {
-                            const u32 v = en[q] & kEllIdMask, key = key0 + 4 * g + q;
-                            const u32 w = ht[(((v * 2654435761u) >> (32 - HBITS)) + round) & (KEYS - 1)];
-                            if (w == key) {
-                                win |= 1u << (4 * g + q);
-                                open &= ~(1u << (4 * g + q));
-                            } else if (kv[w] == v) {
-                                kv[key] = w; // (a loser's key is never read as an owner)
-                                open &= ~(1u << (4 * g + q));
-                            }
-                        }
-                }
-            }
-            // rank the winners: inclusive scan over the threads of (winners, contact winners); valid if this was the last round
-            packed = __popc(win) | (__popc(win & ccand) << 16);
-            incl = packed;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const u32 t = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane_id() >= static_cast<u32>(o))
-                    incl += t;
-            }
-            if (WARPS > 1 && lane_id() == 31)
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane_id() >= static_cast<u32>(o))
+                incl += t;
+        }
+        if (WARPS > 1) {
+            if (lane_id() == 31)
                 sh.warp_cnt[tid >> 5] = incl;
-            if (!__syncthreads_or(open != 0 ? 1 : 0))
-                break;
+            __syncthreads();
         }
         u32 totals = WARPS > 1 ? 0u : __shfl_sync(0xffffffffu, incl, 31);
         if (WARPS > 1) {
@@ -942,9 +934,10 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
                     }
             }
         }
-        ht_mine[0] = empty4; // (no reader of the table is left behind the last round's barrier)
-        ht_mine[1] = empty4;
-        __syncthreads(); // settled vertices, kv and the cleared table are visible
+#pragma unroll
+        for (int q = 0; q < 4; ++q) // (every thread read the hash set before the scan's barrier / shuffles)
+            h_mine[q * BLOCK] = empty4;
+        __syncthreads(); // settled vertices, kv and the cleared hash set are visible
         if (cand & ~win) {
 #pragma unroll 1
             for (int g = 0; g < ng; ++g)
