@@ -676,14 +676,14 @@ void launch_sample_dispatch(u32 block, u32 items, const SamplerParams &p, u32 gr
     EBC_CUDA(cudaGetLastError());
 }
 
-int occupancy_for(u32 block, u32 items) {
+int occupancy_for(u32 block, u32 items, bool fixed_rows) {
     int per_sm = -1;
     switch (block) {
-    case 32: per_sm = sample_occupancy_b32(items); break;
-    case 64: per_sm = sample_occupancy_b64(items); break;
-    case 128: per_sm = sample_occupancy_b128(items); break;
-    case 256: per_sm = sample_occupancy_b256(items); break;
-    case 512: per_sm = sample_occupancy_b512(items); break;
+    case 32: per_sm = sample_occupancy_b32(items, fixed_rows); break;
+    case 64: per_sm = sample_occupancy_b64(items, fixed_rows); break;
+    case 128: per_sm = sample_occupancy_b128(items, fixed_rows); break;
+    case 256: per_sm = sample_occupancy_b256(items, fixed_rows); break;
+    case 512: per_sm = sample_occupancy_b512(items, fixed_rows); break;
     default: break;
     }
     if (per_sm == -1)
@@ -1135,7 +1135,7 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
     bool want_ell = !m.hub_graph && max_degree <= kEllWidth && m.arcs && m.n < kEllIdMask && m.block <= 128;
     if (const char *env = std::getenv("EBC_ELL"))
         want_ell = want_ell && std::atoi(env) != 0;
-    const int per_sm = occupancy_for(m.block, m.items);
+    const int per_sm = occupancy_for(m.block, m.items, want_ell);
     lap("occupancy query");
     if (per_sm < 1)
         throw CudaError("sampling kernel does not fit on an SM");

@@ -13,7 +13,21 @@ namespace ebc {
 #define EBC_CAT2(a, b) a##b
 #define EBC_CAT(a, b) EBC_CAT2(a, b)
 
+// Graphs with fixed-stride rows (SamplerParams::ell) have a kernel of their own: one per block size up to 128 threads
+// (the adjacency slots per thread of the general expansion mean nothing there).
+#if EBC_SHAPE_BLOCK <= 128
+#define EBC_HAVE_FIXED 1
+#else
+#define EBC_HAVE_FIXED 0
+#endif
+
 template <int ITEMS> static void launch_one(const SamplerParams &p, u32 grid, cudaStream_t stream) {
+#if EBC_HAVE_FIXED
+    if (p.ell) {
+        sample_kernel<EBC_SHAPE_BLOCK, 2, false, true><<<grid, EBC_SHAPE_BLOCK, 0, stream>>>(p);
+        return;
+    }
+#endif
     if (p.flags & kFlagUseBitmap)
         sample_kernel<EBC_SHAPE_BLOCK, ITEMS, true><<<grid, EBC_SHAPE_BLOCK, 0, stream>>>(p);
     else
@@ -37,7 +51,18 @@ template <int ITEMS> static int occupancy_one() {
     return per_sm;
 }
 
-int EBC_CAT(sample_occupancy_b, EBC_SHAPE_BLOCK)(u32 items) {
+int EBC_CAT(sample_occupancy_b, EBC_SHAPE_BLOCK)(u32 items, bool fixed_rows) {
+    if (fixed_rows) {
+#if EBC_HAVE_FIXED
+        int per_sm = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sample_kernel<EBC_SHAPE_BLOCK, 2, false, true>,
+                                                          EBC_SHAPE_BLOCK, 0) != cudaSuccess)
+            return -2;
+        return per_sm;
+#else
+        return -1;
+#endif
+    }
     switch (items) {
     case 1: return occupancy_one<1>();
     case 2: return occupancy_one<2>();

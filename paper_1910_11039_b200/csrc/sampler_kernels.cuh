@@ -771,7 +771,8 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
     static_assert((1u << HBITS) == KEYS && W == 8, "hash table size; a row is two 16-byte loads");
     static_assert(sizeof(u32) * 3 * KEYS <= sizeof(sh.f_key) + sizeof(sh.f_s) + sizeof(sh.f_v) + sizeof(sh.f_o),
                   "dedup tables alias the contact-edge arrays (only live in the meet phase)");
-    u32 *kv = reinterpret_cast<u32 *>(sh.f_key); // [KEYS] by key: a loser's winner key / a winner's idx
+    u32 *kv = reinterpret_cast<u32 *>(sh.f_key); // [W][BLOCK] by key 8 t + k at [k][t] (no bank conflicts): the candidate's slot; then a
+                                                 // loser's winner key / a winner's idx
     u32 *hv = kv + KEYS;                         // [KEYS] hash set: the slot's vertex ...
     u32 *hk = hv + KEYS;                         // [KEYS] ... and the lowest key that brought it
     const u32 tid = threadIdx.x;
@@ -800,18 +801,26 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
     u32 pend = 0;  // degrees of the vertices this thread settled
     u64 gsum = 0;  // saturating sum of sigma[u] over this thread's level edges (= its share of the new sigmas)
     u32 n_lvl = 0;
+    // The frontier is known when the level starts, so a chunk's vertex is loaded two chunks ahead and its row is
+    // requested into L2 one chunk ahead: of the three trips only the labels' (and a short L2 hit for the row)
+    // stay on a chunk's critical path.
+    u32 u_cur = fb + tid < fe ? ld_cg(ex.pp->list + fb + tid) : 0u;
+    u32 u_nxt = fb + BLOCK + tid < fe ? ld_cg(ex.pp->list + fb + BLOCK + tid) : 0u;
     for (u32 c0 = fb; c0 < fe; c0 += BLOCK) {
         // ---- trips 1 and 2: the chunk's vertices, their rows ----
         const u32 i = c0 + tid;
         uint4 a = empty4, b = empty4;
         u64 sig_u = 0;
         if (i < fe) {
-            const u32 u = ld_cg(ex.pp->list + i);
             sig_u = ld_cg(ex.pp->sig + i);
-            const uint4 *row = reinterpret_cast<const uint4 *>(p.ell) + 2 * static_cast<u64>(u);
+            const uint4 *row = reinterpret_cast<const uint4 *>(p.ell) + 2 * static_cast<u64>(u_cur);
             a = __ldg(row);
             b = __ldg(row + 1);
         }
+        u_cur = u_nxt;
+        if (i + BLOCK < fe)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const uint4 *>(p.ell) + 2 * static_cast<u64>(u_nxt)));
+        u_nxt = i + 2 * BLOCK < fe ? ld_cg(ex.pp->list + i + 2 * BLOCK) : 0u;
         const int ng = __any_sync(0xffffffffu, b.x != kEllEmpty) ? 2 : 1;
         // ---- trip 3: labels; candidates enter the hash set ----
         u32 cand = 0, ccand = 0; // bit k: entry k is unvisited on this side / and visited on the other one
@@ -847,6 +856,7 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
                     slot = (slot + 1) & (KEYS - 1);
                 }
                 atomicMin(hk + slot, key);
+                kv[(4 * g + q) * BLOCK + tid] = slot;
                 if (!here && idx < ot.cnt) // other.visited(v) (sampler.cpp:107)
                     ccand |= 1u << (4 * g + q);
             }
@@ -865,19 +875,15 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
         if (cand) {
 #pragma unroll 1
             for (int g = 0; g < ng; ++g) {
-                const u32 en[4] = {g ? b.x : a.x, g ? b.y : a.y, g ? b.z : a.z, g ? b.w : a.w};
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
                     if ((cand >> (4 * g + q)) & 1u) {
-                        const u32 v = en[q] & kEllIdMask, key = key0 + 4 * g + q;
-                        u32 slot = (v * 2654435761u) >> (32 - HBITS);
-                        while (hv[slot] != v)
-                            slot = (slot + 1) & (KEYS - 1);
-                        const u32 w = hk[slot];
+                        const u32 key = key0 + 4 * g + q;
+                        const u32 w = hk[kv[(4 * g + q) * BLOCK + tid]];
                         if (w == key)
                             win |= 1u << (4 * g + q);
                         else
-                            kv[key] = w;
+                            kv[(4 * g + q) * BLOCK + tid] = w;
                     }
             }
         }
@@ -928,7 +934,7 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
                         st_cg(lab + v, make_label(ex.base, my_idx, e)); // settle (sampler.cpp:93-95)
                         st_cg(ex.pp->list + my_idx, v);
                         st_cg(ex.pp->sig + my_idx, sig_u); // the discovering edge's sigma (sampler.cpp:98)
-                        kv[key0 + 4 * g + q] = my_idx;
+                        kv[(4 * g + q) * BLOCK + tid] = my_idx;
                         pend += (en[q] >> kEllDegShift) + 1;
                         ++my_idx;
                     }
@@ -944,7 +950,10 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
                     if (((cand & ~win) >> (4 * g + q)) & 1u) // later discoverers of a vertex settled in this chunk (sampler.cpp:97-98)
-                        sat_atomic_add(ex.pp->sig + kv[kv[key0 + 4 * g + q]], sig_u, sigma_small);
+                    {
+                        const u32 w = kv[(4 * g + q) * BLOCK + tid]; // the winner's key
+                        sat_atomic_add(ex.pp->sig + kv[(w & (W - 1)) * BLOCK + w / W], sig_u, sigma_small);
+                    }
         }
         cnt += winners;
         contact_n += ctot;
@@ -1606,14 +1615,22 @@ __device__ void walk_side(const SamplerParams &p, const u32 *lab, int x, const S
 #ifndef EBC_WARPS_PER_SM
 #define EBC_WARPS_PER_SM 32
 #endif
-template <int BLOCK> constexpr int min_blocks_per_sm() {
-    return (EBC_WARPS_PER_SM * 32) / BLOCK > 0 ? (EBC_WARPS_PER_SM * 32) / BLOCK : 1;
+#ifndef EBC_FIXED_WARPS_PER_SM
+#define EBC_FIXED_WARPS_PER_SM 32
+#endif
+template <int BLOCK, bool FIXED> constexpr int min_blocks_per_sm() {
+    constexpr int warps = FIXED ? EBC_FIXED_WARPS_PER_SM : EBC_WARPS_PER_SM;
+    return (warps * 32) / BLOCK > 0 ? (warps * 32) / BLOCK : 1;
 }
 
 // BITS: the launch uses visited bitmaps (kFlagUseBitmap); a template parameter so that each kernel
 // carries only its own variant of the probe code -- the instruction footprint matters, see above.
-template <int BLOCK, int ITEMS, bool BITS>
-__global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kernel(const SamplerParams p) {
+// FIXED: the graph has fixed-stride rows (SamplerParams::ell).  That kernel consists of expand_level_ell, the
+// contact-list meet and the walk only -- no read-only probe (a lattice-like search does not end in a level much
+// wider than the ones before), no general expansion, no bitmaps: a third of the instruction footprint.
+template <int BLOCK, int ITEMS, bool BITS, bool FIXED = false>
+__global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) sample_kernel(const SamplerParams p) {
+    static_assert(!(FIXED && BITS) && (!FIXED || BLOCK <= 128), "fixed-stride rows: no bitmaps, at most 128 threads");
     __shared__ BlockShared<BLOCK, ITEMS> sh;
     __shared__ u32 vf[BITS ? VisitedFilter<BLOCK>::kWords : 1]; // visited filter of the sample in flight
     const u32 tid = threadIdx.x;
@@ -1783,6 +1800,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             // expanding graphs (R-MAT, Erdos-Renyi) end in their widest level; on lattice-like graphs the
             // frontier grows by a few per cent per level, almost no level is the last, and probing every wide
             // level cost config 3 a quarter of its time.
+            if constexpr (!FIXED)
             if (!(p.flags & kFlagMaterializeFinal) && edge_cap() > 0 && side[e].pending >= p.probe_min_slots &&
                 4 * side[e].pending >= p.probe_growth_x4 * sh.prev_pending[e] &&
                 static_cast<u64>(side[e].depth) + 2 <= p.aux_cap) {
@@ -1818,14 +1836,9 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
                     sh.rec.flags |= 4u; // the probe found more contact edges than it can resolve
                 __syncthreads(); // no sh.contact (or too many sh.contact edges): expand normally
             }
-            bool fixed_rows = false; // (the fixed-stride path also takes the new frontier's pending edges)
-            if constexpr (!BITS && BLOCK <= 128)
-                fixed_rows = p.ell != nullptr;
             bool ok;
-            if constexpr (!BITS && BLOCK <= 128)
-                ok = fixed_rows ? expand_level_ell<BLOCK, ITEMS>(p, sh.lab, e, side[e], side[1 - e], sh.contact, contact_n, sh, wk)
-                                : expand_level<BLOCK, ITEMS, BITS>(p, sh.lab, sh.bits, vf, e, side[e], side[1 - e], sh.contact,
-                                                                   contact_n, sh, wk);
+            if constexpr (FIXED) // (also takes the new frontier's pending edges)
+                ok = expand_level_ell<BLOCK, ITEMS>(p, sh.lab, e, side[e], side[1 - e], sh.contact, contact_n, sh, wk);
             else
                 ok = expand_level<BLOCK, ITEMS, BITS>(p, sh.lab, sh.bits, vf, e, side[e], side[1 - e], sh.contact, contact_n, sh, wk);
             if (!ok) {
@@ -1834,13 +1847,14 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             }
             EBC_PH(1)
             found = sh.min_contact != 0xffffffffu;
-            if (!found && !fixed_rows) { // next_pending (sampler.cpp:95,102); evaluated fused into the level it was 3 % slower
-                if (tid == 0)
-                    sh.prev_pending[e] = side[e].pending; // (read after the barriers of sum_frontier_degrees)
-                side[e].pending = sum_frontier_degrees<BLOCK>(p, side[e], sh.red64, &sh.sigma_small[e]);
+            if constexpr (!FIXED) {
+                if (!found) { // next_pending (sampler.cpp:95,102); evaluated fused into the level it was 3 % slower
+                    if (tid == 0)
+                        sh.prev_pending[e] = side[e].pending; // (read after the barriers of sum_frontier_degrees)
+                    side[e].pending = sum_frontier_degrees<BLOCK>(p, side[e], sh.red64, &sh.sigma_small[e]);
+                } else
+                    __syncthreads();
             }
-            else
-                __syncthreads();
             EBC_PH(3)
         }
 
@@ -1871,12 +1885,15 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK>()) sample_kern
             __syncthreads();
 
             // meet set in discovery order (sampler.cpp:109-113) -> sh.meetbuf
-            const u32 meet_count =
-                !probed ? meet_from_contacts<BLOCK, ITEMS>(sh.contact, contact_n, ex, olo, ohi, sh.meetbuf, sh)
-                : edge_n <= static_cast<u32>(FinalEdgeCap<BLOCK>::value)
-                    ? meet_from_edges<BLOCK, ITEMS>(sh.contact, edge_n, olo, ohi, sh.meetbuf, sh)
-                    : meet_from_edges_large<BLOCK, ITEMS>(sh.contact, edge_n, olo, ohi, sh.meetbuf, ex.pp->sig + ex.cnt,
-                                                          ot.pp->sig + ot.cnt, sh);
+            u32 meet_count;
+            if constexpr (FIXED)
+                meet_count = meet_from_contacts<BLOCK, ITEMS>(sh.contact, contact_n, ex, olo, ohi, sh.meetbuf, sh);
+            else
+                meet_count = !probed ? meet_from_contacts<BLOCK, ITEMS>(sh.contact, contact_n, ex, olo, ohi, sh.meetbuf, sh)
+                             : edge_n <= static_cast<u32>(FinalEdgeCap<BLOCK>::value)
+                                 ? meet_from_edges<BLOCK, ITEMS>(sh.contact, edge_n, olo, ohi, sh.meetbuf, sh)
+                                 : meet_from_edges_large<BLOCK, ITEMS>(sh.contact, edge_n, olo, ohi, sh.meetbuf,
+                                                                       ex.pp->sig + ex.cnt, ot.pp->sig + ot.cnt, sh);
 
             // total weight over the meet set (sampler.cpp:121-123), saturating at 2^128-1
             u128 wsum = 0;
