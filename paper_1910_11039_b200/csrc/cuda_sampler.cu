@@ -618,9 +618,9 @@ __global__ void __launch_bounds__(256) dense_rows_kernel(const u64 *ext_offsets,
     }
 }
 
-// Fixed-stride rows (SamplerParams::ell): row v = its entries in row order, each with the target's degree - 1 in
-// the upper three bits, padded with kEllEmpty.  *bad is raised if a degree does not fit (a row above kEllWidth
-// entries, or a target without entries of its own -- an asymmetric input); the sampler then runs without them.
+// Fixed-stride rows (SamplerParams::ell): row v = its entries in row order, each with the position of the reverse arc
+// and the target's degree - 1 in the upper bits, padded with kEllEmpty.  *bad is raised if that does not work out (a
+// row above kEllWidth entries, or an arc without its reverse -- an asymmetric input); the sampler then runs without them.
 __global__ void __launch_bounds__(256) ell_rows_kernel(const u64 *offsets, const u32 *targets, u64 n, u32 *ell, u32 *bad) {
     for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v < n;
          v += static_cast<u64>(gridDim.x) * blockDim.x) {
@@ -631,10 +631,14 @@ __global__ void __launch_bounds__(256) ell_rows_kernel(const u64 *offsets, const
             row[k] = kEllEmpty;
             if (k < deg) {
                 const u32 w = targets[beg + k];
-                const u64 dw = offsets[w + 1] - offsets[w];
-                if (dw < 1 || dw > kEllWidth)
+                const u64 wb = offsets[w], dw = offsets[w + 1] - wb;
+                u32 rev = kEllWidth; // position of v in the row of w
+                for (u32 j = 0; j < kEllWidth && j < dw; ++j)
+                    if (targets[wb + j] == v)
+                        rev = j;
+                if (dw < 1 || dw > kEllWidth || rev == kEllWidth)
                     *bad = 1;
-                row[k] = w | (static_cast<u32>(dw - 1) << kEllDegShift);
+                row[k] = w | ((rev & (kEllWidth - 1)) << kEllRevShift) | (static_cast<u32>(dw - 1) << kEllDegShift);
             }
         }
         if (deg > kEllWidth)
@@ -698,15 +702,19 @@ int occupancy_for(u32 block, u32 items, bool fixed_rows) {
 static u64 bit_words_of(u64 n) { return ((n + 31) / 32 + 3) & ~u64{3}; }
 
 struct SlotArrays {
-    u32 *lab = nullptr, *list = nullptr, *lvl = nullptr, *contact = nullptr, *hdr = nullptr, *bits = nullptr;
+    u32 *lab = nullptr, *list = nullptr, *lvl = nullptr, *contact = nullptr, *hdr = nullptr, *bits = nullptr, *pm = nullptr;
     u64 *sig = nullptr;
     u64 slots = 0, cap = 0, aux_cap = 0;
     u64 bytes = 0;
 
-    void allocate(u64 slots_, u64 cap_, u64 n, cudaStream_t stream) {
+    static u64 pm_words_of(u64 cap) { return (cap + 3) / 4 + 1; }
+
+    void allocate(u64 slots_, u64 cap_, u64 n, bool fixed_rows, cudaStream_t stream) {
         slots = slots_;
         cap = cap_;
         aux_cap = aux_cap_of(cap_, n);
+        if (fixed_rows)
+            pm = dev_alloc<u32>(slots * 2 * pm_words_of(cap));
         lab = dev_alloc<u32>(slots * n);
         list = dev_alloc<u32>(slots * 2 * cap);
         sig = dev_alloc<u64>(slots * 2 * cap);
@@ -715,7 +723,7 @@ struct SlotArrays {
         bits = dev_alloc<u32>(slots * 2 * bit_words_of(n));
         EBC_CUDA(cudaMemsetAsync(bits, 0, slots * 2 * bit_words_of(n) * 4, stream));
         hdr = dev_alloc<u32>(slots * kHdrWords);
-        bytes = slots * bytes_per_slot(n, cap);
+        bytes = slots * bytes_per_slot(n, cap, fixed_rows);
         EBC_CUDA(cudaMemsetAsync(lab, 0, slots * n * 4, stream));
         std::vector<u32> h(slots * kHdrWords, 0);
         for (u64 s = 0; s < slots; ++s)
@@ -732,6 +740,7 @@ struct SlotArrays {
     }
     void release() {
         dev_free(lab);
+        dev_free(pm);
         dev_free(list);
         dev_free(sig);
         dev_free(lvl);
@@ -742,9 +751,9 @@ struct SlotArrays {
     // Level table and contact list are far smaller than the settle lists in practice: 2^16 entries unless
     // the slot is a full-capacity one (cap == n), which must never overflow.
     static u64 aux_cap_of(u64 cap, u64 n) { return cap >= n ? n : std::min<u64>(cap, u64{1} << 16); }
-    static u64 bytes_per_slot(u64 n, u64 cap) {
+    static u64 bytes_per_slot(u64 n, u64 cap, bool fixed_rows) {
         const u64 aux = aux_cap_of(cap, n);
-        return n * 4 + 2 * bit_words_of(n) * 4 + 2 * cap * (4 + 8) + 2 * (aux + 2) * 4 + 6 * aux * 4 + kHdrWords * 4;
+        return (fixed_rows ? 2 * pm_words_of(cap) * 4 : 0) + n * 4 + 2 * bit_words_of(n) * 4 + 2 * cap * (4 + 8) + 2 * (aux + 2) * 4 + 6 * aux * 4 + kHdrWords * 4;
     }
 };
 
@@ -839,6 +848,8 @@ struct CudaSampler::Impl {
         p.contact = a.contact;
         p.hdr = a.hdr;
         p.bits = a.bits;
+        p.pm = a.pm;
+        p.pm_words = SlotArrays::pm_words_of(a.cap);
         p.bit_words = bit_words_of(n);
         p.probe_min_slots = probe_min_slots;
         p.probe_growth_x4 = probe_growth_x4;
@@ -1150,22 +1161,22 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
     const u64 live = pool().live_bytes();
     lap("memory query");
     const u64 fixed = (g.n + 1) * (4 * 2 + 8 + 8 + 16 + 12) + (u64{256} << 20) + kOverflowCap * 4 +
-                      (cap < g.n ? kLargeSlots * SlotArrays::bytes_per_slot(g.n, g.n) : 0) +
+                      (cap < g.n ? kLargeSlots * SlotArrays::bytes_per_slot(g.n, g.n, want_ell) : 0) +
                       (want_dense ? g.n * 40 + m.arcs * 4 + (u64{16} << 20) : 0) + // the dense copy is built below
                       (want_ell ? g.n * kEllWidth * 4 : 0);
     // Buffers cached by the pool are reusable (or released on demand), so they count as free.
     const u64 avail = capacity > live ? capacity - live : 0;
     const u64 budget = avail > fixed ? (avail - fixed) / 10 * 8 : 0;
-    const u64 per_slot = SlotArrays::bytes_per_slot(g.n, cap);
+    const u64 per_slot = SlotArrays::bytes_per_slot(g.n, cap, want_ell);
     if (!opt.slots && slots * per_slot > budget)
         slots = budget / per_slot;
     if (slots < 1)
         throw CudaError("not enough device memory for a single sampling slot");
     // The slot arrays are cleared on the aggregation stream while the graph is still crossing PCIe on the
     // sampling stream (the numbering below waits for it).
-    m.small.allocate(slots, cap, g.n, m.s_agg);
+    m.small.allocate(slots, cap, g.n, want_ell, m.s_agg);
     if (cap < g.n)
-        m.big.allocate(kLargeSlots, g.n, g.n, m.s_agg);
+        m.big.allocate(kLargeSlots, g.n, g.n, want_ell, m.s_agg);
     lap("slot arrays");
     if (want_dense) {
         m.build_dense_graph(numbering == 2);

@@ -40,9 +40,10 @@ constexpr u32 kMaxTileSlots = 4096;        // BLOCK * ITEMS never exceeds this
 constexpr u32 kFlagUseBitmap = 2u;        // per-slot visited bitmaps are maintained and used by probe_level
 constexpr u32 kFlagMaterializeFinal = 1u; // always settle the final level (state dumps, exact V_set / F_chk)
 constexpr u32 kEllWidth = 8;               // entries per fixed-stride row (SamplerParams::ell)
-constexpr u32 kEllDegShift = 29;           // an entry's upper three bits: degree of the target, minus one
-constexpr u32 kEllIdMask = (1u << kEllDegShift) - 1;
-constexpr u32 kEllEmpty = 0xffffffffu;     // (a graph with fixed-stride rows has fewer than 2^29 - 1 vertices)
+constexpr u32 kEllRevShift = 26;           // bits 26..28 of an entry: position of the reverse arc in the target's row
+constexpr u32 kEllDegShift = 29;           // bits 29..31: degree of the target, minus one
+constexpr u32 kEllIdMask = (1u << kEllRevShift) - 1;
+constexpr u32 kEllEmpty = 0xffffffffu;     // (a graph with fixed-stride rows has fewer than 2^26 - 1 vertices)
 constexpr u32 kHdrWords = 16;              // per-slot header (u32)
 // header word indices
 enum : int { kHdrBase0 = 0, kHdrBase1 = 1, kHdrLastBase0 = 2, kHdrLastBase1 = 3, kHdrLastCnt0 = 4,
@@ -69,11 +70,16 @@ struct SamplerParams {
     const u32 *to_ext;   // dense id -> external id
     const u64 *ext_offsets;
     const u32 *ext_targets;
-    // Fixed-stride rows (optional; graphs whose maximum degree is at most kEllWidth, e.g. grids and road networks):
-    // ell[kEllWidth * v + k] = k-th entry of row v of the graph above, packed as target | (degree(target) - 1) << 29,
-    // or kEllEmpty behind the row's end.  A row is one 32-byte sector at a computable address, and the degree of a
-    // settled vertex comes with the entry that discovered it (expand_level_ell in sampler_kernels.cuh).
+    // Fixed-stride rows (optional; symmetric graphs whose maximum degree is at most kEllWidth, e.g. grids and road
+    // networks): ell[kEllWidth * v + k] = k-th entry of row v of the graph above, packed as
+    // target | (position of v in the target's row) << 26 | (degree(target) - 1) << 29, or kEllEmpty behind the
+    // row's end.  A row is one 32-byte sector at a computable address; the degree of a settled vertex comes with the
+    // entry that discovered it, and the reverse position lets it remember which of its own entries lead back to
+    // its discoverers (expand_level_ell in sampler_kernels.cuh).
     const u32 *ell;
+    u32 *pm;       // [slots][2][pm_words] with fixed-stride rows: per settled vertex (indexed like list, one byte each)
+                   // the mask of row entries that lead to its parents
+    u64 pm_words;
     // slots
     u32 *lab;      // [slots][n]
     u32 *list;     // [slots][2][cap]   settled vertices in discovery order

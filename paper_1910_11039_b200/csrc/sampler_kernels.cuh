@@ -25,6 +25,8 @@
 // pending edge counts and counters are order independent.
 #pragma once
 
+#include <cstddef>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "device_types.cuh"
@@ -77,6 +79,22 @@ __device__ __forceinline__ void red_max_u32(u32 *p, u32 v) {
 __device__ __forceinline__ void red_or_u32(u32 *p, u32 v) {
     asm volatile("red.global.or.b32 [%0], %1;" ::"l"(__cvta_generic_to_global(p)), "r"(v) : "memory");
 }
+
+// Shared-memory accesses by shared-window address (see expand_level_ell).
+__device__ __forceinline__ u32 smem_addr(const void *p) { return static_cast<u32>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ u32 lds_u32(u32 a) {
+    u32 v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts_u32(u32 a, u32 v) { asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory"); }
+__device__ __forceinline__ u32 atoms_cas_u32(u32 a, u32 cmp, u32 v) {
+    u32 old;
+    asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(old) : "r"(a), "r"(cmp), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ void reds_min_u32(u32 a, u32 v) { asm volatile("red.shared.min.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory"); }
+__device__ __forceinline__ void reds_or_u32(u32 a, u32 v) { asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory"); }
 
 __device__ __forceinline__ u32 lane_id() { return threadIdx.x & 31u; }
 __device__ __forceinline__ u32 lanemask_lt() {
@@ -142,6 +160,7 @@ struct SidePtrs {
     u32 *list;
     u64 *sig;
     u32 *lvl;
+    u32 *pm; // fixed-stride rows: parent masks, one byte per settled vertex (SamplerParams::pm)
 };
 
 constexpr int kPredCache = 32;
@@ -164,6 +183,10 @@ template <int BLOCK, int ITEMS> struct BlockShared {
     u64 f_s[FinalEdgeCap<BLOCK>::value];   //   sigma of the parent,
     u32 f_v[FinalEdgeCap<BLOCK>::value];   //   target vertex,
     u32 f_o[FinalEdgeCap<BLOCK>::value];   //   its idx on the other side
+    // (f_key .. c_sig are contiguous: expand_level_ell keeps its tables there)
+    u64 c_beg[BLOCK];      // row start of each frontier-chunk vertex
+    u64 c_scan[BLOCK + 1]; // exclusive prefix of the chunk's degrees
+    u64 c_sig[BLOCK];      // sigma of each chunk vertex
     u32 edge_cnt;
     SidePtrs sp[2];
     u64 prev_pending[2]; // per side: pending edges of the level expanded last (0 before the first)
@@ -171,9 +194,6 @@ template <int BLOCK, int ITEMS> struct BlockShared {
     u32 last[6]; // base / cnt / depth of both sides of the last finished sample (state dumps)
     u32 *lab, *bits, *contact, *meetbuf; // the slot's label / bitmap / contact arrays
     SampleRecordDev rec; // record of the sample in flight (thread 0)
-    u64 c_beg[BLOCK];      // row start of each frontier-chunk vertex
-    u64 c_scan[BLOCK + 1]; // exclusive prefix of the chunk's degrees
-    u64 c_sig[BLOCK];      // sigma of each chunk vertex
     u64 red64[WARPS * 3];  // block reductions
     u32 warp_cnt[ITEMS * WARPS];
     u32 warp_cnt2[ITEMS * WARPS];
@@ -769,16 +789,24 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
     constexpr u32 HBITS = BLOCK == 32 ? 8 : BLOCK == 64 ? 9 : 10;
     constexpr int WARPS = BLOCK / 32;
     static_assert((1u << HBITS) == KEYS && W == 8, "hash table size; a row is two 16-byte loads");
-    static_assert(sizeof(u32) * 3 * KEYS <= sizeof(sh.f_key) + sizeof(sh.f_s) + sizeof(sh.f_v) + sizeof(sh.f_o),
-                  "dedup tables alias the contact-edge arrays (only live in the meet phase)");
-    u32 *kv = reinterpret_cast<u32 *>(sh.f_key); // [W][BLOCK] by key 8 t + k at [k][t] (no bank conflicts): the candidate's slot; then a
-                                                 // loser's winner key / a winner's idx
-    u32 *hv = kv + KEYS;                         // [KEYS] hash set: the slot's vertex ...
-    u32 *hk = hv + KEYS;                         // [KEYS] ... and the lowest key that brought it
+    using Shared = BlockShared<BLOCK, ITEMS>;
+    static_assert(sizeof(u32) * (3 * KEYS + KEYS / 4) <= offsetof(Shared, c_sig) + sizeof(sh.c_sig) - offsetof(Shared, f_key) &&
+                      offsetof(Shared, c_sig) + sizeof(sh.c_sig) - offsetof(Shared, f_key) ==
+                          sizeof(sh.f_key) + sizeof(sh.f_s) + sizeof(sh.f_v) + sizeof(sh.f_o) + sizeof(sh.c_beg) +
+                              sizeof(sh.c_scan) + sizeof(sh.c_sig),
+                  "dedup tables alias the contact-edge and chunk arrays (live in the meet phase / the general expansion only)");
+    // Tables, as shared-window byte addresses (ld/st/atom.shared: no generic-address arithmetic per access):
+    u32 *tab = reinterpret_cast<u32 *>(sh.f_key);
+    const u32 kv_base = smem_addr(tab);          // [W][BLOCK] by key 8 t + k at [k][t] (no bank conflicts): the candidate's slot;
+    const u32 kv = kv_base + 4 * threadIdx.x;    //   then a loser's winner key / a winner's parent mask, then its idx
+    const u32 hv = kv_base + 4 * KEYS;           // [KEYS] hash set: the slot's vertex ...
+    const u32 hk = hv + 4 * KEYS;                // [KEYS] ... the lowest key that brought it ...
+    const u32 hm = hk + 4 * KEYS;                // [KEYS] bytes ... and the reverse positions of all arcs that brought it
     const u32 tid = threadIdx.x;
     const u32 fb = ex.fb, fe = ex.cnt;
     const u32 level_start = fe;
     const u32 next_depth = ex.depth + 1;
+    const u32 base = ex.base, ot_cnt = ot.cnt; // (side[] is indexed at run time and lives in local memory)
     u32 cnt = fe;
     contact_n = 0;
     const bool sigma_small = sh.sigma_small[e] != 0;
@@ -792,75 +820,93 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
         sh.ws[kW_E_bfs] += ex.pending; // the frontier's adjacency entries
     }
     const uint4 empty4 = make_uint4(kEllEmpty, kEllEmpty, kEllEmpty, kEllEmpty);
-    uint4 *h_mine = reinterpret_cast<uint4 *>(hv) + tid; // this thread clears h_mine[0], [BLOCK], [2 BLOCK], [3 BLOCK] (hv and hk)
+    uint4 *h_mine = reinterpret_cast<uint4 *>(tab + KEYS) + tid; // this thread clears h_mine[0], [BLOCK], [2 BLOCK], [3 BLOCK] (hv and hk)
+    u32 *hm_mine = tab + 3 * KEYS + tid;                         // ... and hm_mine[0], [BLOCK]
 #pragma unroll
     for (int q = 0; q < 4; ++q)
         h_mine[q * BLOCK] = empty4;
+    hm_mine[0] = 0u;
+    hm_mine[BLOCK] = 0u;
     __syncthreads();
     const u32 key0 = tid * W;
     u32 pend = 0;  // degrees of the vertices this thread settled
     u64 gsum = 0;  // saturating sum of sigma[u] over this thread's level edges (= its share of the new sigmas)
     u32 n_lvl = 0;
-    // The frontier is known when the level starts, so a chunk's vertex is loaded two chunks ahead and its row is
-    // requested into L2 one chunk ahead: of the three trips only the labels' (and a short L2 hit for the row)
-    // stay on a chunk's critical path.
-    u32 u_cur = fb + tid < fe ? ld_cg(ex.pp->list + fb + tid) : 0u;
+    // The frontier is known when the level starts, so a chunk's vertex is loaded two chunks ahead and its row one
+    // chunk ahead: of the three trips only the labels' stays on a chunk's critical path.
+    const uint4 *rows = reinterpret_cast<const uint4 *>(p.ell);
+    uint4 a_nxt = empty4, b_nxt = empty4;
+    if (fb + tid < fe) {
+        const u32 u = ld_cg(ex.pp->list + fb + tid);
+        a_nxt = __ldg(rows + 2 * static_cast<u64>(u));
+        b_nxt = __ldg(rows + 2 * static_cast<u64>(u) + 1);
+    }
     u32 u_nxt = fb + BLOCK + tid < fe ? ld_cg(ex.pp->list + fb + BLOCK + tid) : 0u;
+    const unsigned char *pm_in = reinterpret_cast<const unsigned char *>(ex.pp->pm);
     for (u32 c0 = fb; c0 < fe; c0 += BLOCK) {
-        // ---- trips 1 and 2: the chunk's vertices, their rows ----
+        // ---- trips 1 and 2 (of the next chunks): vertices, rows ----
         const u32 i = c0 + tid;
-        uint4 a = empty4, b = empty4;
-        u64 sig_u = 0;
-        if (i < fe) {
-            sig_u = ld_cg(ex.pp->sig + i);
-            const uint4 *row = reinterpret_cast<const uint4 *>(p.ell) + 2 * static_cast<u64>(u_cur);
-            a = __ldg(row);
-            b = __ldg(row + 1);
+        const uint4 a = a_nxt, b = b_nxt;
+        const u64 sig_u = i < fe ? ld_cg(ex.pp->sig + i) : 0;
+        // Entries that lead back to the vertices this one was discovered from: their targets sit one level down,
+        // visited, and a look at their labels -- two levels after they were written, long evicted from L2 -- would
+        // change nothing (sampler.cpp:92,97 both fail).  On a grid that is every second entry.
+        const u32 parents = i < fe ? __ldcg(pm_in + i) : 0u;
+        a_nxt = empty4, b_nxt = empty4;
+        if (i + BLOCK < fe) {
+            a_nxt = __ldg(rows + 2 * static_cast<u64>(u_nxt));
+            b_nxt = __ldg(rows + 2 * static_cast<u64>(u_nxt) + 1);
         }
-        u_cur = u_nxt;
-        if (i + BLOCK < fe)
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const uint4 *>(p.ell) + 2 * static_cast<u64>(u_nxt)));
         u_nxt = i + 2 * BLOCK < fe ? ld_cg(ex.pp->list + i + 2 * BLOCK) : 0u;
-        const int ng = __any_sync(0xffffffffu, b.x != kEllEmpty) ? 2 : 1;
+        // Entries are handled in two groups of four; the second one exists in few warps (a row of more than four
+        // entries), and its code is a copy of the first with other constants -- executed rarely, it costs no
+        // instruction-cache space worth mentioning, while a loop over the groups costs every access a run-time
+        // shift or select.
+        const bool two = __any_sync(0xffffffffu, b.x != kEllEmpty);
         // ---- trip 3: labels; candidates enter the hash set ----
         u32 cand = 0, ccand = 0; // bit k: entry k is unvisited on this side / and visited on the other one
         u32 n_edges = 0;         // level edges of this thread in this chunk
-#pragma unroll 1
-        for (int g = 0; g < ng; ++g) {
-            const u32 en[4] = {g ? b.x : a.x, g ? b.y : a.y, g ? b.z : a.z, g ? b.w : a.w};
+        auto classify = [&](auto G, const uint4 &r) {
+            constexpr int g = decltype(G)::value;
+            const u32 en[4] = {r.x, r.y, r.z, r.w};
             u32 lb[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-                lb[q] = en[q] != kEllEmpty ? ld_cg(lab + (en[q] & kEllIdMask)) : 0u;
+                lb[q] = en[q] != kEllEmpty && !(parents & (1u << (4 * g + q))) ? ld_cg(lab + (en[q] & kEllIdMask)) : 0u;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                if (en[q] == kEllEmpty)
+                if (en[q] == kEllEmpty || (parents & (1u << (4 * g + q))))
                     continue;
                 const u32 v = en[q] & kEllIdMask;
-                const u32 d = lb[q] - ex.base, idx = d >> 1; // label = base + 2 idx + side (stale labels: idx >= 2^30)
+                const u32 d = lb[q] - base, idx = d >> 1; // label = base + 2 idx + side (stale labels: idx >= 2^30)
                 const bool here = ((d ^ static_cast<u32>(e)) & 1u) == 0;
+                const u32 rev_bit = 1u << ((en[q] >> kEllRevShift) & (W - 1));
                 if (here && idx < cnt) {
                     if (idx >= level_start) { // dist[v] == next_depth (sampler.cpp:97), settled by an earlier chunk
                         sat_atomic_add(ex.pp->sig + idx, sig_u, sigma_small);
+                        red_or_u32(ex.pp->pm + (idx >> 2), rev_bit << (8 * (idx & 3)));
                         ++n_edges;
                     }
                     continue;
                 }
-                const u32 key = key0 + 4 * g + q;
                 cand |= 1u << (4 * g + q);
                 u32 slot = (v * 2654435761u) >> (32 - HBITS);
                 for (;;) { // (a chunk has at most KEYS distinct candidates: there is a slot for each)
-                    const u32 prev = atomicCAS(hv + slot, kEllEmpty, v);
+                    const u32 prev = atoms_cas_u32(hv + 4 * slot, kEllEmpty, v);
                     if (prev == kEllEmpty || prev == v)
                         break;
                     slot = (slot + 1) & (KEYS - 1);
                 }
-                atomicMin(hk + slot, key);
-                kv[(4 * g + q) * BLOCK + tid] = slot;
-                if (!here && idx < ot.cnt) // other.visited(v) (sampler.cpp:107)
+                reds_min_u32(hk + 4 * slot, key0 + 4 * g + q);
+                reds_or_u32(hm + (slot & ~3u), rev_bit << (8 * (slot & 3)));
+                sts_u32(kv + 4 * ((4 * g + q) * BLOCK), slot);
+                if (!here && idx < ot_cnt) // other.visited(v) (sampler.cpp:107)
                     ccand |= 1u << (4 * g + q);
             }
-        }
+        };
+        classify(std::integral_constant<int, 0>{}, a);
+        if (two)
+            classify(std::integral_constant<int, 1>{}, b);
         n_edges += __popc(cand);
         n_lvl += n_edges;
         {
@@ -872,21 +918,26 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
         // ---- winners; rank them: inclusive scan over the threads of (winners, contact winners) ----
         __syncthreads(); // the hash set is complete
         u32 win = 0;
-        if (cand) {
-#pragma unroll 1
-            for (int g = 0; g < ng; ++g) {
+        auto resolve = [&](auto G) {
+            constexpr int g = decltype(G)::value;
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if ((cand >> (4 * g + q)) & 1u) {
-                        const u32 key = key0 + 4 * g + q;
-                        const u32 w = hk[kv[(4 * g + q) * BLOCK + tid]];
-                        if (w == key)
-                            win |= 1u << (4 * g + q);
-                        else
-                            kv[(4 * g + q) * BLOCK + tid] = w;
+            for (int q = 0; q < 4; ++q)
+                if (cand & (1u << (4 * g + q))) {
+                    const u32 mine = kv + 4 * ((4 * g + q) * BLOCK);
+                    const u32 slot = lds_u32(mine);
+                    const u32 w = lds_u32(hk + 4 * slot);
+                    if (w == key0 + 4 * g + q) {
+                        win |= 1u << (4 * g + q);
+                        sts_u32(mine, (lds_u32(hm + (slot & ~3u)) >> (8 * (slot & 3))) & 0xffu); // the vertex' parent mask
+                    } else {
+                        sts_u32(mine, w);
                     }
-            }
-        }
+                }
+        };
+        if (cand & 0x0fu)
+            resolve(std::integral_constant<int, 0>{});
+        if (cand & 0xf0u)
+            resolve(std::integral_constant<int, 1>{});
         const u32 packed = __popc(win) | (__popc(win & ccand) << 16);
         u32 incl = packed;
 #pragma unroll
@@ -915,46 +966,54 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
             ex.cnt = cnt; // nothing of this chunk was written
             return false;
         }
-        if (win) {
-            u32 my_idx = cnt + ((incl - packed) & 0xffffu), my_c = contact_n + ((incl - packed) >> 16);
-#pragma unroll 1
-            for (int g = 0; g < ng; ++g) {
-                const u32 en[4] = {g ? b.x : a.x, g ? b.y : a.y, g ? b.z : a.z, g ? b.w : a.w};
+        u32 my_idx = cnt + ((incl - packed) & 0xffffu), my_c = contact_n + ((incl - packed) >> 16);
+        auto settle = [&](auto G, const uint4 &r) {
+            constexpr int g = decltype(G)::value;
+            const u32 en[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if ((win >> (4 * g + q)) & 1u) {
-                        const u32 v = en[q] & kEllIdMask;
-                        if ((ccand >> (4 * g + q)) & 1u) { // contact (sampler.cpp:105-108); the label still holds the other side's idx
-                            const u32 oi = (ld_cg(lab + v) - ex.base) >> 1;
-                            atomicMin(&sh.min_contact, oi);
-                            st_cg(contact + 2 * static_cast<u64>(my_c), my_idx);
-                            st_cg(contact + 2 * static_cast<u64>(my_c) + 1, oi);
-                            ++my_c;
-                        }
-                        st_cg(lab + v, make_label(ex.base, my_idx, e)); // settle (sampler.cpp:93-95)
-                        st_cg(ex.pp->list + my_idx, v);
-                        st_cg(ex.pp->sig + my_idx, sig_u); // the discovering edge's sigma (sampler.cpp:98)
-                        kv[(4 * g + q) * BLOCK + tid] = my_idx;
-                        pend += (en[q] >> kEllDegShift) + 1;
-                        ++my_idx;
+            for (int q = 0; q < 4; ++q)
+                if (win & (1u << (4 * g + q))) {
+                    const u32 v = en[q] & kEllIdMask;
+                    if (ccand & (1u << (4 * g + q))) { // contact (sampler.cpp:105-108); the label still holds the other side's idx
+                        const u32 oi = (ld_cg(lab + v) - base) >> 1;
+                        atomicMin(&sh.min_contact, oi);
+                        st_cg(contact + 2 * static_cast<u64>(my_c), my_idx);
+                        st_cg(contact + 2 * static_cast<u64>(my_c) + 1, oi);
+                        ++my_c;
                     }
-            }
-        }
+                    const u32 mine = kv + 4 * ((4 * g + q) * BLOCK);
+                    st_cg(lab + v, make_label(base, my_idx, e)); // settle (sampler.cpp:93-95)
+                    st_cg(ex.pp->list + my_idx, v);
+                    st_cg(ex.pp->sig + my_idx, sig_u); // the discovering edge's sigma (sampler.cpp:98)
+                    __stcg(reinterpret_cast<unsigned char *>(ex.pp->pm) + my_idx, static_cast<unsigned char>(lds_u32(mine)));
+                    sts_u32(mine, my_idx);
+                    pend += (en[q] >> kEllDegShift) + 1;
+                    ++my_idx;
+                }
+        };
+        if (win & 0x0fu)
+            settle(std::integral_constant<int, 0>{}, a);
+        if (win & 0xf0u)
+            settle(std::integral_constant<int, 1>{}, b);
 #pragma unroll
         for (int q = 0; q < 4; ++q) // (every thread read the hash set before the scan's barrier / shuffles)
             h_mine[q * BLOCK] = empty4;
+        hm_mine[0] = 0u;
+        hm_mine[BLOCK] = 0u;
         __syncthreads(); // settled vertices, kv and the cleared hash set are visible
-        if (cand & ~win) {
-#pragma unroll 1
-            for (int g = 0; g < ng; ++g)
+        auto add_sigma = [&](auto G) { // later discoverers of a vertex settled in this chunk (sampler.cpp:97-98)
+            constexpr int g = decltype(G)::value;
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if (((cand & ~win) >> (4 * g + q)) & 1u) // later discoverers of a vertex settled in this chunk (sampler.cpp:97-98)
-                    {
-                        const u32 w = kv[(4 * g + q) * BLOCK + tid]; // the winner's key
-                        sat_atomic_add(ex.pp->sig + kv[(w & (W - 1)) * BLOCK + w / W], sig_u, sigma_small);
-                    }
-        }
+            for (int q = 0; q < 4; ++q)
+                if (cand & ~win & (1u << (4 * g + q))) {
+                    const u32 w = lds_u32(kv + 4 * ((4 * g + q) * BLOCK)); // the winner's key
+                    sat_atomic_add(ex.pp->sig + lds_u32(kv_base + 4 * ((w & (W - 1)) * BLOCK + w / W)), sig_u, sigma_small);
+                }
+        };
+        if (cand & ~win & 0x0fu)
+            add_sigma(std::integral_constant<int, 0>{});
+        if (cand & ~win & 0xf0u)
+            add_sigma(std::integral_constant<int, 1>{});
         cnt += winners;
         contact_n += ctot;
     }
@@ -1673,6 +1732,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) samp
             sh.sp[k].list = p.list + (slot * 2 + k) * p.cap;
             sh.sp[k].sig = p.sig + (slot * 2 + k) * p.cap;
             sh.sp[k].lvl = p.lvl + (slot * 2 + k) * (p.aux_cap + 2);
+            sh.sp[k].pm = FIXED ? p.pm + (slot * 2 + k) * p.pm_words : nullptr;
         }
         side[k].pp = &sh.sp[k];
         side[k].base = ld_cg(p.hdr + slot * kHdrWords + kHdrBase0); // written by another SM's CTA
@@ -1760,6 +1820,8 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) samp
                 st_cg(side[k].pp->list, root);
                 st_cg(side[k].pp->sig, static_cast<u64>(1));
                 st_cg(side[k].pp->lvl, 0u);
+                if (FIXED)
+                    st_cg(side[k].pp->pm, 0u); // a root has no parents
             }
         }
         if (tid == 0) {
