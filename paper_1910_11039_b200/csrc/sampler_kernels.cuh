@@ -1077,6 +1077,10 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
     constexpr u32 G = BITS ? EBC_PROBE_G : 4; // lanes per item
     constexpr u32 NG = BLOCK / G;             // groups per CTA
     constexpr u32 kItemLen = 4 * G;           // adjacency entries per item
+#ifndef EBC_LONG_ENTRIES
+#define EBC_LONG_ENTRIES 1
+#endif
+    constexpr u32 kLongEntries = EBC_LONG_ENTRIES * BLOCK; // a long row: at least one entry per thread (profiles/r02_probe.txt)
     const u32 tid = threadIdx.x;
     const u32 gid = tid / G, q = tid % G;
     const u32 fb = ex.fb, fe = ex.cnt;
@@ -1094,7 +1098,12 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
         u32 *l_scan = reinterpret_cast<u32 *>(sh.f_key);
         {
             const u64 deg = sh.c_scan[tid + 1] - sh.c_scan[tid];
-            const u32 items = deg ? static_cast<u32>(((sh.c_beg[tid] & 3) + deg + kItemLen - 1) / kItemLen) : 0u;
+            // Long rows are streamed by the whole CTA, one after the other, below; only the others are cut into items.
+            const bool is_long = (sh.c_beg[tid] & 3) + deg >= kLongEntries;
+            const u32 long_ballot = __ballot_sync(0xffffffffu, is_long);
+            if (lane_id() == 0)
+                sh.warp_cnt2[tid >> 5] = long_ballot;
+            const u32 items = deg && !is_long ? static_cast<u32>(((sh.c_beg[tid] & 3) + deg + kItemLen - 1) / kItemLen) : 0u;
             u32 inc = items;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -1115,6 +1124,96 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
             if (tid == 0)
                 l_scan[0] = 0;
             __syncthreads();
+        }
+        // Tests the four entries `cur` (bit k of `valid`: entry k belongs to the row) of row `row_c` of the chunk;
+        // rel0_c = index in the row of the first of the four (negative where the 16-byte group starts before the row).
+        auto test_quad = [&](const uint4 &cur, u32 valid, u32 row_c, int rel0_c) {
+            const u32 vv[4] = {cur.x, cur.y, cur.z, cur.w};
+            u32 need = 0; // bit k: entry k must be looked up in global memory
+            if (BITS) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const u32 h = vv[k] & (VisitedFilter<BLOCK>::kPositions - 1);
+                    need |= ((vf[h >> 5] >> (h & 31)) & 1u) << k; // clear: certainly unvisited on both sides
+                }
+                need &= valid;
+                fresh += __popc(valid & ~need);
+            } else {
+                need = valid;
+            }
+            if (need) {
+                u64 both[4]; // bitmap word of both sides, or (labels) the 4-byte label
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    both[k] = 0;
+                    if ((need >> k) & 1u)
+                        both[k] = BITS ? ld_cg(reinterpret_cast<const u64 *>(bits) + (vv[k] >> 5))
+                                       : static_cast<u64>(ld_cg(lab + vv[k]));
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (!((need >> k) & 1u))
+                        continue;
+                    u32 oi;
+                    if (BITS) {
+                        if ((static_cast<u32>(both[k] >> (32 * e)) >> (vv[k] & 31)) & 1u)
+                            continue; // visited before this level
+                        fresh += 1;
+                        if (!((static_cast<u32>(both[k] >> (32 * (1 - e))) >> (vv[k] & 31)) & 1u))
+                            continue; // not a contact
+                        // The other side's bit already says "contact"; its idx is only needed for the record
+                        // and is fetched for all contact edges at once after the scan.
+                        oi = 0;
+                    } else {
+                        const u32 lbl = static_cast<u32>(both[k]);
+                        if (label_idx(lbl, ex.base, e) < ex.cnt)
+                            continue; // visited before this level
+                        fresh += 1;
+                        oi = label_idx(lbl, ex.base, 1 - e);
+                    }
+                    if (oi < ot.cnt) {
+                        if (!BITS)
+                            atomicMin(&sh.min_contact, oi);
+                        const u32 pos = atomicAdd(&sh.edge_cnt, 1u);
+                        if (pos < edge_cap)
+                            record_contact_edge(edges, pos, (c0 - fb) + row_c, static_cast<u32>(rel0_c + k), vv[k], oi,
+                                                sh.c_sig[row_c]);
+                    }
+                }
+            }
+        };
+        // ---- long rows: thread t takes the 16-byte groups t, t + BLOCK, ... of the row; no search, and only the
+        // row's first and last group are partial ----
+#pragma unroll 1
+        for (int w = 0; w < BLOCK / 32; ++w) {
+            u32 mask = sh.warp_cnt2[w];
+            while (mask) {
+                const u32 r = 32u * w + (__ffs(mask) - 1);
+                mask &= mask - 1;
+                const u64 beg = sh.c_beg[r];
+                const u32 head = static_cast<u32>(beg & 3);
+                const u32 span = head + static_cast<u32>(sh.c_scan[r + 1] - sh.c_scan[r]); // (a row has < 2^32 entries)
+                const u32 nq = (span + 3) >> 2;
+                const uint4 *quads = reinterpret_cast<const uint4 *>(p.targets + (beg - head));
+                u32 qi = tid;
+                uint4 cur = make_uint4(0, 0, 0, 0);
+                if (qi < nq)
+                    cur = __ldg(quads + qi);
+                while (qi < nq) {
+                    const u32 qn = qi + BLOCK;
+                    uint4 nxt = make_uint4(0, 0, 0, 0);
+                    if (qn < nq)
+                        nxt = __ldg(quads + qn);
+                    u32 valid = 0xfu;
+                    if (qi == 0)
+                        valid = (0xfu << head) & 0xfu;
+                    if (qi == nq - 1)
+                        valid &= 0xfu >> (4 * nq - span);
+                    test_quad(cur, valid, r, static_cast<int>(4 * qi) - static_cast<int>(head));
+                    cur = nxt;
+                    qi = qn;
+                }
+            }
         }
         const u32 n_items = l_scan[BLOCK];
         // Iteration i requests the entries of item i and tests those requested by iteration i - 1 (nothing in
@@ -1152,65 +1251,12 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
                 nxt = ldg_targets4(p.targets + first);
             }
             if (have_c) {
-                const u32 vv[4] = {cur.x, cur.y, cur.z, cur.w};
                 // entries [lo_k, hi_k) of the four belong to the row
                 const int lo_k = rel0_c < 0 ? -rel0_c : 0;
                 const int left = static_cast<int>(deg_c) - rel0_c;
                 const int hi_k = left < 4 ? left : 4;
-                u32 need = 0; // bit k: entry k must be looked up in global memory
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    if (k < lo_k || k >= hi_k)
-                        continue;
-                    if (BITS) {
-                        const u32 h = vv[k] & (VisitedFilter<BLOCK>::kPositions - 1);
-                        if (((vf[h >> 5] >> (h & 31)) & 1u) == 0) { // certainly unvisited on both sides
-                            fresh += 1;
-                            continue;
-                        }
-                    }
-                    need |= 1u << k;
-                }
-                if (need) {
-                    u64 both[4]; // bitmap word of both sides, or (labels) the 4-byte label
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        both[k] = 0;
-                        if ((need >> k) & 1u)
-                            both[k] = BITS ? ld_cg(reinterpret_cast<const u64 *>(bits) + (vv[k] >> 5))
-                                           : static_cast<u64>(ld_cg(lab + vv[k]));
-                    }
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        if (!((need >> k) & 1u))
-                            continue;
-                        u32 oi;
-                        if (BITS) {
-                            if ((static_cast<u32>(both[k] >> (32 * e)) >> (vv[k] & 31)) & 1u)
-                                continue; // visited before this level
-                            fresh += 1;
-                            if (!((static_cast<u32>(both[k] >> (32 * (1 - e))) >> (vv[k] & 31)) & 1u))
-                                continue; // not a contact
-                            // The other side's bit already says "contact"; its idx is only needed for the record
-                            // and is fetched for all contact edges at once after the scan.
-                            oi = 0;
-                        } else {
-                            const u32 lbl = static_cast<u32>(both[k]);
-                            if (label_idx(lbl, ex.base, e) < ex.cnt)
-                                continue; // visited before this level
-                            fresh += 1;
-                            oi = label_idx(lbl, ex.base, 1 - e);
-                        }
-                        if (oi < ot.cnt) {
-                            if (!BITS)
-                                atomicMin(&sh.min_contact, oi);
-                            const u32 pos = atomicAdd(&sh.edge_cnt, 1u);
-                            if (pos < edge_cap)
-                                record_contact_edge(edges, pos, (c0 - fb) + row_c, static_cast<u32>(rel0_c + k), vv[k], oi,
-                                                    sh.c_sig[row_c]);
-                        }
-                    }
-                }
+                if (hi_k > lo_k)
+                    test_quad(cur, ((1u << hi_k) - 1u) & ~((1u << lo_k) - 1u), row_c, rel0_c);
             }
             if (!have_n)
                 break;
