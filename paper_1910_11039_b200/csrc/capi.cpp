@@ -346,7 +346,9 @@ ebc_status ebc_run(const ebc_graph *g, const ebc_run_config *cfg, ebc_result **o
         if (g->g.n < 2)
             throw ContractViolation("run_pipeline: need at least two vertices");
         const auto t0 = std::chrono::steady_clock::now();
-        CudaSampler sampler(g->g, sampler_options(cfg));
+        SamplerOptions so = sampler_options(cfg);
+        so.short_launches = true; // epochs of some 10^4 samples
+        CudaSampler sampler(g->g, so);
         const double upload_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         CudaBackend backend(sampler);
         auto h = std::make_unique<ebc_result>();

@@ -1109,7 +1109,11 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
         // (42.7 / 22.3 M samples/s; 64x2 29.4 / 18.4 M), R-MAT-20 64x2 (9.0 M; 128x4 8.1 M), R-MAT-22 128x4,
         // R-MAT-24 256x4 (2.03 M; 512x2 1.55 M), R-MAT-26 512x4 (742 k; 256x4 614 k, 263 slots either way).
         if (m.hub_graph) {
-            const int lg = m.arcs < (u64{1} << 23) ? 0 : m.arcs < (u64{1} << 26) ? 1 : m.arcs < (u64{1} << 28) ? 2
+            // (one warp per sample is the fastest shape up to 2^25 arcs when a launch holds many samples per slot --
+            // config 2, 524 288-sample launches: 13.1 M samples/s against 10.9 M with two warps -- but not on the
+            // 35 840-sample epochs of its pipeline run: 13.4 ms against 12.0 ms of adaptive phase)
+            const u64 one_warp_below = opt.short_launches ? (u64{1} << 23) : (u64{1} << 25);
+            const int lg = m.arcs < one_warp_below ? 0 : m.arcs < (u64{1} << 26) ? 1 : m.arcs < (u64{1} << 28) ? 2
                            : m.arcs < (u64{1} << 30) ? 3 : 4;
             static const u32 kBlock[5] = {32, 64, 128, 256, 512}, kItems[5] = {2, 2, 4, 4, 4};
             m.block = opt.block_threads ? opt.block_threads : kBlock[lg];
