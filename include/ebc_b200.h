@@ -174,6 +174,10 @@ typedef struct ebc_run_config {
                                 * neighbouring vertices, so the surface of a search ball covers few cache lines.
                                 * Purely internal: row order, discovery order, samples, counters and every id
                                 * that crosses this interface stay those of the caller's graph. */
+    int reserved_sms;          /* SMs the sampling kernel leaves empty so that the frame all-reduce of epoch e (NCCL's
+                                * kernel) runs BESIDE the sampling of epoch e+1 instead of behind it -- the overlap
+                                * of aggregation with sampling (engine.cpp:145-163).  0 = auto: 8 when world_size > 1
+                                * and overlap != 0, else none; -1 = none; k > 0 = k SMs. */
 } ebc_run_config;
 
 EBC_API void ebc_run_config_default(ebc_run_config *cfg);

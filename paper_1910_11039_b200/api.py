@@ -257,13 +257,15 @@ class RunConfig:
     items_per_thread: int = 0
     materialize_final_level: bool = False
     renumber: int = 0  # device-side numbering: 0 auto, -1 never, 1 degree classes (hubs), 2 neighbourhood clusters
+    reserved_sms: int = 0  # SMs left to the frame all-reduce: 0 auto (8 when world_size > 1), -1 none, k > 0
 
     def to_c(self) -> _CRunConfig:
         c = _CRunConfig()
         _capi.load().ebc_run_config_default(C.byref(c))
         for f in ("eps", "delta", "seed", "bound", "allocator", "omega_override", "calib_samples",
                   "diameter_sweeps", "vertex_diameter_override", "epoch_samples", "max_epochs", "device",
-                  "rank", "world_size", "block_threads", "slots", "slot_capacity", "items_per_thread", "renumber"):
+                  "rank", "world_size", "block_threads", "slots", "slot_capacity", "items_per_thread", "renumber",
+                  "reserved_sms"):
             setattr(c, f, getattr(self, f))
         c.overlap = int(self.overlap)
         c.materialize_final_level = int(self.materialize_final_level)

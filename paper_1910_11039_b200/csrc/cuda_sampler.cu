@@ -799,6 +799,7 @@ struct CudaSampler::Impl {
     u64 probe_min_slots = 512;
     u64 probe_growth_x4 = 8; // the frontier's pending edges at least doubled
     bool hub_graph = false; // max degree >= 1024: visited bitmaps, direction-optimising BFS
+    u32 reserved_sms = 0;   // SMs the main pass leaves empty (SamplerOptions::reserved_sms)
     int numbering = 0;      // 0 none, 1 degree classes, 2 neighbourhood clusters
     SlotArrays small, big;
     u32 *d_frame[2] = {nullptr, nullptr};
@@ -977,8 +978,14 @@ struct CudaSampler::Impl {
         p.ring_size = static_cast<u32>(small.slots);
         p.ring_pos = d_ring_pos;
         const u32 grid = static_cast<u32>(std::min<u64>(small.slots, count));
+        p.reserved_sms = reserved_sms;
         launch_sample_dispatch(block, items, p, grid, st);
         ++launches;
+        if (reserved_sms) { // whatever the CTAs that left have not taken (normally nothing: an empty launch)
+            p.reserved_sms = 0;
+            launch_sample_dispatch(block, items, p, std::min<u32>(grid, static_cast<u32>(sm_count)), st);
+            ++launches;
+        }
         if (small.cap < n) { // capacity overflow is impossible when cap == n
             // the large slots are bound to blockIdx: re-run passes of the two lanes must not overlap
             EBC_CUDA(cudaStreamWaitEvent(st, ev_rerun[1 - lane], 0));
@@ -1089,6 +1096,11 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
 
     // ---- launch shape ----
     m.flags = opt.materialize_final_level ? kFlagMaterializeFinal : 0u;
+    if (const char *env = std::getenv("EBC_RESERVED_SMS")) // test / tuning hook
+        m.reserved_sms = static_cast<u32>(std::atoi(env));
+    else
+        m.reserved_sms = opt.reserved_sms;
+    m.reserved_sms = std::min<u32>(m.reserved_sms, m.sm_count > 1 ? static_cast<u32>(m.sm_count) - 1 : 0);
     std::uint64_t max_degree = 0;
     {
         // Visited bitmaps pay off when single rows are long enough to be probed (hub graphs); on

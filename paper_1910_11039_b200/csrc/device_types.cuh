@@ -119,6 +119,10 @@ struct SamplerParams {
     u32 *ring;
     u32 ring_size;
     unsigned long long *ring_pos;
+    // Main pass only: CTAs that land on one of the last `reserved_sms` SMs leave at once, so those SMs stay empty for
+    // a kernel of another stream (NCCL's all-reduce of the previous epoch's frame).  A second, small launch without
+    // reservation takes whatever tickets are left, which makes the result independent of where CTAs were placed.
+    u32 reserved_sms;
 };
 
 } // namespace ebc

@@ -1742,6 +1742,13 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) samp
     if (BITS)
         for (u32 i = tid; i < VisitedFilter<BLOCK>::kWords; i += BLOCK)
             vf[i] = 0;
+    if (p.reserved_sms) { // (before a slot is taken; uniform over the CTA)
+        u32 smid, nsmid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        asm volatile("mov.u32 %0, %%nsmid;" : "=r"(nsmid));
+        if (smid + p.reserved_sms >= nsmid)
+            return;
+    }
     // Slot hand-out.  Launches of consecutive epochs overlap on two streams, so a CTA cannot own
     // slot blockIdx.x: it takes a free slot id from a ring (at most ring_size CTAs are resident, each
     // holds one slot, so a free one is always there or about to be returned) and puts it back at exit.
