@@ -175,9 +175,12 @@ typedef struct ebc_run_config {
                                 * Purely internal: row order, discovery order, samples, counters and every id
                                 * that crosses this interface stay those of the caller's graph. */
     int reserved_sms;          /* SMs the sampling kernel leaves empty so that the frame all-reduce of epoch e (NCCL's
-                                * kernel) runs BESIDE the sampling of epoch e+1 instead of behind it -- the overlap
-                                * of aggregation with sampling (engine.cpp:145-163).  0 = auto: 8 when world_size > 1
-                                * and overlap != 0, else none; -1 = none; k > 0 = k SMs. */
+                                * kernel) finds room BESIDE the sampling of epoch e+1 at once -- the overlap of
+                                * aggregation with sampling (engine.cpp:145-163).  0 = auto: 4 when world_size > 1 and
+                                * overlap != 0 (ebc_nccl_comm_create keeps NCCL to as many CTAs), else none;
+                                * -1 = none; k > 0 = k SMs.  Costs k/148 of the sampling rate; without it a kernel
+                                * of NCCL's footprint waited 40 us for room at the epoch switch
+                                * (tools/overlap_timeline.py, profiles/r02_overlap_timeline.txt). */
 } ebc_run_config;
 
 EBC_API void ebc_run_config_default(ebc_run_config *cfg);

@@ -257,7 +257,7 @@ class RunConfig:
     items_per_thread: int = 0
     materialize_final_level: bool = False
     renumber: int = 0  # device-side numbering: 0 auto, -1 never, 1 degree classes (hubs), 2 neighbourhood clusters
-    reserved_sms: int = 0  # SMs left to the frame all-reduce: 0 auto (8 when world_size > 1), -1 none, k > 0
+    reserved_sms: int = 0  # SMs left to the frame all-reduce: 0 auto (4 when world_size > 1), -1 none, k > 0
 
     def to_c(self) -> _CRunConfig:
         c = _CRunConfig()

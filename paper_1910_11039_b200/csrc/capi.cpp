@@ -87,7 +87,7 @@ SamplerOptions sampler_options(const ebc_run_config *cfg) {
         o.renumber = cfg->renumber;
         // the frame all-reduce of epoch e runs beside the sampling of epoch e+1 (see ebc_b200.h)
         o.reserved_sms = cfg->reserved_sms > 0 ? static_cast<std::uint32_t>(cfg->reserved_sms)
-                         : cfg->reserved_sms == 0 && cfg->world_size > 1 && cfg->overlap ? 8u : 0u;
+                         : cfg->reserved_sms == 0 && cfg->world_size > 1 && cfg->overlap ? 4u : 0u;
     }
     return o;
 }
@@ -780,7 +780,7 @@ ebc_status ebc_nccl_comm_create(const void *id, int rank, int world_size, int de
             throw ConfigError("ebc_nccl_comm_create: need 0 <= rank < world_size");
         // The all-reduce runs beside the sampling kernel on the SMs that kernel leaves empty (ebc_run_config.reserved_sms):
         // keep NCCL's kernel to as many CTAs, unless the caller has chosen otherwise.
-        setenv("NCCL_MAX_CTAS", "8", /*overwrite=*/0);
+        setenv("NCCL_MAX_CTAS", "4", /*overwrite=*/0);
         const NcclApi &a = nccl_api();
         set_device_or_throw(device);
         NcclApi::UniqueId uid;

@@ -800,6 +800,8 @@ struct CudaSampler::Impl {
     u64 probe_growth_x4 = 8; // the frontier's pending edges at least doubled
     bool hub_graph = false; // max degree >= 1024: visited bitmaps, direction-optimising BFS
     u32 reserved_sms = 0;   // SMs the main pass leaves empty (SamplerOptions::reserved_sms)
+    int per_sm = 0;         // resident CTAs per SM of the sampling kernel
+    u32 *d_started = nullptr; // [lane] see SamplerParams::started
     int numbering = 0;      // 0 none, 1 degree classes, 2 neighbourhood clusters
     SlotArrays small, big;
     u32 *d_frame[2] = {nullptr, nullptr};
@@ -978,14 +980,15 @@ struct CudaSampler::Impl {
         p.ring_size = static_cast<u32>(small.slots);
         p.ring_pos = d_ring_pos;
         const u32 grid = static_cast<u32>(std::min<u64>(small.slots, count));
-        p.reserved_sms = reserved_sms;
+        const u32 held = reserved_sms * static_cast<u32>(per_sm); // CTAs the reserved SMs hold
+        if (reserved_sms && grid > 2 * held) { // (a launch that small leaves room anyway)
+            p.reserved_sms = reserved_sms;
+            p.reserve_target = grid - held;
+            p.started = d_started + lane;
+            EBC_CUDA(cudaMemsetAsync(p.started, 0, sizeof(u32), st));
+        }
         launch_sample_dispatch(block, items, p, grid, st);
         ++launches;
-        if (reserved_sms) { // whatever the CTAs that left have not taken (normally nothing: an empty launch)
-            p.reserved_sms = 0;
-            launch_sample_dispatch(block, items, p, std::min<u32>(grid, static_cast<u32>(sm_count)), st);
-            ++launches;
-        }
         if (small.cap < n) { // capacity overflow is impossible when cap == n
             // the large slots are bound to blockIdx: re-run passes of the two lanes must not overlap
             EBC_CUDA(cudaStreamWaitEvent(st, ev_rerun[1 - lane], 0));
@@ -1168,6 +1171,7 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
     if (const char *env = std::getenv("EBC_ELL"))
         want_ell = want_ell && std::atoi(env) != 0;
     const int per_sm = occupancy_for(m.block, m.items, want_ell);
+    m.per_sm = per_sm;
     lap("occupancy query");
     if (per_sm < 1)
         throw CudaError("sampling kernel does not fit on an SM");
@@ -1221,6 +1225,7 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
     m.d_wide = dev_alloc<u64>(g.n + 1);
     EBC_CUDA(cudaMemsetAsync(m.d_S, 0, (g.n + 1) * 8, m.s_sample));
     m.d_ticket = dev_alloc<unsigned long long>(4);
+    m.d_started = dev_alloc<u32>(2);
     {
         m.d_ring = dev_alloc<u32>(m.small.slots);
         std::vector<u32> ids(m.small.slots);
@@ -1280,6 +1285,7 @@ CudaSampler::Impl::~Impl() {
     dev_free(m.d_S);
     dev_free(m.d_wide);
     dev_free(m.d_ticket);
+    dev_free(m.d_started);
     dev_free(m.d_ring);
     dev_free(m.d_ring_pos);
     dev_free(m.d_work);

@@ -119,10 +119,14 @@ struct SamplerParams {
     u32 *ring;
     u32 ring_size;
     unsigned long long *ring_pos;
-    // Main pass only: CTAs that land on one of the last `reserved_sms` SMs leave at once, so those SMs stay empty for
-    // a kernel of another stream (NCCL's all-reduce of the previous epoch's frame).  A second, small launch without
-    // reservation takes whatever tickets are left, which makes the result independent of where CTAs were placed.
+    // Main pass only: CTAs that land on one of the last `reserved_sms` SMs do not sample.  They wait until
+    // `reserve_target` CTAs of this launch have started on the other SMs -- all the grid minus what the reserved
+    // SMs hold -- and leave; from then on those SMs are empty for a kernel of another stream (NCCL's all-reduce of
+    // the previous epoch's frame).  (Leaving at once would drain the whole grid through the reserved SMs while the
+    // other SMs are still held by the previous epoch's kernel.)
     u32 reserved_sms;
+    u32 reserve_target;
+    u32 *started; // CTAs of this launch that started on an SM that is not reserved
 };
 
 } // namespace ebc

@@ -1746,8 +1746,23 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) samp
         u32 smid, nsmid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
         asm volatile("mov.u32 %0, %%nsmid;" : "=r"(nsmid));
-        if (smid + p.reserved_sms >= nsmid)
-            return;
+        if (smid + p.reserved_sms >= nsmid) {
+            // A reserved SM: hold the place until the rest of the grid is running elsewhere, then leave.  Should that
+            // never happen (about a second), sample here after all: progress does not depend on CTA placement.
+            if (tid == 0) {
+                const long long t0 = clock64();
+                u32 seen;
+                while ((seen = *reinterpret_cast<volatile u32 *>(p.started)) < p.reserve_target && clock64() - t0 < (1ll << 31))
+                    __nanosleep(2000);
+                sh.bcast[2] = seen >= p.reserve_target ? 1u : 0u;
+            }
+            __syncthreads();
+            if (sh.bcast[2])
+                return;
+            __syncthreads();
+        } else if (tid == 0) {
+            atomicAdd(p.started, 1u);
+        }
     }
     // Slot hand-out.  Launches of consecutive epochs overlap on two streams, so a CTA cannot own
     // slot blockIdx.x: it takes a free slot id from a ring (at most ring_size CTAs are resident, each
