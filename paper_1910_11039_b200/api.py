@@ -453,7 +453,8 @@ class Sampler:
         _check(_capi.load().ebc_sampler_info(self._h, _p(w, _capi.u64p)))
         return dict(slots=int(w[0]), block_threads=int(w[1]), slot_capacity=int(w[2]),
                     device_bytes=int(w[3]), sm_count=int(w[4]), launches=int(w[5]) & ((1 << 48) - 1),
-                    renumbered=(int(w[5]) >> 48) & 0xFF, items_per_thread=int(w[5]) >> 56)
+                    renumbered=(int(w[5]) >> 48) & 0xF, fixed_rows=bool((int(w[5]) >> 52) & 1),
+                    items_per_thread=int(w[5]) >> 56)
 
     def stream(self) -> int:
         p = C.c_void_p()

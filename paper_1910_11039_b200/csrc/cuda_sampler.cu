@@ -1561,7 +1561,7 @@ void CudaSampler::info(std::uint64_t *out) {
     out[3] = m.small.bytes + m.big.bytes + m.graph_bytes + (m.n + 1) * (4 * 2 + 8 + 8 + 16);
     out[4] = static_cast<std::uint64_t>(m.sm_count);
     out[5] = (m.launches & ((std::uint64_t{1} << 48) - 1)) | (static_cast<std::uint64_t>(m.numbering) << 48) |
-             (static_cast<std::uint64_t>(m.items) << 56);
+             (static_cast<std::uint64_t>(m.d_ell ? 1 : 0) << 52) | (static_cast<std::uint64_t>(m.items) << 56);
 }
 
 void *CudaSampler::stream_handle() { return impl_->s_sample; }

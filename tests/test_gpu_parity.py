@@ -259,3 +259,66 @@ def test_reserved_sms_do_not_change_results(monkeypatch, reserved):
     assert np.array_equal(s.read_frame(0), o.accumulate(SEED, 100, 20000))
     assert np.array_equal(s.read_frame(1), o.accumulate(SEED, 30000, 20000))
     s.close()
+
+
+def _ring_lattice(n, chords=True):
+    """Every vertex tied to i+1, i+2, i+5 (degree 6) plus a few chords: rows of five to eight entries, no hubs."""
+    src = np.concatenate([np.arange(n)] * 3)
+    dst = np.concatenate([(np.arange(n) + k) % n for k in (1, 2, 5)])
+    if chords:
+        c = np.arange(0, n, 37)
+        src, dst = np.concatenate([src, c]), np.concatenate([dst, (c * 7 + n // 3) % n])
+    from helpers import csr_from_edges
+    return csr_from_edges(n, src, dst)
+
+
+@pytest.mark.parametrize("block", [32, 64, 128])
+def test_fixed_stride_rows_samples_state_and_work_counters(block, monkeypatch):
+    """Graphs of maximum degree <= 8 take the fixed-stride-row kernel (expand_level_ell: both entry groups, hash-set
+    dedup, parent masks, degrees carried in the entries).  Samples, paths, dist / sigma arrays and ALL work counters
+    equal the oracle's -- that kernel settles every level, so V_set / F_chk / E_lvl need no materialize flag -- and
+    the general kernel (EBC_ELL=0) gives the same records."""
+    off, tg = _ring_lattice(3000)
+    deg = np.diff(off)
+    assert deg.max() <= 8 and deg.max() >= 7 and deg.min() >= 6
+    g = ebc.Graph.from_csr(off, tg)
+    o = Oracle(off, tg)
+    s, _ = check_samples((off, tg), 500, ebc.RunConfig(block_threads=block, slots=8))
+    assert s.info()["fixed_rows"]
+    s.close()
+    s = ebc.Sampler(g, ebc.RunConfig(block_threads=block))
+    s.sample(SEED, 1000, 6000)
+    assert np.array_equal(s.read_frame(0), o.accumulate(SEED, 1000, 6000))
+    w, ow = s.work(), o.work()
+    for i, k in enumerate(ebc.WORK_NAMES[:11]):
+        assert w[k] == int(ow[i]), k
+    rec_a, paths_a = s.sample_debug(SEED, 0, 300, frame=1, path_stride=32)
+    s.close()
+    s1 = ebc.Sampler(g, ebc.RunConfig(block_threads=block, slots=1))
+    for i in range(10):
+        s1.sample_debug(SEED, i, 1)
+        o.sample(SEED, i)
+        for side in (0, 1):
+            d, sg = s1.last_state(side)
+            od, osg = o.last_state(side)
+            assert np.array_equal(d, od) and np.array_equal(sg, osg), (i, side)
+    s1.close()
+    monkeypatch.setenv("EBC_ELL", "0")
+    s = ebc.Sampler(g, ebc.RunConfig(block_threads=block))
+    assert not s.info()["fixed_rows"]
+    rec_b, paths_b = s.sample_debug(SEED, 0, 300, frame=1, path_stride=32)
+    for f in ("s", "t", "dist", "meet", "meet_count", "draws", "path_len", "weight_lo", "weight_hi"):
+        assert np.array_equal(rec_a[f], rec_b[f]), f
+    assert np.array_equal(paths_a, paths_b)
+    s.close()
+
+
+def test_fixed_stride_rows_need_a_symmetric_graph():
+    """An arc without its reverse has no reverse position to record: the sampler notices while it builds the rows and
+    runs the general kernel instead (validate=0 adopts the CSR as it is)."""
+    off = np.array([0, 1, 3, 4], dtype=np.uint64)  # 0 -> 1, 1 -> {0, 2}, 2 -> 0 (2 -> 1 is missing)
+    tg = np.array([1, 0, 2, 0], dtype=np.uint32)
+    g = ebc.Graph.from_csr(off, tg, validate=False)
+    s = ebc.Sampler(g, ebc.RunConfig(block_threads=32, slots=2))
+    assert not s.info()["fixed_rows"]
+    s.close()
