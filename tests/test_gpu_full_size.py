@@ -69,7 +69,7 @@ def _check(g, samples, spot, stride, shapes, block_first=None, block_count=0, ex
 def test_config2_rmat20_full_size():
     g = ebc.gen_rmat(20, 16, seed=2).largest_connected_component()
     assert (g.num_vertices, g.num_edges) == (645739, 15700555)
-    f = _check(g, 107520, 300, 8, [(0, 0, 0), (128, 4, 0), (256, 4, 256)], expect_default=(64, 2))
+    f = _check(g, 107520, 300, 8, [(0, 0, 0), (64, 2, 0), (256, 4, 256)], expect_default=(32, 2))
     # the whole run's frame, word for word (was tools/soak_config2.py)
     assert np.array_equal(f, oracle_frame(g.offsets, g.targets, SEED, 0, 107520))
 
