@@ -1129,7 +1129,7 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
             // 35 840-sample epochs of its pipeline run: 13.4 ms against 12.0 ms of adaptive phase)
             const u64 one_warp_below = opt.short_launches ? (u64{1} << 23) : (u64{1} << 25);
             const int lg = m.arcs < one_warp_below ? 0 : m.arcs < (u64{1} << 26) ? 1 : m.arcs < (u64{1} << 28) ? 2
-                           : m.arcs < (u64{1} << 30) ? 3 : 4;
+                           : m.arcs < (u64{1} << 32) ? 3 : 4;
             static const u32 kBlock[5] = {32, 64, 128, 256, 512}, kItems[5] = {2, 2, 4, 4, 4};
             m.block = opt.block_threads ? opt.block_threads : kBlock[lg];
             m.items = opt.items_per_thread ? opt.items_per_thread : kItems[lg];
@@ -1175,8 +1175,10 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
     lap("occupancy query");
     if (per_sm < 1)
         throw CudaError("sampling kernel does not fit on an SM");
+    // (hub graphs: the probe never settles a large final level, a side rarely holds 10^5 vertices, and with n/32
+    // config 5 fits 592 slots of 256 threads: 1.71 M samples/s, n/16 1.58 M, n/8 with the 515 slots that fit 1.47 M)
     u64 cap = opt.slot_capacity ? std::min<u64>(opt.slot_capacity, g.n)
-                                : std::min<u64>(g.n, std::max<u64>(u64{1} << 17, g.n / 8));
+                                : std::min<u64>(g.n, std::max<u64>(u64{1} << 17, m.hub_graph ? g.n / 32 : g.n / 8));
     // (While large final levels were still settled, n/6 instead of n/4 cost 10x throughput through the re-run
     // path on R-MAT graphs; now that they are only scanned, n/16 runs as fast as n/4 on R-MAT-20/24/26 --
     // profiles/r01_capacity_sweep.txt.  n/8 lets config 5 keep two 512-thread CTAs per SM.)

@@ -9,7 +9,7 @@ seconds, so parity is checked through
  * word-for-word frames: the epoch frame of a contiguous block of sample indices equals the oracle's
    (config 2: the whole run of 107 520 samples; configs 3-5: a 2 000 / 1 000-sample block);
  * the full config-2 pipeline against an oracle replay of the same epochs (counters, tau, stop epoch).
-Configs 4 and 5 run with their DEFAULT launch shapes (256x4 / 512x4) and slot counts.
+Configs 4 and 5 run with their DEFAULT launch shape (256x4) and slot counts.
 """
 import numpy as np
 import pytest
@@ -114,11 +114,11 @@ def test_config4_rmat24_full_size():
 
 
 def test_config5_rmat26_full_size():
-    """BASELINE configs[4]: Kronecker/R-MAT scale 26 (graph seed 5, 2.1 * 10^9 arcs), default launch shape 512x4."""
+    """BASELINE configs[4]: Kronecker/R-MAT scale 26 (graph seed 5, 2.1 * 10^9 arcs), default launch shape 256x4."""
     g = ebc.gen_rmat_device(26, 16, seed=5, take_lcc=True)
     assert g.num_vertices > 30_000_000 and 2 * g.num_edges > 2_000_000_000
-    _check(g, 20480, 300, 8, [(0, 0, 0), (256, 4, 64)], block_first=3_000_000, block_count=1000,
-           expect_default=(512, 4))
+    _check(g, 20480, 300, 8, [(0, 0, 0), (512, 4, 64)], block_first=3_000_000, block_count=1000,
+           expect_default=(256, 4))
 
 
 def test_config1_er_full_run_twice_identical():
