@@ -1204,6 +1204,10 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
                     uint4 nxt = make_uint4(0, 0, 0, 0);
                     if (qn < nq)
                         nxt = __ldg(quads + qn);
+                    // the row is a stream from DRAM: ask L2 for the sector three rounds ahead (config 4 +5 %; six
+                    // rounds ahead +4 %; config 2, whose rows mostly sit in L2, +0)
+                    if (qi + 3 * BLOCK < nq && (tid & 1) == 0) // (one request per 32-byte sector)
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(quads + qi + 3 * BLOCK));
                     u32 valid = 0xfu;
                     if (qi == 0)
                         valid = (0xfu << head) & 0xfu;
