@@ -1299,8 +1299,25 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
 template <int BLOCK, int ITEMS>
 __device__ u32 meet_from_edges(const u32 *edges, u32 m, u32 olo, u32 ohi, u32 *meetbuf,
                                BlockShared<BLOCK, ITEMS> &sh) {
-    constexpr int PER = FinalEdgeCap<BLOCK>::value / BLOCK > 0 ? FinalEdgeCap<BLOCK>::value / BLOCK : 1;
+    constexpr int CAP = FinalEdgeCap<BLOCK>::value;
+    constexpr int PER = CAP / BLOCK > 0 ? CAP / BLOCK : 1;
+    // Edges of one vertex find each other through hash buckets (a chained table over the edge indices: head[] by
+    // bucket, next[] by edge), members rank themselves against the dense list of members only: both passes used to
+    // walk all m edges per edge -- 2 m^2 / BLOCK steps per thread, a fifth of a sample on hub graphs.  The tables
+    // live in the chunk arrays, which nobody uses between the level loop and the next sample.
+    using Shared = BlockShared<BLOCK, ITEMS>;
+    static_assert(CAP <= 0xffff && sizeof(u32) * CAP + sizeof(unsigned short) * CAP <=
+                                       sizeof(sh.c_beg) + sizeof(sh.c_scan) + sizeof(sh.c_sig) &&
+                      offsetof(Shared, c_sig) + sizeof(sh.c_sig) - offsetof(Shared, c_beg) ==
+                          sizeof(sh.c_beg) + sizeof(sh.c_scan) + sizeof(sh.c_sig),
+                  "bucket heads and chains alias the chunk arrays");
+    u32 *head = reinterpret_cast<u32 *>(sh.c_beg);                        // [CAP] first edge of the bucket, or kNone
+    unsigned short *next = reinterpret_cast<unsigned short *>(head + CAP); // [CAP] next edge of the same bucket
+    unsigned short *dense = reinterpret_cast<unsigned short *>(sh.c_beg); // [CAP] afterwards: the members' edge indices
+    constexpr u32 kNone = 0xffffu;
     const u32 tid = threadIdx.x;
+    for (u32 i = tid; i < static_cast<u32>(CAP); i += BLOCK)
+        head[i] = kNone;
     for (u32 i = tid; i < m; i += BLOCK) {
         const u32 *w = edges + 6 * static_cast<u64>(i);
         sh.f_key[i] = (static_cast<u64>(ld_cg(w)) << 32) | ld_cg(w + 1);
@@ -1309,59 +1326,83 @@ __device__ u32 meet_from_edges(const u32 *edges, u32 m, u32 olo, u32 ohi, u32 *m
         sh.f_s[i] = static_cast<u64>(ld_cg(w + 4)) | (static_cast<u64>(ld_cg(w + 5)) << 32);
     }
     __syncthreads();
-    // Every thread owns PER edges; the table is walked once per pass (j outer, shared loads broadcast).
     u32 vi[PER];
-    u64 ki[PER], sum[PER];
-    bool first[PER];
+    u64 ki[PER];
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
         const u32 i = tid + q * BLOCK;
         vi[q] = i < m ? sh.f_v[i] : 0u;
-        ki[q] = i < m ? sh.f_key[i] : 0ull; // (no key is below 0: a padding item never loses `first`, and is ignored)
+        ki[q] = i < m ? sh.f_key[i] : 0ull;
+        if (i < m)
+            next[i] = static_cast<unsigned short>(atomicExch(head + ((vi[q] * 2654435761u) >> 16) % CAP, i));
+    }
+    __syncthreads();
+    // sigma_ex[v] = sat-sum over v's edges (sampler.cpp:11-13,97-98); the edge with the smallest key represents v
+    u64 sum[PER];
+    bool first[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const u32 i = tid + q * BLOCK;
         sum[q] = 0;
         first[q] = i < m;
+        if (i < m)
+            for (u32 j = head[((vi[q] * 2654435761u) >> 16) % CAP]; j != kNone; j = next[j])
+                if (sh.f_v[j] == vi[q]) {
+                    const u64 sj = sh.f_s[j];
+                    sum[q] = sum[q] > ~0ull - sj ? ~0ull : sum[q] + sj;
+                    if (sh.f_key[j] < ki[q])
+                        first[q] = false;
+                }
     }
-#pragma unroll 1
-    for (u32 j = 0; j < m; ++j) {
-        const u32 vj = sh.f_v[j];
-        const u64 kj = sh.f_key[j], sj = sh.f_s[j];
+    __syncthreads(); // every thread has read f_s, head and next
+    bool member[PER];
+    u32 before = 0; // members in slots below this thread's (ranking them all needs an order, any order)
+    {
+        u32 mine = 0;
 #pragma unroll
-        for (int q = 0; q < PER; ++q)
-            if (vj == vi[q]) {
-                sum[q] = sum[q] > ~0ull - sj ? ~0ull : sum[q] + sj; // sat_add_u64 (sampler.cpp:11-13)
-                if (kj < ki[q])
-                    first[q] = false;
-            }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-        const u32 i = tid + q * BLOCK;
-        if (i < m) {
+        for (int q = 0; q < PER; ++q) {
+            const u32 i = tid + q * BLOCK;
+            member[q] = first[q] && sh.f_o[i] - olo < ohi - olo;
             if (first[q])
                 sh.f_s[i] = sum[q];
-            else
-                sh.f_o[i] = 0xffffffffu; // a later edge of an already listed vertex
+            mine += member[q] ? 1u : 0u;
         }
-    }
-    __syncthreads();
-    u32 rank[PER];
-    bool member[PER];
+        u32 incl = mine;
 #pragma unroll
-    for (int q = 0; q < PER; ++q) {
-        const u32 i = tid + q * BLOCK;
-        member[q] = i < m && sh.f_o[i] - olo < ohi - olo;
-        rank[q] = 0;
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane_id() >= static_cast<u32>(o))
+                incl += t;
+        }
+        if (BLOCK > 32) {
+            if (lane_id() == 31)
+                sh.warp_cnt[tid >> 5] = incl;
+            __syncthreads();
+            for (u32 w = 0; w < (tid >> 5); ++w)
+                incl += sh.warp_cnt[w];
+        }
+        before = incl - mine;
+        if (tid == BLOCK - 1)
+            sh.bcast[1] = incl;
     }
+#pragma unroll
+    for (int q = 0; q < PER; ++q)
+        if (member[q])
+            dense[before++] = static_cast<unsigned short>(tid + q * BLOCK);
+    __syncthreads();
+    const u32 members = sh.bcast[1];
+    // position in discovery order = number of members with a smaller key (sampler.cpp:92-95: order of `next`)
+    u32 rank[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q)
+        rank[q] = 0;
 #pragma unroll 1
-    for (u32 j = 0; j < m; ++j) {
-        const u64 kj = sh.f_key[j];
-        const bool in_range = sh.f_o[j] - olo < ohi - olo;
+    for (u32 jj = 0; jj < members; ++jj) {
+        const u64 kj = sh.f_key[dense[jj]];
 #pragma unroll
         for (int q = 0; q < PER; ++q)
-            rank[q] += in_range && kj < ki[q] ? 1u : 0u;
+            rank[q] += kj < ki[q] ? 1u : 0u;
     }
-    u32 members = 0;
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
         const u32 i = tid + q * BLOCK;
@@ -1371,12 +1412,10 @@ __device__ u32 meet_from_edges(const u32 *edges, u32 m, u32 olo, u32 ohi, u32 *m
             st_cg(w + 1, sh.f_o[i]);
             st_cg(w + 2, static_cast<u32>(sh.f_s[i]));
             st_cg(w + 3, static_cast<u32>(sh.f_s[i] >> 32));
-            ++members;
         }
     }
-    const u32 total = static_cast<u32>(block_sum_u64<BLOCK>(members, sh.red64));
     __syncthreads();
-    return total;
+    return members;
 }
 
 // The same for a probed final level with more contact edges than meet_from_edges holds in shared
