@@ -181,6 +181,13 @@ typedef struct ebc_run_config {
                                 * -1 = none; k > 0 = k SMs.  Costs k/148 of the sampling rate; without it a kernel
                                 * of NCCL's footprint waited 40 us for room at the epoch switch
                                 * (tools/overlap_timeline.py, profiles/r02_overlap_timeline.txt). */
+    int work_counters;         /* 1 (ebc_run_config_default) = the sampling kernels maintain the device work counters
+                                * (ebc_sampler_work, ebc_run_stats.work) and the bookkeeping behind
+                                * ebc_sampler_last_state; 0 = production kernels without them: the counters read 0,
+                                * results are the same, sampling is 3-10 % faster (the statistics are code every
+                                * sample runs through once, and instruction fetch is the kernel's largest stall).
+                                * Launches that return records or paths, or materialize_final_level, always use the
+                                * kernels with statistics. */
 } ebc_run_config;
 
 EBC_API void ebc_run_config_default(ebc_run_config *cfg);

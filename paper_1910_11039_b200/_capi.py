@@ -30,7 +30,7 @@ class RunConfig(C.Structure):
         ("device", C.c_int), ("rank", C.c_int), ("world_size", C.c_int),
         ("allreduce", ALLREDUCE_FN), ("allreduce_user", C.c_void_p),
         ("block_threads", C.c_uint32), ("slots", C.c_uint32), ("slot_capacity", C.c_uint64),
-        ("overlap", C.c_int), ("items_per_thread", C.c_uint32), ("materialize_final_level", C.c_int), ("renumber", C.c_int), ("reserved_sms", C.c_int),
+        ("overlap", C.c_int), ("items_per_thread", C.c_uint32), ("materialize_final_level", C.c_int), ("renumber", C.c_int), ("reserved_sms", C.c_int), ("work_counters", C.c_int),
     ]
 
 

@@ -258,6 +258,7 @@ class RunConfig:
     materialize_final_level: bool = False
     renumber: int = 0  # device-side numbering: 0 auto, -1 never, 1 degree classes (hubs), 2 neighbourhood clusters
     reserved_sms: int = 0  # SMs left to the frame all-reduce: 0 auto (4 when world_size > 1), -1 none, k > 0
+    work_counters: bool = True  # False: production kernels without work counters / state-dump bookkeeping (3-10 % faster)
 
     def to_c(self) -> _CRunConfig:
         c = _CRunConfig()
@@ -269,6 +270,7 @@ class RunConfig:
             setattr(c, f, getattr(self, f))
         c.overlap = int(self.overlap)
         c.materialize_final_level = int(self.materialize_final_level)
+        c.work_counters = int(self.work_counters)
         if self.allreduce is not None:
             c.allreduce = self.allreduce
             c.allreduce_user = self.allreduce_user

@@ -85,6 +85,7 @@ SamplerOptions sampler_options(const ebc_run_config *cfg) {
         o.items_per_thread = cfg->items_per_thread;
         o.materialize_final_level = cfg->materialize_final_level != 0;
         o.renumber = cfg->renumber;
+        o.work_counters = cfg->work_counters != 0;
         // the frame all-reduce of epoch e runs beside the sampling of epoch e+1 (see ebc_b200.h)
         o.reserved_sms = cfg->reserved_sms > 0 ? static_cast<std::uint32_t>(cfg->reserved_sms)
                          : cfg->reserved_sms == 0 && cfg->world_size > 1 && cfg->overlap ? 4u : 0u;
@@ -322,6 +323,7 @@ void ebc_run_config_default(ebc_run_config *cfg) {
     cfg->rank = 0;
     cfg->world_size = 1;
     cfg->overlap = 1;
+    cfg->work_counters = 1;
 }
 
 ebc_status ebc_run(const ebc_graph *g, const ebc_run_config *cfg, ebc_result **out) {

@@ -963,6 +963,8 @@ struct CudaSampler::Impl {
         EBC_CUDA(cudaMemsetAsync(ticket, 0, 2 * sizeof(unsigned long long), st));
         EBC_CUDA(cudaMemsetAsync(ovf_count, 0, 2 * sizeof(u32), st));
         SamplerParams p = base_params(small);
+        if (d_records || d_paths)
+            p.flags |= kFlagStats; // (only the kernels with statistics fill records and paths)
         p.seed = seed;
         p.tag = tag;
         p.first = first;
@@ -993,6 +995,7 @@ struct CudaSampler::Impl {
             // the large slots are bound to blockIdx: re-run passes of the two lanes must not overlap
             EBC_CUDA(cudaStreamWaitEvent(st, ev_rerun[1 - lane], 0));
             SamplerParams q = base_params(big);
+            q.flags = p.flags;
             q.seed = seed;
             q.tag = tag;
             q.first = first;
@@ -1099,6 +1102,8 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
 
     // ---- launch shape ----
     m.flags = opt.materialize_final_level ? kFlagMaterializeFinal : 0u;
+    if (opt.work_counters || opt.materialize_final_level)
+        m.flags |= kFlagStats;
     if (const char *env = std::getenv("EBC_RESERVED_SMS")) // test / tuning hook
         m.reserved_sms = static_cast<u32>(std::atoi(env));
     else

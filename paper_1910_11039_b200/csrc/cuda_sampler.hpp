@@ -22,6 +22,7 @@ struct SamplerOptions {
     bool materialize_final_level = false; // settle the final level of every sample (see ebc_b200.h)
     int renumber = 0; // device-side numbering: 0 = auto, -1 = never, 1 = degree classes, 2 = neighbourhood clusters
     std::uint32_t reserved_sms = 0; // SMs the main sampling pass leaves empty (for a collective running beside it)
+    bool work_counters = true; // false: kernels without statistics (see ebc_run_config.work_counters)
     bool short_launches = false; // launches of a few samples per slot (the epochs of a pipeline run): prefer fewer, larger CTAs
 };
 

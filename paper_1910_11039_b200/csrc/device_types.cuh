@@ -39,6 +39,7 @@ constexpr u32 kMaxBlockThreads = 1024;
 constexpr u32 kMaxTileSlots = 4096;        // BLOCK * ITEMS never exceeds this
 constexpr u32 kFlagUseBitmap = 2u;        // per-slot visited bitmaps are maintained and used by probe_level
 constexpr u32 kFlagMaterializeFinal = 1u; // always settle the final level (state dumps, exact V_set / F_chk)
+constexpr u32 kFlagStats = 4u;            // launch the kernels that keep work counters, sample records, paths and state-dump bookkeeping
 constexpr u32 kEllWidth = 8;               // entries per fixed-stride row (SamplerParams::ell)
 constexpr u32 kEllRevShift = 26;           // bits 26..28 of an entry: position of the reverse arc in the target's row
 constexpr u32 kEllDegShift = 29;           // bits 29..31: degree of the target, minus one

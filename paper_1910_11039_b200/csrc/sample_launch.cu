@@ -2,7 +2,13 @@
 // adjacency slots per thread, with and without visited bitmaps.  Compiled once per block size so that the
 // fifteen shapes build in parallel; nothing here but the launches.
 #include "sample_launch.hpp"
+// the kernels twice: with the statistics (work counters, records, paths, state dumps) and without (see the header)
+#define EBC_STATS 1
 #include "sampler_kernels.cuh"
+#undef EBC_STATS
+#define EBC_STATS 0
+#include "sampler_kernels.cuh"
+#undef EBC_STATS
 
 #ifndef EBC_SHAPE_BLOCK
 #error "compile with -DEBC_SHAPE_BLOCK=32|64|128|256|512"
@@ -22,16 +28,27 @@ namespace ebc {
 #endif
 
 template <int ITEMS> static void launch_one(const SamplerParams &p, u32 grid, cudaStream_t stream) {
+    const bool stats = (p.flags & kFlagStats) != 0;
 #if EBC_HAVE_FIXED
     if (p.ell) {
-        sample_kernel<EBC_SHAPE_BLOCK, 2, false, true><<<grid, EBC_SHAPE_BLOCK, 0, stream>>>(p);
+        if (stats)
+            with_stats::sample_kernel<EBC_SHAPE_BLOCK, 2, false, true><<<grid, EBC_SHAPE_BLOCK, 0, stream>>>(p);
+        else
+            lean::sample_kernel<EBC_SHAPE_BLOCK, 2, false, true><<<grid, EBC_SHAPE_BLOCK, 0, stream>>>(p);
         return;
     }
 #endif
-    if (p.flags & kFlagUseBitmap)
-        sample_kernel<EBC_SHAPE_BLOCK, ITEMS, true><<<grid, EBC_SHAPE_BLOCK, 0, stream>>>(p);
-    else
-        sample_kernel<EBC_SHAPE_BLOCK, ITEMS, false><<<grid, EBC_SHAPE_BLOCK, 0, stream>>>(p);
+    if (p.flags & kFlagUseBitmap) {
+        if (stats)
+            with_stats::sample_kernel<EBC_SHAPE_BLOCK, ITEMS, true><<<grid, EBC_SHAPE_BLOCK, 0, stream>>>(p);
+        else
+            lean::sample_kernel<EBC_SHAPE_BLOCK, ITEMS, true><<<grid, EBC_SHAPE_BLOCK, 0, stream>>>(p);
+    } else {
+        if (stats)
+            with_stats::sample_kernel<EBC_SHAPE_BLOCK, ITEMS, false><<<grid, EBC_SHAPE_BLOCK, 0, stream>>>(p);
+        else
+            lean::sample_kernel<EBC_SHAPE_BLOCK, ITEMS, false><<<grid, EBC_SHAPE_BLOCK, 0, stream>>>(p);
+    }
 }
 
 bool EBC_CAT(launch_sample_b, EBC_SHAPE_BLOCK)(u32 items, const SamplerParams &p, u32 grid, cudaStream_t stream) {
@@ -45,7 +62,7 @@ bool EBC_CAT(launch_sample_b, EBC_SHAPE_BLOCK)(u32 items, const SamplerParams &p
 
 template <int ITEMS> static int occupancy_one() {
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sample_kernel<EBC_SHAPE_BLOCK, ITEMS, true>, EBC_SHAPE_BLOCK, 0) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, with_stats::sample_kernel<EBC_SHAPE_BLOCK, ITEMS, true>, EBC_SHAPE_BLOCK, 0) !=
         cudaSuccess)
         return -2;
     return per_sm;
@@ -55,7 +72,7 @@ int EBC_CAT(sample_occupancy_b, EBC_SHAPE_BLOCK)(u32 items, bool fixed_rows) {
     if (fixed_rows) {
 #if EBC_HAVE_FIXED
         int per_sm = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sample_kernel<EBC_SHAPE_BLOCK, 2, false, true>,
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, with_stats::sample_kernel<EBC_SHAPE_BLOCK, 2, false, true>,
                                                           EBC_SHAPE_BLOCK, 0) != cudaSuccess)
             return -2;
         return per_sm;

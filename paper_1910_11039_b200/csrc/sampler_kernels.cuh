@@ -23,8 +23,13 @@
 // idx = cnt + rank.  Earlier tiles are final before later tiles start, hence
 // idx == the reference's position in `next` (sampler.cpp:92-95).  Sigma sums,
 // pending edge counts and counters are order independent.
-#pragma once
-
+//
+// This file is included TWICE by sample_launch.cu (no include guard): once with EBC_STATS 1 -> namespace
+// ebc::with_stats, the kernels that maintain the work counters, sample records, paths and state-dump bookkeeping;
+// once with EBC_STATS 0 -> namespace ebc::lean, the same kernels without any of it (EBC_STAT(...) expands to
+// nothing).  A warp runs through some 3000 instructions once per sample, sixteen to thirty-two CTAs per SM each at a
+// different place of them, and instruction fetch is the largest stall of the hub kernels
+// (profiles/r02_instruction_supply.txt): the statistics cost config 2 a tenth of its rate.
 #include <cstddef>
 #include <type_traits>
 #include <cuda_runtime.h>
@@ -32,7 +37,16 @@
 #include "device_types.cuh"
 #include "philox.cuh"
 
+#if EBC_STATS
+#define EBC_VARIANT with_stats
+#define EBC_STAT(...) { __VA_ARGS__ }
+#else
+#define EBC_VARIANT lean
+#define EBC_STAT(...) {}
+#endif
+
 namespace ebc {
+namespace EBC_VARIANT {
 
 using u128 = unsigned __int128;
 
@@ -497,15 +511,15 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, u32 *v
     if (tid == 0) {
         st_cg(ex.pp->lvl + next_depth, level_start);
         sh.min_contact = 0xffffffffu;
-        sh.ws[kW_V_exp] += fe - fb;
-        sh.ws[kW_levels] += 1;
+        EBC_STAT(sh.ws[kW_V_exp] += fe - fb;)
+        EBC_STAT(sh.ws[kW_levels] += 1;)
     }
     for (u32 c0 = fb; c0 < fe; c0 += BLOCK) {
         // ---- load a chunk of BLOCK frontier vertices, scan their degrees ----
         // (the loader's first barrier: the previous chunk's tiles are done with c_*, their label stores visible)
         const u64 T = load_chunk<BLOCK>(p, ex.pp, c0, fe, sh.c_beg, sh.c_scan, sh.c_sig, sh.red64);
         if (tid == 0)
-            sh.ws[kW_E_bfs] += T;
+            EBC_STAT(sh.ws[kW_E_bfs] += T;)
 
         // ---- ordered tiles of TILE adjacency slots ----
         int prev_row = -1;
@@ -579,10 +593,10 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, u32 *v
                             atomicMin(&sh.min_contact, other_idx[k]);
                             any_contact_local = true;
                         }
-                        wk.e_lvl += 1;
+                        EBC_STAT(wk.e_lvl += 1;)
                     } else if (at_level[k]) {
                         sat_atomic_add(ex.pp->sig + idx[k], sig_u, sigma_small);
-                        wk.e_lvl += 1;
+                        EBC_STAT(wk.e_lvl += 1;)
                     }
                 }
                 if (__syncthreads_or(any_contact_local ? 1 : 0)) {
@@ -702,7 +716,7 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, u32 *v
                         idx[k] = tile_idx[won_by[k]]; // the winner's idx
                     if (candidate[k] || at_level[k]) {
                         sat_atomic_add(ex.pp->sig + idx[k], sig_u[k], sigma_small); // sampler.cpp:97-98
-                        wk.e_lvl += 1;
+                        EBC_STAT(wk.e_lvl += 1;)
                     }
                 }
                 if (any_contact) {
@@ -726,8 +740,8 @@ __device__ bool expand_level(const SamplerParams &p, u32 *lab, u32 *bits, u32 *v
     }
     __syncthreads();
     if (tid == 0) {
-        sh.ws[kW_V_set] += cnt - level_start;
-        sh.ws[kW_F_chk] += cnt - level_start;
+        EBC_STAT(sh.ws[kW_V_set] += cnt - level_start;)
+        EBC_STAT(sh.ws[kW_F_chk] += cnt - level_start;)
     }
     ex.fb = level_start; // sampler.cpp:101-103
     ex.cnt = cnt;
@@ -815,9 +829,9 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
     if (tid == 0) {
         st_cg(ex.pp->lvl + next_depth, level_start);
         sh.min_contact = 0xffffffffu;
-        sh.ws[kW_V_exp] += fe - fb;
-        sh.ws[kW_levels] += 1;
-        sh.ws[kW_E_bfs] += ex.pending; // the frontier's adjacency entries
+        EBC_STAT(sh.ws[kW_V_exp] += fe - fb;)
+        EBC_STAT(sh.ws[kW_levels] += 1;)
+        EBC_STAT(sh.ws[kW_E_bfs] += ex.pending;) // the frontier's adjacency entries
     }
     const uint4 empty4 = make_uint4(kEllEmpty, kEllEmpty, kEllEmpty, kEllEmpty);
     uint4 *h_mine = reinterpret_cast<uint4 *>(tab + KEYS) + tid; // this thread clears h_mine[0], [BLOCK], [2 BLOCK], [3 BLOCK] (hv and hk)
@@ -1017,12 +1031,12 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
         cnt += winners;
         contact_n += ctot;
     }
-    wk.e_lvl += n_lvl;
+    EBC_STAT(wk.e_lvl += n_lvl;)
     const u64 pending = block_sum_u64<BLOCK>(pend, sh.red64);
     const int big = __syncthreads_or(gsum >= (1ull << 63) / BLOCK ? 1 : 0);
     if (tid == 0) {
-        sh.ws[kW_V_set] += cnt - level_start;
-        sh.ws[kW_F_chk] += cnt - level_start;
+        EBC_STAT(sh.ws[kW_V_set] += cnt - level_start;)
+        EBC_STAT(sh.ws[kW_F_chk] += cnt - level_start;)
         sh.prev_pending[e] = ex.pending;
         sh.sigma_small[e] = big ? 0u : 1u;
     }
@@ -1630,8 +1644,8 @@ __device__ void walk_side(const SamplerParams &p, const u32 *lab, int x, const S
     while (d > 0) {
         const u64 beg = __ldg(p.offsets + u), end = __ldg(p.offsets + u + 1);
         if (tid == 0) {
-            sh.ws[kW_S_walk] += 1;
-            sh.ws[kW_E_walk] += end - beg;
+            EBC_STAT(sh.ws[kW_S_walk] += 1;)
+            EBC_STAT(sh.ws[kW_E_walk] += end - beg;)
         }
         u32 chosen = u;
         if (d == 1) {
@@ -1639,7 +1653,7 @@ __device__ void walk_side(const SamplerParams &p, const u32 *lab, int x, const S
             (void)uniform_below_u128(rng, 1);
             chosen = ld_cg(sd.pp->list);
             if (tid == 0)
-                wk.p_walk += 1;
+                EBC_STAT(wk.p_walk += 1;)
         } else {
             const u32 lo = ld_cg(sd.pp->lvl + (d - 1)), hi = ld_cg(sd.pp->lvl + d);
             const u32 span = hi - lo;
@@ -1667,7 +1681,7 @@ __device__ void walk_side(const SamplerParams &p, const u32 *lab, int x, const S
                     if (a < xend && __ldg(p.ext_targets + a) == wx) {
                         const u64 sg = ld_cg(sd.pp->sig + i);
                         total_local += sg;
-                        wk.p_walk += 1;
+                        EBC_STAT(wk.p_walk += 1;)
                         const u32 slot = atomicAdd(&sh.pred_cnt, 1u);
                         if (slot < kPredCache) {
                             sh.pred_pos[slot] = static_cast<u32>(a - xbeg);
@@ -1683,7 +1697,7 @@ __device__ void walk_side(const SamplerParams &p, const u32 *lab, int x, const S
                     if (rel < span) {
                         const u64 sg = ld_cg(sd.pp->sig + lo + rel);
                         total_local += sg;
-                        wk.p_walk += 1;
+                        EBC_STAT(wk.p_walk += 1;)
                         const u32 slot = atomicAdd(&sh.pred_cnt, 1u);
                         if (slot < kPredCache) {
                             sh.pred_pos[slot] = static_cast<u32>(k - beg);
@@ -1859,7 +1873,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) samp
             sh.wk[c] = 0;
     if (tid == 0)
         for (int c = 0; c < 6; ++c)
-            sh.last[c] = 0;
+            EBC_STAT(sh.last[c] = 0;)
 #ifdef EBC_PHASE_TIMERS // experiment only: cycles per phase replace the work counters
     long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     long long ph_t = clock64();
@@ -1909,7 +1923,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) samp
             s = static_cast<u32>(a);
             t = static_cast<u32>(b);
         }
-        const u32 s_ext = s, t_ext = t;
+        [[maybe_unused]] const u32 s_ext = s, t_ext = t; // (for the record)
         if (p.to_dense) {
             s = __ldg(p.to_dense + s);
             t = __ldg(p.to_dense + t);
@@ -1937,9 +1951,9 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) samp
         }
         if (tid == 0) {
             for (int c = 0; c < kWorkCounters; ++c)
-                sh.ws[c] = 0;
-            sh.ws[kW_V_set] = 2;
-            sh.ws[kW_samples] = 1;
+                EBC_STAT(sh.ws[c] = 0;)
+            EBC_STAT(sh.ws[kW_V_set] = 2;)
+            EBC_STAT(sh.ws[kW_samples] = 1;)
             sh.sigma_small[0] = sh.sigma_small[1] = 1; // sigma[root] = 1
             sh.prev_pending[0] = sh.prev_pending[1] = 0;
         }
@@ -1947,6 +1961,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) samp
         wk.p_walk = 0;
         __syncthreads();
 
+#if EBC_STATS
         if (tid == 0) { // the sample's record is kept in shared memory, written by thread 0 only
             SampleRecordDev &rec = sh.rec;
             rec.s = s_ext;
@@ -1958,6 +1973,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) samp
             rec.flags = 0;
             rec.weight_lo = rec.weight_hi = 0;
         }
+#endif
 
         // ---- level loop (sampler.cpp:81-116) ----
         EBC_PH(0)
@@ -1993,11 +2009,11 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) samp
                 }
                 if (resolvable) {
                     // final level: account its scan, open the (virtual) level for the walk, stop
-                    wk.e_lvl += new_slots;
+                    EBC_STAT(wk.e_lvl += new_slots;)
                     if (tid == 0) {
-                        sh.ws[kW_E_bfs] += total_slots;
-                        sh.ws[kW_V_exp] += side[e].cnt - side[e].fb;
-                        sh.ws[kW_levels] += 1;
+                        EBC_STAT(sh.ws[kW_E_bfs] += total_slots;)
+                        EBC_STAT(sh.ws[kW_V_exp] += side[e].cnt - side[e].fb;)
+                        EBC_STAT(sh.ws[kW_levels] += 1;)
                         st_cg(side[e].pp->lvl + side[e].depth + 1, side[e].cnt);
                     }
                     __syncthreads();
@@ -2033,7 +2049,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) samp
 
         if (aborted) {
             if (tid == 0) {
-                sh.rec.flags |= 1u;
+                EBC_STAT(sh.rec.flags |= 1u;)
                 const u32 k = atomicAdd(p.overflow_count, 1u);
                 if (k < p.overflow_cap)
                     p.overflow_list[k] = static_cast<u32>(local);
@@ -2051,9 +2067,9 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) samp
             const u32 olo = ld_cg(ot.pp->lvl + best);
             const u32 ohi = best == ot.depth ? ot.cnt : ld_cg(ot.pp->lvl + best + 1);
             if (tid == 0) {
-                sh.rec.dist = d_ex + best;
+                EBC_STAT(sh.rec.dist = d_ex + best;)
                 if (probed)
-                    sh.rec.flags |= 2u;
+                    EBC_STAT(sh.rec.flags |= 2u;)
             }
             __syncthreads();
 
@@ -2080,10 +2096,10 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) samp
             __syncthreads();
             const u128 total_weight = wov ? ~static_cast<u128>(0) : ((static_cast<u128>(whi) << 64) | wlo);
             if (tid == 0) {
-                sh.rec.weight_lo = static_cast<u64>(total_weight);
-                sh.rec.weight_hi = static_cast<u64>(total_weight >> 64);
-                sh.rec.meet_count = meet_count;
-                sh.ws[kW_M] += meet_count;
+                EBC_STAT(sh.rec.weight_lo = static_cast<u64>(total_weight);)
+                EBC_STAT(sh.rec.weight_hi = static_cast<u64>(total_weight >> 64);)
+                EBC_STAT(sh.rec.meet_count = meet_count;)
+                EBC_STAT(sh.ws[kW_M] += meet_count;)
             }
 
             // pick and ordered prefix search (sampler.cpp:124-133).  pick < total_weight <=
@@ -2117,7 +2133,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) samp
                     meet = ld_cg(sh.meetbuf + 4 * static_cast<u64>(meet_count - 1));
             }
             if (tid == 0)
-                sh.rec.meet = ext_id(p, meet);
+                EBC_STAT(sh.rec.meet = ext_id(p, meet);)
             EBC_PH(4)
 
             // walks (sampler.cpp:157-163): path order s .. meet .. t
@@ -2144,22 +2160,22 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) samp
                 }
             }
             if (tid == 0)
-                sh.rec.path_len = emitted;
+                EBC_STAT(sh.rec.path_len = emitted;)
             EBC_PH(5)
             if (tid == 0)
-                sh.ws[kW_L] += emitted;
+                EBC_STAT(sh.ws[kW_L] += emitted;)
         }
 
         // ---- apply_sample: tau += 1 (sampler.hpp:75); retire the sample's labels ----
         if (tid == 0)
-            sh.rec.draws = rng.draws();
+            EBC_STAT(sh.rec.draws = rng.draws();)
         if (!aborted) {
             tot_e_lvl += wk.e_lvl;
             tot_p_walk += wk.p_walk;
             if (tid == 0) {
                 atomicAdd(p.frame, 1u);
                 for (int c = 0; c < kWorkCounters; ++c)
-                    sh.wk[c] += sh.ws[c];
+                    EBC_STAT(sh.wk[c] += sh.ws[c];)
             }
         }
         if (p.records && tid == 0)
@@ -2188,9 +2204,9 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) samp
         }
         for (int k = 0; k < 2; ++k) {
             if (tid == 0) {
-                sh.last[k] = side[k].base;
-                sh.last[2 + k] = side[k].cnt;
-                sh.last[4 + k] = side[k].depth;
+                EBC_STAT(sh.last[k] = side[k].base;)
+                EBC_STAT(sh.last[2 + k] = side[k].cnt;)
+                EBC_STAT(sh.last[4 + k] = side[k].depth;)
             }
         }
         {
@@ -2240,4 +2256,8 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) samp
     }
 }
 
+} // namespace EBC_VARIANT
 } // namespace ebc
+
+#undef EBC_VARIANT
+#undef EBC_STAT

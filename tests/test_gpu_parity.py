@@ -322,3 +322,32 @@ def test_fixed_stride_rows_need_a_symmetric_graph():
     s = ebc.Sampler(g, ebc.RunConfig(block_threads=32, slots=2))
     assert not s.info()["fixed_rows"]
     s.close()
+
+
+@pytest.mark.parametrize("name,block", [("er300dense", 32), ("grid12", 64), ("layers70", 128), ("rmat12", 64), ("rmat12", 256)])
+def test_kernels_without_statistics_give_the_same_frames(name, block):
+    """ebc_run_config.work_counters = 0 launches the production kernels (namespace ebc::lean: no work counters, records or
+    state-dump bookkeeping).  Frames are the oracle's; the counters read zero; a launch that asks for records falls
+    back to the kernels with statistics."""
+    if name == "rmat12":
+        g0 = ebc.gen_rmat(12, 16, seed=3).largest_connected_component()
+        off, tg = g0.offsets.copy(), g0.targets.copy()
+    else:
+        off, tg = small_graphs()[name]
+    g = ebc.Graph.from_csr(off, tg)
+    o = Oracle(off, tg)
+    s = ebc.Sampler(g, ebc.RunConfig(block_threads=block, work_counters=False))
+    s.sample(SEED, 50, 3000)
+    assert np.array_equal(s.read_frame(0), o.accumulate(SEED, 50, 3000))
+    assert s.work()["samples"] == 0 and s.work()["E_bfs"] == 0
+    rec, _ = s.sample_debug(SEED, 0, 40, frame=1)
+    for i in range(40):
+        want = o.sample(SEED, i)
+        assert (int(rec[i]["s"]), int(rec[i]["t"]), int(rec[i]["dist"]), int(rec[i]["meet"])) == \
+               (want["s"], want["t"], want["dist"], want["meet"])
+    assert s.work()["samples"] == 40
+    s.close()
+    res_a, st_a = ebc.run_pipeline(g, ebc.RunConfig(eps=0.05, delta=0.1, seed=SEED, block_threads=block, work_counters=False))
+    res_b, st_b = ebc.run_pipeline(g, ebc.RunConfig(eps=0.05, delta=0.1, seed=SEED, block_threads=block))
+    assert np.array_equal(res_a.counts, res_b.counts) and st_a["tau"] == st_b["tau"] and st_a["epochs"] == st_b["epochs"]
+    assert st_a["work"]["samples"] == 0 and st_b["work"]["samples"] > 0

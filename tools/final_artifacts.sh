@@ -10,8 +10,8 @@ python bench.py --impl reference --steps 2 --warmup 1 > $O/fa_bench_reference.js
 # DRAM traffic of bench-sized launches first: bench.py reads profiles/traffic.json
 for spec in "rmat20 524288" "grid2000 32768" "rmat24 262144"; do
   set -- $spec
-  python tools/prof_launch.py $1 $2 > $O/fa_plain_$1.log 2>&1 || exit 1      # exits 0 without ncu first
-  ncu --set full --import-source on --clock-control none -k regex:sample_kernel --launch-skip 1 --launch-count 1 \
+  python tools/prof_launch.py $1 $2 > $O/fa_plain_$1.log 2>&1 || exit 1      # exits 0 without ncu first; launches: warm-up main + re-run pass, then the measured main (+ re-run) pass
+  ncu --set full --import-source on --clock-control none -k regex:sample_kernel --launch-skip 2 --launch-count 2 \
       -o $O/fa_ncu_$1 -f python tools/prof_launch.py $1 $2 > $O/fa_ncu_$1.log 2>&1
   python tools/record_traffic.py $1 $O/fa_ncu_$1.ncu-rep $2 r02_final_$1 > $O/fa_traffic_$1.log 2>&1
   python tools/ncu_summary.py $O/fa_ncu_$1.ncu-rep > $O/fa_ncu_summary_$1.txt 2>&1
