@@ -7,7 +7,7 @@ from bench import workload_of, build_graph
 key = sys.argv[1]; N = int(sys.argv[2]); W = int(sys.argv[3]) if len(sys.argv) > 3 else max(N // 4, 1)
 w = workload_of(key)
 g = build_graph(w, on_device=w["kind"] == "rmat" and w["scale"] >= 22)
-s = ebc.Sampler(g, ebc.RunConfig())
+s = ebc.Sampler(g, ebc.RunConfig(work_counters=os.environ.get("EBC_PROF_STATS", "0") != "0"))  # the kernels bench.py times
 s.sample(7, 0, W, frame=0); s.sync()
 s.mark(0); s.sample(7, 1 << 22, N, frame=1); s.mark(1)
 ms = s.elapsed_ms(0, 1)
