@@ -1667,10 +1667,38 @@ __device__ void walk_side(const SamplerParams &p, const u32 *lab, int x, const S
             if (by_level) {
                 // rows are ascending in EXTERNAL ids: search the uploaded graph's row of u
                 const u64 xbeg = __ldg(p.ext_offsets + ext_id(p, u)), xend = xbeg + degu;
+                // A hub's row is searched by every vertex of the level: the first steps of all those searches -- a
+                // dozen dependent loads each -- are taken in a table of kSplit evenly spaced entries of the row,
+                // fetched once by the CTA (in f_v, which only the meet phase uses).
+                constexpr u32 kSplit = 64;
+                static_assert(kSplit <= FinalEdgeCap<BLOCK>::value, "splitter table aliases f_v");
+                const bool split = degu >= 16 * kSplit;
+                if (split) {
+                    for (u32 j = tid; j < kSplit; j += BLOCK)
+                        sh.f_v[j] = __ldg(p.ext_targets + xbeg + (static_cast<u64>(j) * degu) / kSplit);
+                    __syncthreads();
+                }
                 for (u32 i = lo + tid; i < hi; i += BLOCK) {
                     const u32 w = ld_cg(sd.pp->list + i);
                     const u32 wx = ext_id(p, w);
                     u64 a = xbeg, b = xend; // lower_bound of w in the row of u
+                    if (split) {
+                        if (wx < sh.f_v[0]) {
+                            b = a; // before the row's first entry
+                        } else {
+                            u32 jl = 0, jh = kSplit; // last j with f_v[j] <= wx
+                            while (jh - jl > 1) {
+                                const u32 jm = (jl + jh) >> 1;
+                                if (sh.f_v[jm] <= wx)
+                                    jl = jm;
+                                else
+                                    jh = jm;
+                            }
+                            a = xbeg + (static_cast<u64>(jl) * degu) / kSplit;
+                            b = jl + 1 < kSplit ? xbeg + (static_cast<u64>(jl + 1) * degu) / kSplit + 1 : xend;
+                            b = b < xend ? b : xend;
+                        }
+                    }
                     while (a < b) {
                         const u64 mid = (a + b) >> 1;
                         if (__ldg(p.ext_targets + mid) < wx)
