@@ -12,6 +12,7 @@ copies = {
     "fa_launches_bench_steps2_warmup3.csv": "r02_final_launches_bench_steps2_warmup3.csv",
     "fa_configs.txt": "r02_final_configs.txt", "fa_fuzz_parity.txt": "r02_fuzz_parity.txt",
     "fa_fuzz_pipeline.txt": "r02_fuzz_pipeline.txt", "fa_overlap_timeline.txt": "r02_overlap_timeline_final.txt",
+    "fa_traffic.json": "traffic.json",
 }
 for k in ("rmat20", "grid2000", "rmat24"):
     copies[f"fa_ncu_summary_{k}.txt"] = f"r02_final_{k}_sample_kernel_ncu_summary.txt"
