@@ -1798,6 +1798,88 @@ __device__ void walk_side(const SamplerParams &p, const u32 *lab, int x, const S
     }
 }
 
+// walk_side for graphs with fixed-stride rows: a row has at most eight entries, so lane k of EVERY warp takes entry k
+// (the warps compute the same step redundantly: no shared memory, no block barrier, and the random stream -- which
+// all threads advance alike -- needs no broadcast).  Per step three dependent trips: the row (one sector), the labels
+// of its targets, sigma of the predecessors; the pick is an 8-lane prefix scan in row (= CSR) order (sampler.cpp:139-151).
+template <int BLOCK, int ITEMS>
+__device__ void walk_side_ell(const SamplerParams &p, const u32 *lab, int x, const SideRegs &sd, u32 u, u32 d,
+                              SampleStream &rng, u32 *path_out, long long pos, int pos_step, u32 &emitted,
+                              BlockShared<BLOCK, ITEMS> &sh, WorkRegs &wk) {
+    const u32 tid = threadIdx.x;
+    const u32 k = lane_id();
+    const u32 *lvl = sd.pp->lvl;
+    const u64 *sig = sd.pp->sig;
+    const u32 base = sd.base;
+    (void)sh;
+    (void)wk;
+    while (d > 0) {
+        u32 chosen;
+        if (d == 1) {
+            // the only vertex at depth 0 is the root and sigma[root] == 1: total = 1, r = 0
+            (void)uniform_below_u128(rng, 1);
+            chosen = ld_cg(sd.pp->list);
+            EBC_STAT(if (tid == 0) {
+                sh.ws[kW_S_walk] += 1;
+                sh.ws[kW_E_walk] += __ldg(p.offsets + u + 1) - __ldg(p.offsets + u);
+                wk.p_walk += 1;
+            })
+        } else {
+            const u32 lo = ld_cg(lvl + (d - 1)), span = ld_cg(lvl + d) - lo;
+            const u32 ent = k < kEllWidth ? __ldg(p.ell + kEllWidth * static_cast<u64>(u) + k) : kEllEmpty;
+            const u32 w = ent & kEllIdMask;
+            u64 sg = 0;
+            bool pred = false;
+            if (ent != kEllEmpty) {
+                const u32 rel = label_idx(ld_cg(lab + w), base, x) - lo;
+                pred = rel < span;
+                if (pred)
+                    sg = ld_cg(sig + lo + rel);
+            }
+            EBC_STAT(if (tid < 32) {
+                const u32 entries = __popc(__ballot_sync(0xffffffffu, ent != kEllEmpty));
+                if (tid == 0) {
+                    sh.ws[kW_S_walk] += 1;
+                    sh.ws[kW_E_walk] += entries;
+                }
+                wk.p_walk += pred ? 1 : 0;
+            })
+            // inclusive prefix of sigma over the lanes (at most 8 x (2^64 - 1): 67 bits)
+            u64 plo = sg;
+            u32 phi = 0;
+#pragma unroll
+            for (int o = 1; o < static_cast<int>(kEllWidth); o <<= 1) {
+                const u64 tlo = __shfl_up_sync(0xffffffffu, plo, o);
+                const u32 thi = __shfl_up_sync(0xffffffffu, phi, o);
+                if (k >= static_cast<u32>(o)) {
+                    const u64 nlo = plo + tlo;
+                    phi += thi + (nlo < plo ? 1u : 0u);
+                    plo = nlo;
+                }
+            }
+            const u64 tot_lo = __shfl_sync(0xffffffffu, plo, kEllWidth - 1);
+            const u32 tot_hi = __shfl_sync(0xffffffffu, phi, kEllWidth - 1);
+            const u128 total = (static_cast<u128>(tot_hi) << 64) | tot_lo;
+            const u128 r = uniform_below_u128(rng, total); // sampler.cpp:142
+            const u128 mine = (static_cast<u128>(phi) << 64) | plo;
+            const u32 hit = __ballot_sync(0xffffffffu, pred && mine > r) & ((1u << kEllWidth) - 1);
+            chosen = __shfl_sync(0xffffffffu, w, __ffs(hit) - 1); // first prefix above r (a predecessor exists: total > 0)
+        }
+        u = chosen;
+        d -= 1;
+        if (d > 0) { // sampler.cpp:152-153: endpoints are never counted
+            if (tid == 0) {
+                const u32 ux = ext_id(p, u);
+                atomicAdd(p.frame + 1 + ux, 1u); // apply_sample (sampler.hpp:77)
+                if (path_out && pos >= 0 && static_cast<u64>(pos) < p.path_stride)
+                    path_out[pos] = ux; // longer paths are truncated to path_stride entries
+            }
+            pos += pos_step;
+            emitted += 1;
+        }
+    }
+}
+
 // Resident CTAs per SM the kernel is compiled for (register budget = 65536 / (BLOCK * this)).
 // Measured on config 2 (profiles/r01_occupancy_sweep.txt): 16 -> 3.26M, 24 -> 3.80M, 32 -> 3.88M,
 // 40 -> 3.68M, 48 -> 2.99M samples/s.  The kernel is latency bound, so resident warps matter more than
@@ -2173,6 +2255,12 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) samp
 #pragma unroll 1 // one copy of the walk in the instruction stream
             for (int x = 0; x < 2; ++x) {
                 const SideRegs sd = x == 0 ? side[0] : side[1];
+                if constexpr (FIXED)
+                    walk_side_ell<BLOCK, ITEMS>(p, sh.lab, x, sd, meet, x == 0 ? dist_f : dist_b, rng,
+                                                p.paths ? p.paths + local * p.path_stride : nullptr,
+                                                x == 0 ? static_cast<long long>(dist_f) - 2 : static_cast<long long>(dist_f),
+                                                x == 0 ? -1 : +1, emitted, sh, wk);
+                else
                 walk_side<BLOCK, ITEMS>(p, sh.lab, x, sd, meet, x == 0 ? dist_f : dist_b, rng,
                                         p.paths ? p.paths + local * p.path_stride : nullptr,
                                         x == 0 ? static_cast<long long>(dist_f) - 2 : static_cast<long long>(dist_f),
