@@ -275,7 +275,9 @@ typedef struct ebc_sample_record {
     uint32_t path_len;    /* internal vertices                            */
     uint32_t flags;       /* bit0: capacity overflow (re-run in big slot); bit1: the final level was resolved by the
                            * read-only probe (not settled); bit2: a probe found contact edges it could not resolve
-                           * (buffer or scratch too small) and the level was expanded instead */
+                           * (buffer or scratch too small) and the level was expanded instead; bit3: the probed
+                           * level had more contact edges than the shared-memory meet path holds (resolved in the
+                           * slot's global arrays: config 2 12-20 % of the samples, tools/probe_stats.py) */
     uint64_t weight_lo, weight_hi; /* total meet weight (saturating u128) */
 } ebc_sample_record;
 

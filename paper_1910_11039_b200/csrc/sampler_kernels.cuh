@@ -2185,6 +2185,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) samp
 
             // meet set in discovery order (sampler.cpp:109-113) -> sh.meetbuf
             u32 meet_count;
+            EBC_STAT(if (tid == 0 && probed && edge_n > static_cast<u32>(FinalEdgeCap<BLOCK>::value)) sh.rec.flags |= 8u;) // resolved in global memory
             if constexpr (FIXED)
                 meet_count = meet_from_contacts<BLOCK, ITEMS>(sh.contact, contact_n, ex, olo, ohi, sh.meetbuf, sh);
             else
