@@ -778,8 +778,12 @@ __device__ __forceinline__ u64 sum_frontier_degrees(const SamplerParams &p, cons
 // (one 32-byte sector each, no offsets look-up) -> the labels of their targets.  Everything else stays on the SM:
 //  * thread t owns frontier vertex c0 + t and its (at most eight) entries, key = 8 t + k = discovery order
 //    (sampler.cpp:90-95: frontier order, then row order).  Entries are handled in two groups of four, the second
-//    only by warps that hold a row of more than four entries (the loops over groups are not unrolled: the code
-//    of a chunk is what sixteen CTAs per SM in different phases have to share the instruction cache for);
+//    only by warps that hold a row of more than four entries.  The chunk's vertex is loaded two chunks ahead and
+//    its row one chunk ahead, so only the label trip stays on the critical path;
+//  * entries that lead back to the vertices this one was discovered from are skipped (parent mask pm[idx], one
+//    bit per row entry): every discoverer of a vertex -- the winner with a byte store, the others with a
+//    red.or next to their sigma add -- leaves the position of its arc's reverse in the vertex' row, which every
+//    entry carries;
 //  * the unvisited targets of the chunk are deduplicated in a shared-memory hash set instead of being claimed in
 //    their labels: a candidate inserts its vertex with linear probing (atomicCAS(hv[slot], empty, v) until the
 //    slot is empty or already holds v -- slots are never emptied while a chunk inserts, so all candidates of a
@@ -804,7 +808,7 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
     constexpr int WARPS = BLOCK / 32;
     static_assert((1u << HBITS) == KEYS && W == 8, "hash table size; a row is two 16-byte loads");
     using Shared = BlockShared<BLOCK, ITEMS>;
-    static_assert(sizeof(u32) * (3 * KEYS + KEYS / 4) <= offsetof(Shared, c_sig) + sizeof(sh.c_sig) - offsetof(Shared, f_key) &&
+    static_assert(sizeof(u32) * 3 * KEYS <= offsetof(Shared, c_sig) + sizeof(sh.c_sig) - offsetof(Shared, f_key) &&
                       offsetof(Shared, c_sig) + sizeof(sh.c_sig) - offsetof(Shared, f_key) ==
                           sizeof(sh.f_key) + sizeof(sh.f_s) + sizeof(sh.f_v) + sizeof(sh.f_o) + sizeof(sh.c_beg) +
                               sizeof(sh.c_scan) + sizeof(sh.c_sig),
@@ -812,10 +816,9 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
     // Tables, as shared-window byte addresses (ld/st/atom.shared: no generic-address arithmetic per access):
     u32 *tab = reinterpret_cast<u32 *>(sh.f_key);
     const u32 kv_base = smem_addr(tab);          // [W][BLOCK] by key 8 t + k at [k][t] (no bank conflicts): the candidate's slot;
-    const u32 kv = kv_base + 4 * threadIdx.x;    //   then a loser's winner key / a winner's parent mask, then its idx
+    const u32 kv = kv_base + 4 * threadIdx.x;    //   then a loser's winner key / a winner's idx
     const u32 hv = kv_base + 4 * KEYS;           // [KEYS] hash set: the slot's vertex ...
-    const u32 hk = hv + 4 * KEYS;                // [KEYS] ... the lowest key that brought it ...
-    const u32 hm = hk + 4 * KEYS;                // [KEYS] bytes ... and the reverse positions of all arcs that brought it
+    const u32 hk = hv + 4 * KEYS;                // [KEYS] ... and the lowest key that brought it
     const u32 tid = threadIdx.x;
     const u32 fb = ex.fb, fe = ex.cnt;
     const u32 level_start = fe;
@@ -835,12 +838,9 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
     }
     const uint4 empty4 = make_uint4(kEllEmpty, kEllEmpty, kEllEmpty, kEllEmpty);
     uint4 *h_mine = reinterpret_cast<uint4 *>(tab + KEYS) + tid; // this thread clears h_mine[0], [BLOCK], [2 BLOCK], [3 BLOCK] (hv and hk)
-    u32 *hm_mine = tab + 3 * KEYS + tid;                         // ... and hm_mine[0], [BLOCK]
 #pragma unroll
     for (int q = 0; q < 4; ++q)
         h_mine[q * BLOCK] = empty4;
-    hm_mine[0] = 0u;
-    hm_mine[BLOCK] = 0u;
     __syncthreads();
     const u32 key0 = tid * W;
     u32 pend = 0;  // degrees of the vertices this thread settled
@@ -912,7 +912,6 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
                     slot = (slot + 1) & (KEYS - 1);
                 }
                 reds_min_u32(hk + 4 * slot, key0 + 4 * g + q);
-                reds_or_u32(hm + (slot & ~3u), rev_bit << (8 * (slot & 3)));
                 sts_u32(kv + 4 * ((4 * g + q) * BLOCK), slot);
                 if (!here && idx < ot_cnt) // other.visited(v) (sampler.cpp:107)
                     ccand |= 1u << (4 * g + q);
@@ -940,12 +939,10 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
                     const u32 mine = kv + 4 * ((4 * g + q) * BLOCK);
                     const u32 slot = lds_u32(mine);
                     const u32 w = lds_u32(hk + 4 * slot);
-                    if (w == key0 + 4 * g + q) {
+                    if (w == key0 + 4 * g + q)
                         win |= 1u << (4 * g + q);
-                        sts_u32(mine, (lds_u32(hm + (slot & ~3u)) >> (8 * (slot & 3))) & 0xffu); // the vertex' parent mask
-                    } else {
+                    else
                         sts_u32(mine, w);
-                    }
                 }
         };
         if (cand & 0x0fu)
@@ -999,7 +996,8 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
                     st_cg(lab + v, make_label(base, my_idx, e)); // settle (sampler.cpp:93-95)
                     st_cg(ex.pp->list + my_idx, v);
                     st_cg(ex.pp->sig + my_idx, sig_u); // the discovering edge's sigma (sampler.cpp:98)
-                    __stcg(reinterpret_cast<unsigned char *>(ex.pp->pm) + my_idx, static_cast<unsigned char>(lds_u32(mine)));
+                    __stcg(reinterpret_cast<unsigned char *>(ex.pp->pm) + my_idx,
+                           static_cast<unsigned char>(1u << ((en[q] >> kEllRevShift) & (W - 1))));
                     sts_u32(mine, my_idx);
                     pend += (en[q] >> kEllDegShift) + 1;
                     ++my_idx;
@@ -1012,22 +1010,23 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
 #pragma unroll
         for (int q = 0; q < 4; ++q) // (every thread read the hash set before the scan's barrier / shuffles)
             h_mine[q * BLOCK] = empty4;
-        hm_mine[0] = 0u;
-        hm_mine[BLOCK] = 0u;
         __syncthreads(); // settled vertices, kv and the cleared hash set are visible
-        auto add_sigma = [&](auto G) { // later discoverers of a vertex settled in this chunk (sampler.cpp:97-98)
+        auto add_sigma = [&](auto G, const uint4 &r) { // later discoverers of a vertex settled in this chunk (sampler.cpp:97-98)
             constexpr int g = decltype(G)::value;
+            const u32 en[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
             for (int q = 0; q < 4; ++q)
                 if (cand & ~win & (1u << (4 * g + q))) {
                     const u32 w = lds_u32(kv + 4 * ((4 * g + q) * BLOCK)); // the winner's key
-                    sat_atomic_add(ex.pp->sig + lds_u32(kv_base + 4 * ((w & (W - 1)) * BLOCK + w / W)), sig_u, sigma_small);
+                    const u32 idx = lds_u32(kv_base + 4 * ((w & (W - 1)) * BLOCK + w / W));
+                    sat_atomic_add(ex.pp->sig + idx, sig_u, sigma_small);
+                    red_or_u32(ex.pp->pm + (idx >> 2), (1u << ((en[q] >> kEllRevShift) & (W - 1))) << (8 * (idx & 3)));
                 }
         };
         if (cand & ~win & 0x0fu)
-            add_sigma(std::integral_constant<int, 0>{});
+            add_sigma(std::integral_constant<int, 0>{}, a);
         if (cand & ~win & 0xf0u)
-            add_sigma(std::integral_constant<int, 1>{});
+            add_sigma(std::integral_constant<int, 1>{}, b);
         cnt += winners;
         contact_n += ctot;
     }
