@@ -621,7 +621,8 @@ __global__ void __launch_bounds__(256) dense_rows_kernel(const u64 *ext_offsets,
 // Fixed-stride rows (SamplerParams::ell): row v = its entries in row order, each with the position of the reverse arc
 // and the target's degree - 1 in the upper bits, padded with kEllEmpty.  *bad is raised if that does not work out (a
 // row above kEllWidth entries, or an arc without its reverse -- an asymmetric input); the sampler then runs without them.
-__global__ void __launch_bounds__(256) ell_rows_kernel(const u64 *offsets, const u32 *targets, u64 n, u32 *ell, u32 *bad) {
+// `width` = entries stored per row: kEllWidth, or kEllNarrow when the caller knows that no row is longer.
+__global__ void __launch_bounds__(256) ell_rows_kernel(const u64 *offsets, const u32 *targets, u64 n, u32 width, u32 *ell, u32 *bad) {
     for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v < n;
          v += static_cast<u64>(gridDim.x) * blockDim.x) {
         const u64 beg = offsets[v], deg = offsets[v + 1] - beg;
@@ -636,16 +637,17 @@ __global__ void __launch_bounds__(256) ell_rows_kernel(const u64 *offsets, const
                 for (u32 j = 0; j < kEllWidth && j < dw; ++j)
                     if (targets[wb + j] == v)
                         rev = j;
-                if (dw < 1 || dw > kEllWidth || rev == kEllWidth)
+                if (dw < 1 || dw > width || rev == kEllWidth)
                     *bad = 1;
                 row[k] = w | ((rev & (kEllWidth - 1)) << kEllRevShift) | (static_cast<u32>(dw - 1) << kEllDegShift);
             }
         }
-        if (deg > kEllWidth)
+        if (deg > width)
             *bad = 1;
-        uint4 *out = reinterpret_cast<uint4 *>(ell) + 2 * v;
+        uint4 *out = reinterpret_cast<uint4 *>(ell) + (width / 4) * v;
         out[0] = make_uint4(row[0], row[1], row[2], row[3]);
-        out[1] = make_uint4(row[4], row[5], row[6], row[7]);
+        if (width == kEllWidth)
+            out[1] = make_uint4(row[4], row[5], row[6], row[7]);
     }
 }
 
@@ -792,6 +794,7 @@ struct CudaSampler::Impl {
     u32 *d_dense_targets = nullptr;
     u32 *d_to_dense = nullptr, *d_to_ext = nullptr;
     u32 *d_ell = nullptr; // fixed-stride rows of the graph the kernel searches on (null: maximum degree above kEllWidth)
+    u32 ell_width = kEllWidth; // entries per row: kEllNarrow when the maximum degree allows
     std::vector<u32> h_to_ext; // fetched on demand (last_state)
     u32 block = 128;
     u32 items = 4;
@@ -844,6 +847,7 @@ struct CudaSampler::Impl {
         p.ext_offsets = d_offsets;
         p.ext_targets = d_targets;
         p.ell = d_ell;
+        p.ell_width = ell_width;
         p.lab = a.lab;
         p.list = a.list;
         p.sig = a.sig;
@@ -932,12 +936,12 @@ struct CudaSampler::Impl {
     // Fixed-stride rows of the graph the kernel searches on (the dense copy if there is one).
     void build_fixed_rows() {
         cudaStream_t st = s_sample;
-        d_ell = dev_alloc<u32>(n * kEllWidth);
+        d_ell = dev_alloc<u32>(n * ell_width);
         u32 *bad = dev_alloc<u32>(1);
         EBC_CUDA(cudaMemsetAsync(bad, 0, 4, st));
         const u32 grid = static_cast<u32>(std::min<u64>((n + 255) / 256, static_cast<u64>(sm_count) * 8));
         ell_rows_kernel<<<grid, 256, 0, st>>>(d_dense_offsets ? d_dense_offsets : d_offsets,
-                                              d_dense_targets ? d_dense_targets : d_targets, n, d_ell, bad);
+                                              d_dense_targets ? d_dense_targets : d_targets, n, ell_width, d_ell, bad);
         EBC_CUDA(cudaGetLastError());
         u32 h_bad = 0;
         EBC_CUDA(cudaMemcpyAsync(&h_bad, bad, 4, cudaMemcpyDeviceToHost, st));
@@ -947,7 +951,7 @@ struct CudaSampler::Impl {
             dev_free(d_ell);
             d_ell = nullptr;
         } else {
-            graph_bytes += n * kEllWidth * 4;
+            graph_bytes += n * ell_width * 4;
         }
     }
 
@@ -1175,6 +1179,11 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
     bool want_ell = !m.hub_graph && max_degree <= kEllWidth && m.arcs && m.n < kEllIdMask && m.block <= 128;
     if (const char *env = std::getenv("EBC_ELL"))
         want_ell = want_ell && std::atoi(env) != 0;
+    // 16-byte rows when no row has more than four entries (EBC_ELL_WIDTH=8: the wide rows all the same)
+    m.ell_width = max_degree <= kEllNarrow ? kEllNarrow : kEllWidth;
+    if (const char *env = std::getenv("EBC_ELL_WIDTH"))
+        if (std::atoi(env) == static_cast<int>(kEllWidth))
+            m.ell_width = kEllWidth;
     const int per_sm = occupancy_for(m.block, m.items, want_ell);
     m.per_sm = per_sm;
     lap("occupancy query");
@@ -1568,7 +1577,8 @@ void CudaSampler::info(std::uint64_t *out) {
     out[3] = m.small.bytes + m.big.bytes + m.graph_bytes + (m.n + 1) * (4 * 2 + 8 + 8 + 16);
     out[4] = static_cast<std::uint64_t>(m.sm_count);
     out[5] = (m.launches & ((std::uint64_t{1} << 48) - 1)) | (static_cast<std::uint64_t>(m.numbering) << 48) |
-             (static_cast<std::uint64_t>(m.d_ell ? 1 : 0) << 52) | (static_cast<std::uint64_t>(m.items) << 56);
+             (static_cast<std::uint64_t>(m.d_ell ? 1 : 0) << 52) |
+             (static_cast<std::uint64_t>(m.d_ell && m.ell_width == kEllNarrow ? 1 : 0) << 53) | (static_cast<std::uint64_t>(m.items) << 56);
 }
 
 void *CudaSampler::stream_handle() { return impl_->s_sample; }

@@ -40,7 +40,8 @@ constexpr u32 kMaxTileSlots = 4096;        // BLOCK * ITEMS never exceeds this
 constexpr u32 kFlagUseBitmap = 2u;        // per-slot visited bitmaps are maintained and used by probe_level
 constexpr u32 kFlagMaterializeFinal = 1u; // always settle the final level (state dumps, exact V_set / F_chk)
 constexpr u32 kFlagStats = 4u;            // launch the kernels that keep work counters, sample records, paths and state-dump bookkeeping
-constexpr u32 kEllWidth = 8;               // entries per fixed-stride row (SamplerParams::ell)
+constexpr u32 kEllWidth = 8;               // entries per fixed-stride row (SamplerParams::ell), at most ...
+constexpr u32 kEllNarrow = 4;              // ... and on graphs of maximum degree <= 4 (SamplerParams::ell_width): 16-byte rows
 constexpr u32 kEllRevShift = 26;           // bits 26..28 of an entry: position of the reverse arc in the target's row
 constexpr u32 kEllDegShift = 29;           // bits 29..31: degree of the target, minus one
 constexpr u32 kEllIdMask = (1u << kEllRevShift) - 1;
@@ -77,7 +78,10 @@ struct SamplerParams {
     // row's end.  A row is one 32-byte sector at a computable address; the degree of a settled vertex comes with the
     // entry that discovered it, and the reverse position lets it remember which of its own entries lead back to
     // its discoverers (expand_level_ell in sampler_kernels.cuh).
+    // ell_width = 8, or 4 when no row has more than four entries (a 2-D lattice): row v is then the 16 bytes at
+    // ell + 4 v, two rows per sector, the whole table half the size (config 3: 64 MB, below the L2 capacity).
     const u32 *ell;
+    u32 ell_width;
     u32 *pm;       // [slots][2][pm_words] with fixed-stride rows: per settled vertex (indexed like list, one byte each)
                    // the mask of row entries that lead to its parents
     u64 pm_words;

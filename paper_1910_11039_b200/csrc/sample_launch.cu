@@ -30,11 +30,18 @@ namespace ebc {
 template <int ITEMS> static void launch_one(const SamplerParams &p, u32 grid, cudaStream_t stream) {
     const bool stats = (p.flags & kFlagStats) != 0;
 #if EBC_HAVE_FIXED
-    if (p.ell) {
-        if (stats)
-            with_stats::sample_kernel<EBC_SHAPE_BLOCK, 2, false, true><<<grid, EBC_SHAPE_BLOCK, 0, stream>>>(p);
-        else
-            lean::sample_kernel<EBC_SHAPE_BLOCK, 2, false, true><<<grid, EBC_SHAPE_BLOCK, 0, stream>>>(p);
+    if (p.ell) { // (rows of eight or of four entries: SamplerParams::ell_width)
+        if (p.ell_width == kEllNarrow) {
+            if (stats)
+                with_stats::sample_kernel<EBC_SHAPE_BLOCK, 2, false, kEllNarrow><<<grid, EBC_SHAPE_BLOCK, 0, stream>>>(p);
+            else
+                lean::sample_kernel<EBC_SHAPE_BLOCK, 2, false, kEllNarrow><<<grid, EBC_SHAPE_BLOCK, 0, stream>>>(p);
+        } else {
+            if (stats)
+                with_stats::sample_kernel<EBC_SHAPE_BLOCK, 2, false, kEllWidth><<<grid, EBC_SHAPE_BLOCK, 0, stream>>>(p);
+            else
+                lean::sample_kernel<EBC_SHAPE_BLOCK, 2, false, kEllWidth><<<grid, EBC_SHAPE_BLOCK, 0, stream>>>(p);
+        }
         return;
     }
 #endif
@@ -72,10 +79,13 @@ int EBC_CAT(sample_occupancy_b, EBC_SHAPE_BLOCK)(u32 items, bool fixed_rows) {
     if (fixed_rows) {
 #if EBC_HAVE_FIXED
         int per_sm = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, with_stats::sample_kernel<EBC_SHAPE_BLOCK, 2, false, true>,
+        int narrow = 0; // (both row widths must fit: the width is known only once the rows are built)
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, with_stats::sample_kernel<EBC_SHAPE_BLOCK, 2, false, kEllWidth>,
+                                                          EBC_SHAPE_BLOCK, 0) != cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&narrow, with_stats::sample_kernel<EBC_SHAPE_BLOCK, 2, false, kEllNarrow>,
                                                           EBC_SHAPE_BLOCK, 0) != cudaSuccess)
             return -2;
-        return per_sm;
+        return per_sm < narrow ? per_sm : narrow;
 #else
         return -1;
 #endif

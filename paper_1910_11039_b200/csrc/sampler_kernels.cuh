@@ -799,14 +799,16 @@ __device__ __forceinline__ u64 sum_frontier_degrees(const SamplerParams &p, cons
 //    frontier's pending edges (sampler.cpp:95,102) and the bound behind `sigma_small` are sums over registers:
 //    sum_frontier_degrees -- two more dependent round trips per level -- is not needed.
 // Sets ex.pending, sh.prev_pending[e] and sh.sigma_small[e] itself.
-template <int BLOCK, int ITEMS>
+// RW = entries per row (SamplerParams::ell_width): 8, or 4 -- one 16-byte load per row, half the tables, no second
+// entry group.
+template <int BLOCK, int ITEMS, int RW>
 __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRegs &ex, const SideRegs &ot, u32 *contact,
                                  u32 &contact_n, BlockShared<BLOCK, ITEMS> &sh, WorkRegs &wk) {
-    constexpr u32 W = kEllWidth;
+    constexpr u32 W = RW;
     constexpr u32 KEYS = BLOCK * W; // candidates per chunk, at most; also the number of hash slots
-    constexpr u32 HBITS = BLOCK == 32 ? 8 : BLOCK == 64 ? 9 : 10;
+    constexpr u32 HBITS = (BLOCK == 32 ? 5 : BLOCK == 64 ? 6 : 7) + (W == 8 ? 3 : 2);
     constexpr int WARPS = BLOCK / 32;
-    static_assert((1u << HBITS) == KEYS && W == 8, "hash table size; a row is two 16-byte loads");
+    static_assert((1u << HBITS) == KEYS && (W == 8 || W == 4), "hash table size; a row is one or two 16-byte loads");
     using Shared = BlockShared<BLOCK, ITEMS>;
     static_assert(sizeof(u32) * 3 * KEYS <= offsetof(Shared, c_sig) + sizeof(sh.c_sig) - offsetof(Shared, f_key) &&
                       offsetof(Shared, c_sig) + sizeof(sh.c_sig) - offsetof(Shared, f_key) ==
@@ -837,9 +839,9 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
         EBC_STAT(sh.ws[kW_E_bfs] += ex.pending;) // the frontier's adjacency entries
     }
     const uint4 empty4 = make_uint4(kEllEmpty, kEllEmpty, kEllEmpty, kEllEmpty);
-    uint4 *h_mine = reinterpret_cast<uint4 *>(tab + KEYS) + tid; // this thread clears h_mine[0], [BLOCK], [2 BLOCK], [3 BLOCK] (hv and hk)
+    uint4 *h_mine = reinterpret_cast<uint4 *>(tab + KEYS) + tid; // this thread clears h_mine[0], [BLOCK], ... [(W/2 - 1) BLOCK] (hv and hk)
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < static_cast<int>(W / 2); ++q)
         h_mine[q * BLOCK] = empty4;
     __syncthreads();
     const u32 key0 = tid * W;
@@ -852,8 +854,9 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
     uint4 a_nxt = empty4, b_nxt = empty4;
     if (fb + tid < fe) {
         const u32 u = ld_cg(ex.pp->list + fb + tid);
-        a_nxt = __ldg(rows + 2 * static_cast<u64>(u));
-        b_nxt = __ldg(rows + 2 * static_cast<u64>(u) + 1);
+        a_nxt = __ldg(rows + (W / 4) * static_cast<u64>(u));
+        if constexpr (W == 8)
+            b_nxt = __ldg(rows + 2 * static_cast<u64>(u) + 1);
     }
     u32 u_nxt = fb + BLOCK + tid < fe ? ld_cg(ex.pp->list + fb + BLOCK + tid) : 0u;
     const unsigned char *pm_in = reinterpret_cast<const unsigned char *>(ex.pp->pm);
@@ -868,15 +871,16 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
         const u32 parents = i < fe ? __ldcg(pm_in + i) : 0u;
         a_nxt = empty4, b_nxt = empty4;
         if (i + BLOCK < fe) {
-            a_nxt = __ldg(rows + 2 * static_cast<u64>(u_nxt));
-            b_nxt = __ldg(rows + 2 * static_cast<u64>(u_nxt) + 1);
+            a_nxt = __ldg(rows + (W / 4) * static_cast<u64>(u_nxt));
+            if constexpr (W == 8)
+                b_nxt = __ldg(rows + 2 * static_cast<u64>(u_nxt) + 1);
         }
         u_nxt = i + 2 * BLOCK < fe ? ld_cg(ex.pp->list + i + 2 * BLOCK) : 0u;
         // Entries are handled in two groups of four; the second one exists in few warps (a row of more than four
         // entries), and its code is a copy of the first with other constants -- executed rarely, it costs no
         // instruction-cache space worth mentioning, while a loop over the groups costs every access a run-time
         // shift or select.
-        const bool two = __any_sync(0xffffffffu, b.x != kEllEmpty);
+        const bool two = W == 8 && __any_sync(0xffffffffu, b.x != kEllEmpty);
         // ---- trip 3: labels; candidates enter the hash set ----
         u32 cand = 0, ccand = 0; // bit k: entry k is unvisited on this side / and visited on the other one
         u32 n_edges = 0;         // level edges of this thread in this chunk
@@ -918,8 +922,9 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
             }
         };
         classify(std::integral_constant<int, 0>{}, a);
-        if (two)
-            classify(std::integral_constant<int, 1>{}, b);
+        if constexpr (W == 8)
+            if (two)
+                classify(std::integral_constant<int, 1>{}, b);
         n_edges += __popc(cand);
         n_lvl += n_edges;
         {
@@ -947,8 +952,9 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
         };
         if (cand & 0x0fu)
             resolve(std::integral_constant<int, 0>{});
-        if (cand & 0xf0u)
-            resolve(std::integral_constant<int, 1>{});
+        if constexpr (W == 8)
+            if (cand & 0xf0u)
+                resolve(std::integral_constant<int, 1>{});
         const u32 packed = __popc(win) | (__popc(win & ccand) << 16);
         u32 incl = packed;
 #pragma unroll
@@ -1005,10 +1011,11 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
         };
         if (win & 0x0fu)
             settle(std::integral_constant<int, 0>{}, a);
-        if (win & 0xf0u)
-            settle(std::integral_constant<int, 1>{}, b);
+        if constexpr (W == 8)
+            if (win & 0xf0u)
+                settle(std::integral_constant<int, 1>{}, b);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) // (every thread read the hash set before the scan's barrier / shuffles)
+        for (int q = 0; q < static_cast<int>(W / 2); ++q) // (every thread read the hash set before the scan's barrier / shuffles)
             h_mine[q * BLOCK] = empty4;
         __syncthreads(); // settled vertices, kv and the cleared hash set are visible
         auto add_sigma = [&](auto G, const uint4 &r) { // later discoverers of a vertex settled in this chunk (sampler.cpp:97-98)
@@ -1025,8 +1032,9 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
         };
         if (cand & ~win & 0x0fu)
             add_sigma(std::integral_constant<int, 0>{}, a);
-        if (cand & ~win & 0xf0u)
-            add_sigma(std::integral_constant<int, 1>{}, b);
+        if constexpr (W == 8)
+            if (cand & ~win & 0xf0u)
+                add_sigma(std::integral_constant<int, 1>{}, b);
         cnt += winners;
         contact_n += ctot;
     }
@@ -1801,7 +1809,7 @@ __device__ void walk_side(const SamplerParams &p, const u32 *lab, int x, const S
 // (the warps compute the same step redundantly: no shared memory, no block barrier, and the random stream -- which
 // all threads advance alike -- needs no broadcast).  Per step three dependent trips: the row (one sector), the labels
 // of its targets, sigma of the predecessors; the pick is an 8-lane prefix scan in row (= CSR) order (sampler.cpp:139-151).
-template <int BLOCK, int ITEMS>
+template <int BLOCK, int ITEMS, int RW>
 __device__ void walk_side_ell(const SamplerParams &p, const u32 *lab, int x, const SideRegs &sd, u32 u, u32 d,
                               SampleStream &rng, u32 *path_out, long long pos, int pos_step, u32 &emitted,
                               BlockShared<BLOCK, ITEMS> &sh, WorkRegs &wk) {
@@ -1825,7 +1833,7 @@ __device__ void walk_side_ell(const SamplerParams &p, const u32 *lab, int x, con
             })
         } else {
             const u32 lo = ld_cg(lvl + (d - 1)), span = ld_cg(lvl + d) - lo;
-            const u32 ent = k < kEllWidth ? __ldg(p.ell + kEllWidth * static_cast<u64>(u) + k) : kEllEmpty;
+            const u32 ent = k < RW ? __ldg(p.ell + RW * static_cast<u64>(u) + k) : kEllEmpty;
             const u32 w = ent & kEllIdMask;
             u64 sg = 0;
             bool pred = false;
@@ -1847,7 +1855,7 @@ __device__ void walk_side_ell(const SamplerParams &p, const u32 *lab, int x, con
             u64 plo = sg;
             u32 phi = 0;
 #pragma unroll
-            for (int o = 1; o < static_cast<int>(kEllWidth); o <<= 1) {
+            for (int o = 1; o < RW; o <<= 1) {
                 const u64 tlo = __shfl_up_sync(0xffffffffu, plo, o);
                 const u32 thi = __shfl_up_sync(0xffffffffu, phi, o);
                 if (k >= static_cast<u32>(o)) {
@@ -1856,12 +1864,12 @@ __device__ void walk_side_ell(const SamplerParams &p, const u32 *lab, int x, con
                     plo = nlo;
                 }
             }
-            const u64 tot_lo = __shfl_sync(0xffffffffu, plo, kEllWidth - 1);
-            const u32 tot_hi = __shfl_sync(0xffffffffu, phi, kEllWidth - 1);
+            const u64 tot_lo = __shfl_sync(0xffffffffu, plo, RW - 1);
+            const u32 tot_hi = __shfl_sync(0xffffffffu, phi, RW - 1);
             const u128 total = (static_cast<u128>(tot_hi) << 64) | tot_lo;
             const u128 r = uniform_below_u128(rng, total); // sampler.cpp:142
             const u128 mine = (static_cast<u128>(phi) << 64) | plo;
-            const u32 hit = __ballot_sync(0xffffffffu, pred && mine > r) & ((1u << kEllWidth) - 1);
+            const u32 hit = __ballot_sync(0xffffffffu, pred && mine > r) & ((1u << RW) - 1);
             chosen = __shfl_sync(0xffffffffu, w, __ffs(hit) - 1); // first prefix above r (a predecessor exists: total > 0)
         }
         u = chosen;
@@ -1889,7 +1897,7 @@ __device__ void walk_side_ell(const SamplerParams &p, const u32 *lab, int x, con
 #ifndef EBC_FIXED_WARPS_PER_SM
 #define EBC_FIXED_WARPS_PER_SM 32
 #endif
-template <int BLOCK, bool FIXED> constexpr int min_blocks_per_sm() {
+template <int BLOCK, int FIXED> constexpr int min_blocks_per_sm() {
     constexpr int warps = FIXED ? EBC_FIXED_WARPS_PER_SM : EBC_WARPS_PER_SM;
     return (warps * 32) / BLOCK > 0 ? (warps * 32) / BLOCK : 1;
 }
@@ -1899,7 +1907,7 @@ template <int BLOCK, bool FIXED> constexpr int min_blocks_per_sm() {
 // FIXED: the graph has fixed-stride rows (SamplerParams::ell).  That kernel consists of expand_level_ell, the
 // contact-list meet and the walk only -- no read-only probe (a lattice-like search does not end in a level much
 // wider than the ones before), no general expansion, no bitmaps: a third of the instruction footprint.
-template <int BLOCK, int ITEMS, bool BITS, bool FIXED = false>
+template <int BLOCK, int ITEMS, bool BITS, int FIXED = 0>
 __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) sample_kernel(const SamplerParams p) {
     static_assert(!(FIXED && BITS) && (!FIXED || BLOCK <= 128), "fixed-stride rows: no bitmaps, at most 128 threads");
     __shared__ BlockShared<BLOCK, ITEMS> sh;
@@ -2136,7 +2144,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) samp
             }
             bool ok;
             if constexpr (FIXED) // (also takes the new frontier's pending edges)
-                ok = expand_level_ell<BLOCK, ITEMS>(p, sh.lab, e, side[e], side[1 - e], sh.contact, contact_n, sh, wk);
+                ok = expand_level_ell<BLOCK, ITEMS, FIXED>(p, sh.lab, e, side[e], side[1 - e], sh.contact, contact_n, sh, wk);
             else
                 ok = expand_level<BLOCK, ITEMS, BITS>(p, sh.lab, sh.bits, vf, e, side[e], side[1 - e], sh.contact, contact_n, sh, wk);
             if (!ok) {
@@ -2256,7 +2264,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) samp
             for (int x = 0; x < 2; ++x) {
                 const SideRegs sd = x == 0 ? side[0] : side[1];
                 if constexpr (FIXED)
-                    walk_side_ell<BLOCK, ITEMS>(p, sh.lab, x, sd, meet, x == 0 ? dist_f : dist_b, rng,
+                    walk_side_ell<BLOCK, ITEMS, FIXED>(p, sh.lab, x, sd, meet, x == 0 ? dist_f : dist_b, rng,
                                                 p.paths ? p.paths + local * p.path_stride : nullptr,
                                                 x == 0 ? static_cast<long long>(dist_f) - 2 : static_cast<long long>(dist_f),
                                                 x == 0 ? -1 : +1, emitted, sh, wk);

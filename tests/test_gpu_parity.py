@@ -313,6 +313,48 @@ def test_fixed_stride_rows_samples_state_and_work_counters(block, monkeypatch):
     s.close()
 
 
+@pytest.mark.parametrize("block,width", [(32, 4), (64, 4), (128, 4), (64, 8)])
+def test_fixed_stride_rows_of_four_entries(block, width, monkeypatch):
+    """Maximum degree <= 4 (a 2-D lattice with holes, here disconnected as well): rows are stored as 16 bytes
+    (SamplerParams::ell_width = 4, kernel variant FIXED = 4: one entry group, half the dedup tables); EBC_ELL_WIDTH=8
+    keeps the 32-byte rows.  Samples, paths, frames, all work counters and the dist / sigma arrays equal the oracle's."""
+    if width == 8:
+        monkeypatch.setenv("EBC_ELL_WIDTH", "8")
+    off, tg = grid_graph(61, 47, drop=0.12, seed=5)
+    assert np.diff(off).max() == 4
+    g = ebc.Graph.from_csr(off, tg)
+    o = Oracle(off, tg)
+    s, _ = check_samples((off, tg), 500, ebc.RunConfig(block_threads=block, slots=8))
+    assert s.info()["fixed_rows"] and s.info()["fixed_row_width"] == width
+    s.close()
+    s = ebc.Sampler(g, ebc.RunConfig(block_threads=block))
+    s.sample(SEED, 1000, 6000)
+    assert np.array_equal(s.read_frame(0), o.accumulate(SEED, 1000, 6000))
+    w, ow = s.work(), o.work()
+    for i, k in enumerate(ebc.WORK_NAMES[:11]):
+        assert w[k] == int(ow[i]), k
+    s.close()
+    s = ebc.Sampler(g, ebc.RunConfig(block_threads=block, work_counters=0))  # the kernels without statistics
+    s.sample(SEED, 1000, 6000)
+    assert np.array_equal(s.read_frame(0), o.accumulate(SEED, 1000, 6000))
+    s.close()
+    s1 = ebc.Sampler(g, ebc.RunConfig(block_threads=block, slots=1))
+    for i in range(10):
+        s1.sample_debug(SEED, i, 1)
+        o.sample(SEED, i)
+        for side in (0, 1):
+            d, sg = s1.last_state(side)
+            od, osg = o.last_state(side)
+            assert np.array_equal(d, od) and np.array_equal(sg, osg), (i, side)
+    s1.close()
+    for off2, tg2 in (path_graph(900), cycle_graph(901), grid_graph(40, 40)):  # degree 2 throughout; a full lattice
+        s = ebc.Sampler(ebc.Graph.from_csr(off2, tg2), ebc.RunConfig(block_threads=block))
+        assert s.info()["fixed_row_width"] == width
+        s.sample(SEED, 0, 3000)
+        assert np.array_equal(s.read_frame(0), Oracle(off2, tg2).accumulate(SEED, 0, 3000))
+        s.close()
+
+
 def test_fixed_stride_rows_need_a_symmetric_graph():
     """An arc without its reverse has no reverse position to record: the sampler notices while it builds the rows and
     runs the general kernel instead (validate=0 adopts the CSR as it is)."""
