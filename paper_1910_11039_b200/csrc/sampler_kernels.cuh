@@ -1439,18 +1439,31 @@ __device__ u32 meet_from_edges(const u32 *edges, u32 m, u32 olo, u32 ohi, u32 *m
     return members;
 }
 
-// The same for a probed final level with more contact edges than meet_from_edges holds in shared
-// memory (R-MAT-20: 6.5 % of the samples, R-MAT-24: 16 % -- the ones with the largest final levels, which
-// would otherwise be expanded and settled in full).  Works in the slot's global arrays:
-//  * a member's other-side idx oi is unique and lies in [olo, ohi), so oi - olo indexes two scratch
-//    arrays (unused tails of the two sides' sigma arrays): first[] = smallest discovery key among the
-//    vertex's contact edges, sum[] = saturating sum of the parents' sigma;
-//  * the edge whose key equals first[] represents its vertex; the representatives are written to
-//    meetbuf as {key hi, key lo, v, oi}, sorted by key with a bitonic network (one CTA, global memory,
-//    padded to a power of two), and rewritten in place as {v, oi, sigma lo, sigma hi}.
+// A probed final level with more contact edges than meet_from_edges holds in shared memory (R-MAT-20: a fifth of
+// the samples at one warp per sample, R-MAT-24: 16 % -- the ones with the largest final levels, which would otherwise
+// be expanded and settled in full).  The reference orders the meet set only to turn `pick` into a vertex
+// (sampler.cpp:124-133: the first member whose inclusive prefix of weights exceeds pick), so the set is not sorted
+// here: it is SEARCHED, a weighted quickselect on the discovery keys in the slot's global arrays.
+//  * a member's other-side idx oi is unique and lies in [olo, ohi), so oi - olo indexes two scratch arrays (unused
+//    tails of the two sides' sigma arrays): first[] = smallest discovery key among the vertex' contact edges
+//    (= its place in the reference's `next`), sum[] = saturating sum of the parents' sigma (sampler.cpp:97-98);
+//  * the edge whose key equals first[] represents its vertex: the members' oi are collected (unordered) in
+//    `scratch`, their weights sum[oi - olo] * sigma_other[oi] are totalled (sampler.cpp:121-123), pick is drawn;
+//  * select: pivot = a member of the active list; S = total weight of the active members with a smaller key.
+//    acc + S > pick: the answer is among those; else acc + S + w(pivot) > pick: it is the pivot; else acc takes
+//    both and the members with a larger key stay.  The two candidate lists are written in the same pass (front and
+//    back of the other buffer).  Contact edges arrive roughly in key order, so the middle of the list is a good
+//    pivot: ~log2(members) passes over geometrically shrinking lists.  Sums that leave 128 bits compare as
+//    "exceeds", exactly like the reference's running subtraction.
+// (Round 1-2 sorted the representatives with a one-CTA bitonic network through shared-memory chunks: ~3 10^5 cycles
+// for 1000 members on a one-warp CTA, a fifth of the time of a config-2 sample.)
+// Returns the chosen member's other-side idx; meet_count and total_weight as the reference would see them.
 template <int BLOCK, int ITEMS>
-__device__ __noinline__ u32 meet_from_edges_large(const u32 *edges, u32 m, u32 olo, u32 ohi, u32 *meetbuf, u64 *first,
-                                                  u64 *sum, BlockShared<BLOCK, ITEMS> &sh) {
+__device__ __noinline__ u32 pick_meet_large(const u32 *edges, u32 m, u32 olo, u32 ohi, u32 *scratch, u64 *first, u64 *sum,
+                                            const u64 *ot_sig, SampleStream &rng, BlockShared<BLOCK, ITEMS> &sh,
+                                            u32 &meet_count, u128 &total_weight) {
+    constexpr int WARPS = BLOCK / 32;
+    constexpr int PER = 4; // list entries per thread and batch: their dependent loads overlap
     const u32 tid = threadIdx.x;
     const u32 L = ohi - olo;
     for (u32 i = tid; i < m; i += BLOCK) {
@@ -1470,132 +1483,134 @@ __device__ __noinline__ u32 meet_from_edges_large(const u32 *edges, u32 m, u32 o
         }
     }
     __syncthreads();
-    u32 count = 0;
-    for (u32 i0 = 0; i0 < m; i0 += BLOCK) {
-        const u32 i = i0 + tid;
-        bool rep[1] = {false};
-        u32 k_hi = 0, k_lo = 0, v = 0, oi = 0;
-        if (i < m) {
+    // Appends to two lists at once: `a` entries go to out_a[na ...] upwards, `b` entries to out_b[... nb] downwards
+    // (out_b points behind its last slot); any order inside a list.  Uniform call; one barrier when WARPS > 1 and
+    // the caller keeps another one before the next call.
+    auto append = [&](const bool (&fa)[PER], const bool (&fb)[PER], const u32 (&val)[PER], u32 *out_a, u32 *out_b, u32 &na,
+                      u32 &nb) {
+        u32 pa[PER], pb[PER], wa = 0, wb = 0;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const u32 ba = __ballot_sync(0xffffffffu, fa[q]), bb = __ballot_sync(0xffffffffu, fb[q]);
+            pa[q] = wa + __popc(ba & lanemask_lt());
+            pb[q] = wb + __popc(bb & lanemask_lt());
+            wa += __popc(ba);
+            wb += __popc(bb);
+        }
+        u32 before = 0, tot = wa | (wb << 16);
+        if (WARPS > 1) {
+            if (lane_id() == 0)
+                sh.warp_cnt[tid >> 5] = tot; // (at most PER * 32 of each kind per warp, PER * BLOCK <= 2048 in all)
+            __syncthreads();
+            tot = 0;
+#pragma unroll 1
+            for (u32 w = 0; w < static_cast<u32>(WARPS); ++w) {
+                const u32 c = sh.warp_cnt[w];
+                before += w < (tid >> 5) ? c : 0u;
+                tot += c;
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            if (fa[q])
+                st_cg(out_a + na + (before & 0xffffu) + pa[q], val[q]);
+            if (fb[q])
+                st_cg(out_b - 1 - (nb + (before >> 16) + pb[q]), val[q]);
+        }
+        na += tot & 0xffffu;
+        nb += tot >> 16;
+    };
+    const bool none[PER] = {false, false, false, false};
+    u32 count = 0, unused = 0;
+    u128 wsum = 0;
+    for (u32 i0 = 0; i0 < m; i0 += PER * BLOCK) { // the representatives: members of the meet set
+        bool rep[PER];
+        u32 oi[PER];
+        u64 key[PER];
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const u32 i = i0 + q * BLOCK + tid;
             const u32 *w = edges + 6 * static_cast<u64>(i);
-            oi = ld_cg(w + 3);
-            if (oi - olo < L) {
-                k_hi = ld_cg(w);
-                k_lo = ld_cg(w + 1);
-                v = ld_cg(w + 2);
-                rep[0] = ld_cg(first + (oi - olo)) == ((static_cast<u64>(k_hi) << 32) | k_lo);
-            }
+            oi[q] = i < m ? ld_cg(w + 3) : olo + L;
+            key[q] = oi[q] - olo < L ? (static_cast<u64>(ld_cg(w)) << 32) | ld_cg(w + 1) : 0ull;
         }
-        u32 rank[1];
-        const u32 tot = block_ranks<BLOCK, 1>(rep, rank, sh.warp_cnt);
-        if (rep[0]) {
-            u32 *w = meetbuf + 4 * static_cast<u64>(count + rank[0]);
-            st_cg(w + 0, k_hi);
-            st_cg(w + 1, k_lo);
-            st_cg(w + 2, v);
-            st_cg(w + 3, oi);
-        }
-        count += tot;
-        __syncthreads();
-    }
-    u32 n2 = 1;
-    while (n2 < count)
-        n2 <<= 1;
-    for (u32 i = count + tid; i < n2; i += BLOCK) { // padding sorts last
-        st_cg(meetbuf + 4 * static_cast<u64>(i), 0xffffffffu);
-        st_cg(meetbuf + 4 * static_cast<u64>(i) + 1, 0xffffffffu);
-    }
-    __syncthreads();
-    // Bitonic network over n2 entries.  Steps whose partner distance is below the chunk length run in shared
-    // memory (the arrays of meet_from_edges), chunk by chunk; only the few wider steps of a member set that
-    // does not fit go through global memory.  Usually n2 <= len and the whole sort is one chunk.
-    const u32 len = n2 < static_cast<u32>(FinalEdgeCap<BLOCK>::value) ? n2 : static_cast<u32>(FinalEdgeCap<BLOCK>::value);
-    auto chunk_in = [&](u32 base) {
-        for (u32 i = tid; i < len; i += BLOCK) {
-            const u32 *w = meetbuf + 4 * static_cast<u64>(base + i);
-            sh.f_key[i] = (static_cast<u64>(ld_cg(w)) << 32) | ld_cg(w + 1);
-            sh.f_v[i] = ld_cg(w + 2);
-            sh.f_o[i] = ld_cg(w + 3);
-        }
-        __syncthreads();
-    };
-    auto chunk_out = [&](u32 base) {
-        for (u32 i = tid; i < len; i += BLOCK) {
-            u32 *w = meetbuf + 4 * static_cast<u64>(base + i);
-            st_cg(w + 0, static_cast<u32>(sh.f_key[i] >> 32));
-            st_cg(w + 1, static_cast<u32>(sh.f_key[i]));
-            st_cg(w + 2, sh.f_v[i]);
-            st_cg(w + 3, sh.f_o[i]);
-        }
-        __syncthreads();
-    };
-    auto chunk_steps = [&](u32 base, u32 k, u32 j_from) { // steps j_from, j_from/2, ..., 1 of stage k on one chunk
-#pragma unroll 1
-        for (u32 j = j_from; j > 0; j >>= 1) {
-            for (u32 t = tid; t < (len >> 1); t += BLOCK) {
-                const u32 i = ((t & ~(j - 1)) << 1) | (t & (j - 1)), q = i | j; // t with a zero inserted at bit log2(j)
-                const u64 ka = sh.f_key[i], kb = sh.f_key[q];
-                if ((ka > kb) == (((base + i) & k) == 0)) {
-                    sh.f_key[i] = kb;
-                    sh.f_key[q] = ka;
-                    const u32 va = sh.f_v[i], oa = sh.f_o[i];
-                    sh.f_v[i] = sh.f_v[q];
-                    sh.f_o[i] = sh.f_o[q];
-                    sh.f_v[q] = va;
-                    sh.f_o[q] = oa;
-                }
-            }
+#pragma unroll
+        for (int q = 0; q < PER; ++q)
+            rep[q] = oi[q] - olo < L && ld_cg(first + (oi[q] - olo)) == key[q];
+#pragma unroll
+        for (int q = 0; q < PER; ++q)
+            if (rep[q])
+                wsum += static_cast<u128>(ld_cg(sum + (oi[q] - olo))) * ld_cg(ot_sig + oi[q]);
+        append(rep, none, oi, scratch, scratch, count, unused);
+        if (WARPS > 1)
             __syncthreads();
-        }
-    };
-#pragma unroll 1
-    for (u32 base = 0; base < n2; base += len) { // stages 2 .. len, chunk by chunk
-        chunk_in(base);
-#pragma unroll 1
-        for (u32 k = 2; k <= len; k <<= 1)
-            chunk_steps(base, k, k >> 1);
-        chunk_out(base);
     }
+    u64 wlo, whi, wov;
+    block_sum_u128<BLOCK>(wsum, wlo, whi, wov, sh.red64);
+    __syncthreads(); // (also: the list is visible)
+    total_weight = wov ? ~static_cast<u128>(0) : ((static_cast<u128>(whi) << 64) | wlo);
+    meet_count = count;
+    const u128 pick = uniform_below_u128(rng, total_weight); // sampler.cpp:124
+    u32 *cur = scratch, *oth = scratch + count; // the active list and the buffer the next one is written to
+    u32 *cur_buf = scratch;
+    u32 n_act = count;
+    u128 acc = 0; // exact weight of the members below the active keys; acc <= pick
+    u32 ans = ld_cg(scratch);
 #pragma unroll 1
-    for (u32 k = len << 1; k <= n2 && k != 0; k <<= 1) { // wider stages: global steps down to the chunk length
+    while (n_act > 1) {
+        const u32 op = ld_cg(cur + (n_act >> 1));
+        const u64 kp = ld_cg(first + (op - olo));
+        u128 s_lt = 0;
+        u32 n_lt = 0, n_gt = 0;
 #pragma unroll 1
-        for (u32 j = k >> 1; j >= len; j >>= 1) {
-            for (u32 t = tid; t < (n2 >> 1); t += BLOCK) {
-                const u32 i = ((t & ~(j - 1)) << 1) | (t & (j - 1));
-                u32 *a = meetbuf + 4 * static_cast<u64>(i), *b = meetbuf + 4 * static_cast<u64>(i | j);
-                const u32 a0 = ld_cg(a), a1 = ld_cg(a + 1), b0 = ld_cg(b), b1 = ld_cg(b + 1);
-                const u64 ka = (static_cast<u64>(a0) << 32) | a1, kb = (static_cast<u64>(b0) << 32) | b1;
-                if ((ka > kb) == ((i & k) == 0)) {
-                    const u32 a2 = ld_cg(a + 2), a3 = ld_cg(a + 3), b2 = ld_cg(b + 2), b3 = ld_cg(b + 3);
-                    st_cg(a, b0);
-                    st_cg(a + 1, b1);
-                    st_cg(a + 2, b2);
-                    st_cg(a + 3, b3);
-                    st_cg(b, a0);
-                    st_cg(b + 1, a1);
-                    st_cg(b + 2, a2);
-                    st_cg(b + 3, a3);
-                }
+        for (u32 i0 = 0; i0 < n_act; i0 += PER * BLOCK) {
+            bool lt[PER], gt[PER];
+            u32 oi[PER];
+            u64 key[PER];
+#pragma unroll
+            for (int q = 0; q < PER; ++q) {
+                const u32 i = i0 + q * BLOCK + tid;
+                oi[q] = i < n_act ? ld_cg(cur + i) : op;
             }
-            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < PER; ++q)
+                key[q] = ld_cg(first + (oi[q] - olo));
+#pragma unroll
+            for (int q = 0; q < PER; ++q) {
+                lt[q] = key[q] < kp;
+                gt[q] = key[q] > kp;
+                if (lt[q])
+                    s_lt += static_cast<u128>(ld_cg(sum + (oi[q] - olo))) * ld_cg(ot_sig + oi[q]);
+            }
+            append(lt, gt, oi, oth, oth + n_act, n_lt, n_gt);
+            if (WARPS > 1)
+                __syncthreads();
         }
-#pragma unroll 1
-        for (u32 base = 0; base < n2; base += len) {
-            chunk_in(base);
-            chunk_steps(base, k, len >> 1);
-            chunk_out(base);
+        u64 lo, hi, ov;
+        block_sum_u128<BLOCK>(s_lt, lo, hi, ov, sh.red64);
+        const u128 below = acc + ((static_cast<u128>(hi) << 64) | lo);
+        ans = op;
+        if (ov || below < acc || below > pick) { // the answer has a smaller key than the pivot
+            u32 *t = cur_buf;
+            cur = oth, cur_buf = oth, oth = t;
+            n_act = n_lt;
+        } else {
+            const u128 wp = static_cast<u128>(ld_cg(sum + (op - olo))) * ld_cg(ot_sig + op);
+            const u128 incl = below + wp;
+            if (incl < below || incl > pick || n_gt == 0)
+                n_act = 0; // the pivot it is
+            else {
+                acc = incl;
+                u32 *t = cur_buf;
+                cur = oth + (n_act - n_gt), cur_buf = oth, oth = t;
+                n_act = n_gt;
+            }
         }
+        __syncthreads(); // the new lists are visible; red64 and warp_cnt may be reused
+        if (n_act == 1)
+            ans = ld_cg(cur);
     }
-    for (u32 i = tid; i < count; i += BLOCK) {
-        u32 *w = meetbuf + 4 * static_cast<u64>(i);
-        const u32 v = ld_cg(w + 2), oi = ld_cg(w + 3);
-        const u64 sg = ld_cg(sum + (oi - olo));
-        st_cg(w + 0, v);
-        st_cg(w + 1, oi);
-        st_cg(w + 2, static_cast<u32>(sg));
-        st_cg(w + 3, static_cast<u32>(sg >> 32));
-    }
-    __syncthreads();
-    return count;
+    return ans;
 }
 
 // Meet set of a normally expanded final level: the contacts (in discovery order)
@@ -2190,17 +2205,25 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) samp
             }
             __syncthreads();
 
-            // meet set in discovery order (sampler.cpp:109-113) -> sh.meetbuf
-            u32 meet_count;
+            u32 meet_count = 0;
+            u128 total_weight = 0;
+            u32 meet = 0xffffffffu;
+            bool searched = false; // a large probed level: the meet vertex is selected, the set is never ordered
             EBC_STAT(if (tid == 0 && probed && edge_n > static_cast<u32>(FinalEdgeCap<BLOCK>::value)) sh.rec.flags |= 8u;) // resolved in global memory
+            if constexpr (!FIXED)
+                if (probed && edge_n > static_cast<u32>(FinalEdgeCap<BLOCK>::value)) {
+                    const u32 oi = pick_meet_large<BLOCK, ITEMS>(sh.contact, edge_n, olo, ohi, sh.meetbuf, ex.pp->sig + ex.cnt,
+                                                                 ot.pp->sig + ot.cnt, ot.pp->sig, rng, sh, meet_count, total_weight);
+                    meet = ld_cg(ot.pp->list + oi); // (a member's other-side idx names it)
+                    searched = true;
+                }
+            if (!searched) {
+            // meet set in discovery order (sampler.cpp:109-113) -> sh.meetbuf
             if constexpr (FIXED)
                 meet_count = meet_from_contacts<BLOCK, ITEMS>(sh.contact, contact_n, ex, olo, ohi, sh.meetbuf, sh);
             else
                 meet_count = !probed ? meet_from_contacts<BLOCK, ITEMS>(sh.contact, contact_n, ex, olo, ohi, sh.meetbuf, sh)
-                             : edge_n <= static_cast<u32>(FinalEdgeCap<BLOCK>::value)
-                                 ? meet_from_edges<BLOCK, ITEMS>(sh.contact, edge_n, olo, ohi, sh.meetbuf, sh)
-                                 : meet_from_edges_large<BLOCK, ITEMS>(sh.contact, edge_n, olo, ohi, sh.meetbuf,
-                                                                       ex.pp->sig + ex.cnt, ot.pp->sig + ot.cnt, sh);
+                                     : meet_from_edges<BLOCK, ITEMS>(sh.contact, edge_n, olo, ohi, sh.meetbuf, sh);
 
             // total weight over the meet set (sampler.cpp:121-123), saturating at 2^128-1
             u128 wsum = 0;
@@ -2212,19 +2235,12 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) samp
             u64 wlo, whi, wov;
             block_sum_u128<BLOCK>(wsum, wlo, whi, wov, sh.red64);
             __syncthreads();
-            const u128 total_weight = wov ? ~static_cast<u128>(0) : ((static_cast<u128>(whi) << 64) | wlo);
-            if (tid == 0) {
-                EBC_STAT(sh.rec.weight_lo = static_cast<u64>(total_weight);)
-                EBC_STAT(sh.rec.weight_hi = static_cast<u64>(total_weight >> 64);)
-                EBC_STAT(sh.rec.meet_count = meet_count;)
-                EBC_STAT(sh.ws[kW_M] += meet_count;)
-            }
+            total_weight = wov ? ~static_cast<u128>(0) : ((static_cast<u128>(whi) << 64) | wlo);
 
             // pick and ordered prefix search (sampler.cpp:124-133).  pick < total_weight <=
             // sum of the weights, so a hit always exists; the reference's fall-through
             // default (last meet vertex, sampler.cpp:125) is kept for completeness.
             const u128 pick = uniform_below_u128(rng, total_weight);
-            u32 meet = 0xffffffffu;
             {
                 u128 running = 0;
                 bool running_ovf = false;
@@ -2249,6 +2265,13 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) samp
                 }
                 if (meet == 0xffffffffu)
                     meet = ld_cg(sh.meetbuf + 4 * static_cast<u64>(meet_count - 1));
+            }
+            }
+            if (tid == 0) {
+                EBC_STAT(sh.rec.weight_lo = static_cast<u64>(total_weight);)
+                EBC_STAT(sh.rec.weight_hi = static_cast<u64>(total_weight >> 64);)
+                EBC_STAT(sh.rec.meet_count = meet_count;)
+                EBC_STAT(sh.ws[kW_M] += meet_count;)
             }
             if (tid == 0)
                 EBC_STAT(sh.rec.meet = ext_id(p, meet);)

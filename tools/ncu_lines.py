@@ -33,6 +33,9 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_ou
 rows = list(csv.reader(out.splitlines()))
 hdr = rows[1]; ci = {h: i for i, h in enumerate(hdr)}
 data = rows[2:]
+for k, r in enumerate(data): # (a report with several launches: the first one's table)
+    if not r or r[0] in ("Kernel Name", "Address"):
+        data = data[:k]; break
 base = int(data[0][ci["Address"]], 16) if data[0][ci["Address"]].startswith("0x") else int(data[0][ci["Address"]])
 agg = collections.defaultdict(lambda: [0.0, 0.0, 0.0, 0.0, 0.0])
 sort_col = 4 if "--noinst" in sys.argv else 3 if "--byinst" in sys.argv else 0
