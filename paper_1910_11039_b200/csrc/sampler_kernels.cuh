@@ -84,6 +84,11 @@ __device__ __forceinline__ u64 atom_add_u64(u64 *p, u64 v) {
 __device__ __forceinline__ void red_max_u64(u64 *p, u64 v) {
     asm volatile("red.global.max.u64 [%0], %1;" ::"l"(__cvta_generic_to_global(p)), "l"(v) : "memory");
 }
+__device__ __forceinline__ u64 atom_min_u64(u64 *p, u64 v) {
+    u64 old;
+    asm volatile("atom.global.min.u64 %0, [%1], %2;" : "=l"(old) : "l"(__cvta_generic_to_global(p)), "l"(v) : "memory");
+    return old;
+}
 __device__ __forceinline__ void red_min_u64(u64 *p, u64 v) {
     asm volatile("red.global.min.u64 [%0], %1;" ::"l"(__cvta_generic_to_global(p)), "l"(v) : "memory");
 }
@@ -1094,7 +1099,7 @@ static __device__ __noinline__ void record_contact_edge(u32 *edges, u32 pos, u32
 template <int BLOCK, int ITEMS, bool BITS>
 __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bits, const u32 *vf, int e, const SideRegs &ex,
                            const SideRegs &ot, u32 *edges, u32 edge_cap, BlockShared<BLOCK, ITEMS> &sh, u64 &new_slots,
-                           u64 &total_slots) {
+                           u64 &total_slots, u64 *scr_first, u64 *scr_sum) {
     constexpr u32 G = BITS ? EBC_PROBE_G : 4; // lanes per item
     constexpr u32 NG = BLOCK / G;             // groups per CTA
     constexpr u32 kItemLen = 4 * G;           // adjacency entries per item
@@ -1297,12 +1302,33 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
     total_slots = t_total;
     const u32 found = sh.edge_cnt;
     if (BITS && found > 0 && found <= edge_cap) { // other-side idx of every contact edge, and their minimum
+        // (four edges per thread at a time: the two dependent trips of each overlap.)  More edges than
+        // meet_from_edges takes: the scratch entries pick_meet_large indexes by oi - ot.fb are cleared on the way
+        // (its pass A) -- a contact vertex always sits in the other side's LAST level: had it been expanded there,
+        // its neighbour on this side's frontier would have been a contact one level earlier.
+        const bool clear = scr_first != nullptr && found > static_cast<u32>(FinalEdgeCap<BLOCK>::value);
         u32 lowest = 0xffffffffu;
-        for (u32 i = tid; i < found; i += BLOCK) {
-            u32 *w = edges + 6 * static_cast<u64>(i);
-            const u32 oi = label_idx(ld_cg(lab + ld_cg(w + 2)), ot.base, 1 - e);
-            st_cg(w + 3, oi);
-            lowest = oi < lowest ? oi : lowest;
+#pragma unroll 1
+        for (u32 i0 = 0; i0 < found; i0 += 4 * BLOCK) {
+            u32 v[4], oi[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const u32 i = i0 + k * BLOCK + tid;
+                v[k] = i < found ? ld_cg(edges + 6 * static_cast<u64>(i) + 2) : 0xffffffffu;
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                oi[k] = v[k] != 0xffffffffu ? label_idx(ld_cg(lab + v[k]), ot.base, 1 - e) : 0xffffffffu;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (v[k] != 0xffffffffu) {
+                    st_cg(edges + 6 * static_cast<u64>(i0 + k * BLOCK + tid) + 3, oi[k]);
+                    lowest = oi[k] < lowest ? oi[k] : lowest;
+                    if (clear && oi[k] - ot.fb < ot.cnt - ot.fb) {
+                        st_cg(scr_first + (oi[k] - ot.fb), ~0ull);
+                        st_cg(scr_sum + (oi[k] - ot.fb), static_cast<u64>(0));
+                    }
+                }
         }
         if (lowest != 0xffffffffu)
             atomicMin(&sh.min_contact, lowest);
@@ -1441,66 +1467,56 @@ __device__ u32 meet_from_edges(const u32 *edges, u32 m, u32 olo, u32 ohi, u32 *m
 
 // A probed final level with more contact edges than meet_from_edges holds in shared memory (R-MAT-20: a fifth of
 // the samples at one warp per sample, R-MAT-24: 16 % -- the ones with the largest final levels, which would otherwise
-// be expanded and settled in full).  The reference orders the meet set only to turn `pick` into a vertex
-// (sampler.cpp:124-133: the first member whose inclusive prefix of weights exceeds pick), so the set is not sorted
-// here: it is SEARCHED, a weighted quickselect on the discovery keys in the slot's global arrays.
+// be expanded and settled in full; a hub on the other side's frontier alone brings thousands of contact edges).
+// The reference orders the meet set only to turn `pick` into a vertex (sampler.cpp:124-133: the first member whose
+// inclusive prefix of weights exceeds pick), so the set is not sorted here: it is SEARCHED, a weighted quickselect on
+// the discovery keys.  Everything lives in the slot's global arrays and every pass keeps several independent loads
+// per thread in flight (a pass costs its dependent round trips, not its bytes):
 //  * a member's other-side idx oi is unique and lies in [olo, ohi), so oi - olo indexes two scratch arrays (unused
 //    tails of the two sides' sigma arrays): first[] = smallest discovery key among the vertex' contact edges
 //    (= its place in the reference's `next`), sum[] = saturating sum of the parents' sigma (sampler.cpp:97-98);
-//  * the edge whose key equals first[] represents its vertex: the members' oi are collected (unordered) in
-//    `scratch`, their weights sum[oi - olo] * sigma_other[oi] are totalled (sampler.cpp:121-123), pick is drawn;
-//  * select: pivot = a member of the active list; S = total weight of the active members with a smaller key.
+//  * pass A clears first[] / sum[] where an edge points; pass B does atom.min(first[], key) and adds sigma -- the one
+//    edge of a vertex that still finds ~0 in first[] enters the vertex in the member list;
+//  * pass C turns the member list into records {key, weight = sum * sigma_other (sampler.cpp:121-123), oi} and
+//    totals the weights; pick is drawn;
+//  * select: pivot = a record of the active list; S = total weight of the active records with a smaller key.
 //    acc + S > pick: the answer is among those; else acc + S + w(pivot) > pick: it is the pivot; else acc takes
-//    both and the members with a larger key stay.  The two candidate lists are written in the same pass (front and
+//    both and the records with a larger key stay.  Both candidate lists are written in the same pass (front and
 //    back of the other buffer).  Contact edges arrive roughly in key order, so the middle of the list is a good
 //    pivot: ~log2(members) passes over geometrically shrinking lists.  Sums that leave 128 bits compare as
 //    "exceeds", exactly like the reference's running subtraction.
-// (Round 1-2 sorted the representatives with a one-CTA bitonic network through shared-memory chunks: ~3 10^5 cycles
-// for 1000 members on a one-warp CTA, a fifth of the time of a config-2 sample.)
+// (Rounds 1-2 sorted the representatives with a one-CTA bitonic network through shared-memory chunks and walked the
+// edges one dependent load at a time: 3.3 10^5 cycles per such sample on a one-warp CTA.)
+// `contact`: the 6-word edge records at [0, 6 m) of the slot's 6 aux_cap >= 18 m words; the rest is scratch here.
 // Returns the chosen member's other-side idx; meet_count and total_weight as the reference would see them.
 template <int BLOCK, int ITEMS>
-__device__ __noinline__ u32 pick_meet_large(const u32 *edges, u32 m, u32 olo, u32 ohi, u32 *scratch, u64 *first, u64 *sum,
-                                            const u64 *ot_sig, SampleStream &rng, BlockShared<BLOCK, ITEMS> &sh,
+__device__ __noinline__ u32 pick_meet_large(u32 *contact, u32 m, u32 olo, u32 ohi, u64 *first, u64 *sum, const u64 *ot_sig,
+                                            bool sigma_small, bool cleared, SampleStream &rng, BlockShared<BLOCK, ITEMS> &sh,
                                             u32 &meet_count, u128 &total_weight) {
     constexpr int WARPS = BLOCK / 32;
-    constexpr int PER = 4; // list entries per thread and batch: their dependent loads overlap
+    constexpr int PE = 4; // edges per thread and batch
+    constexpr int PR = 2; // records per thread and batch
     const u32 tid = threadIdx.x;
     const u32 L = ohi - olo;
-    for (u32 i = tid; i < m; i += BLOCK) {
-        const u32 r = ld_cg(edges + 6 * static_cast<u64>(i) + 3) - olo;
-        if (r < L) {
-            st_cg(first + r, ~0ull);
-            st_cg(sum + r, static_cast<u64>(0));
-        }
-    }
-    __syncthreads();
-    for (u32 i = tid; i < m; i += BLOCK) {
-        const u32 *w = edges + 6 * static_cast<u64>(i);
-        const u32 r = ld_cg(w + 3) - olo;
-        if (r < L) {
-            red_min_u64(first + r, (static_cast<u64>(ld_cg(w)) << 32) | ld_cg(w + 1));
-            sat_atomic_add(sum + r, static_cast<u64>(ld_cg(w + 4)) | (static_cast<u64>(ld_cg(w + 5)) << 32), false);
-        }
-    }
-    __syncthreads();
-    // Appends to two lists at once: `a` entries go to out_a[na ...] upwards, `b` entries to out_b[... nb] downwards
-    // (out_b points behind its last slot); any order inside a list.  Uniform call; one barrier when WARPS > 1 and
-    // the caller keeps another one before the next call.
-    auto append = [&](const bool (&fa)[PER], const bool (&fb)[PER], const u32 (&val)[PER], u32 *out_a, u32 *out_b, u32 &na,
-                      u32 &nb) {
-        u32 pa[PER], pb[PER], wa = 0, wb = 0;
+    const u64 *e64 = reinterpret_cast<const u64 *>(contact); // an edge: {position | index << 32, v | oi << 32, sigma}
+    // Positions in two lists for P flagged items per thread: `a` items count upwards from na, `b` items from nb
+    // (any order inside a list).  Uniform call; one barrier when WARPS > 1, and the caller keeps another one
+    // before the next call.
+    auto place = [&](auto P, const bool *fa, const bool *fb, u32 *pa, u32 *pb, u32 &na, u32 &nb) {
+        constexpr int N = decltype(P)::value;
+        u32 wa = 0, wb = 0;
 #pragma unroll
-        for (int q = 0; q < PER; ++q) {
+        for (int q = 0; q < N; ++q) {
             const u32 ba = __ballot_sync(0xffffffffu, fa[q]), bb = __ballot_sync(0xffffffffu, fb[q]);
             pa[q] = wa + __popc(ba & lanemask_lt());
             pb[q] = wb + __popc(bb & lanemask_lt());
             wa += __popc(ba);
             wb += __popc(bb);
         }
-        u32 before = 0, tot = wa | (wb << 16);
+        u32 before = 0, tot = wa | (wb << 16); // (at most 4 * 32 of each kind per warp, 4 * BLOCK <= 2048 in all)
         if (WARPS > 1) {
             if (lane_id() == 0)
-                sh.warp_cnt[tid >> 5] = tot; // (at most PER * 32 of each kind per warp, PER * BLOCK <= 2048 in all)
+                sh.warp_cnt[tid >> 5] = tot;
             __syncthreads();
             tot = 0;
 #pragma unroll 1
@@ -1511,104 +1527,177 @@ __device__ __noinline__ u32 pick_meet_large(const u32 *edges, u32 m, u32 olo, u3
             }
         }
 #pragma unroll
-        for (int q = 0; q < PER; ++q) {
-            if (fa[q])
-                st_cg(out_a + na + (before & 0xffffu) + pa[q], val[q]);
-            if (fb[q])
-                st_cg(out_b - 1 - (nb + (before >> 16) + pb[q]), val[q]);
+        for (int q = 0; q < N; ++q) {
+            pa[q] += na + (before & 0xffffu);
+            pb[q] += nb + (before >> 16);
         }
         na += tot & 0xffffu;
         nb += tot >> 16;
     };
-    const bool none[PER] = {false, false, false, false};
-    u32 count = 0, unused = 0;
-    u128 wsum = 0;
-    for (u32 i0 = 0; i0 < m; i0 += PER * BLOCK) { // the representatives: members of the meet set
-        bool rep[PER];
-        u32 oi[PER];
-        u64 key[PER];
+    if (!cleared) { // (probe_level has done it on the way when it could)
+#pragma unroll 1
+    for (u32 i0 = 0; i0 < m; i0 += PE * BLOCK) { // pass A
+        u32 r[PE];
 #pragma unroll
-        for (int q = 0; q < PER; ++q) {
+        for (int q = 0; q < PE; ++q) {
             const u32 i = i0 + q * BLOCK + tid;
-            const u32 *w = edges + 6 * static_cast<u64>(i);
-            oi[q] = i < m ? ld_cg(w + 3) : olo + L;
-            key[q] = oi[q] - olo < L ? (static_cast<u64>(ld_cg(w)) << 32) | ld_cg(w + 1) : 0ull;
+            r[q] = i < m ? static_cast<u32>(ld_cg(e64 + 3 * static_cast<u64>(i) + 1) >> 32) - olo : L;
         }
 #pragma unroll
-        for (int q = 0; q < PER; ++q)
-            rep[q] = oi[q] - olo < L && ld_cg(first + (oi[q] - olo)) == key[q];
+        for (int q = 0; q < PE; ++q)
+            if (r[q] < L) {
+                st_cg(first + r[q], ~0ull);
+                st_cg(sum + r[q], static_cast<u64>(0));
+            }
+    }
+    }
+    __syncthreads();
+    u32 *members = contact + 16 * static_cast<u64>(m); // other-side idx of every member, unordered
+    u32 count = 0, unused = 0;
+#pragma unroll 1
+    for (u32 i0 = 0; i0 < m; i0 += PE * BLOCK) { // pass B
+        u64 key[PE], sg[PE];
+        u32 oi[PE];
 #pragma unroll
-        for (int q = 0; q < PER; ++q)
-            if (rep[q])
-                wsum += static_cast<u128>(ld_cg(sum + (oi[q] - olo))) * ld_cg(ot_sig + oi[q]);
-        append(rep, none, oi, scratch, scratch, count, unused);
+        for (int q = 0; q < PE; ++q) {
+            const u32 i = i0 + q * BLOCK + tid;
+            const u64 *w = e64 + 3 * static_cast<u64>(i);
+            oi[q] = i < m ? static_cast<u32>(ld_cg(w + 1) >> 32) : olo + L;
+            const u64 k = i < m ? ld_cg(w) : 0ull;
+            key[q] = (k << 32) | (k >> 32);
+            sg[q] = i < m ? ld_cg(w + 2) : 0ull;
+        }
+        bool fresh[PE], none[PE];
+#pragma unroll
+        for (int q = 0; q < PE; ++q) {
+            fresh[q] = oi[q] - olo < L && atom_min_u64(first + (oi[q] - olo), key[q]) == ~0ull;
+            none[q] = false;
+        }
+#pragma unroll
+        for (int q = 0; q < PE; ++q)
+            if (oi[q] - olo < L)
+                sat_atomic_add(sum + (oi[q] - olo), sg[q], sigma_small);
+        u32 pa[PE], pb[PE];
+        place(std::integral_constant<int, PE>{}, fresh, none, pa, pb, count, unused);
+#pragma unroll
+        for (int q = 0; q < PE; ++q)
+            if (fresh[q])
+                st_cg(members + pa[q], oi[q]);
         if (WARPS > 1)
             __syncthreads();
     }
+    __syncthreads();
+    // records of four 8-byte words {key, weight lo, weight hi, oi}: two buffers of `count` records
+    u64 *cur = reinterpret_cast<u64 *>(contact + 8 * static_cast<u64>(m));
+    u64 *oth = reinterpret_cast<u64 *>(contact); // (over the edges, which nobody reads any more)
+    u128 wsum = 0;
+#pragma unroll 1
+    for (u32 i0 = 0; i0 < count; i0 += PR * BLOCK) { // pass C
+        u32 oi[PR];
+#pragma unroll
+        for (int q = 0; q < PR; ++q) {
+            const u32 i = i0 + q * BLOCK + tid;
+            oi[q] = i < count ? ld_cg(members + i) : 0xffffffffu;
+        }
+        u64 key[PR], sm[PR], so[PR];
+#pragma unroll
+        for (int q = 0; q < PR; ++q)
+            key[q] = sm[q] = so[q] = 0;
+#pragma unroll
+        for (int q = 0; q < PR; ++q)
+            if (oi[q] != 0xffffffffu) {
+                key[q] = ld_cg(first + (oi[q] - olo));
+                sm[q] = ld_cg(sum + (oi[q] - olo));
+                so[q] = ld_cg(ot_sig + oi[q]);
+            }
+#pragma unroll
+        for (int q = 0; q < PR; ++q)
+            if (oi[q] != 0xffffffffu) {
+                const u128 w = static_cast<u128>(sm[q]) * so[q];
+                wsum += w;
+                u64 *rec = cur + 4 * static_cast<u64>(i0 + q * BLOCK + tid);
+                st_cg(rec + 0, key[q]);
+                st_cg(rec + 1, static_cast<u64>(w));
+                st_cg(rec + 2, static_cast<u64>(w >> 64));
+                st_cg(rec + 3, static_cast<u64>(oi[q]));
+            }
+    }
     u64 wlo, whi, wov;
     block_sum_u128<BLOCK>(wsum, wlo, whi, wov, sh.red64);
-    __syncthreads(); // (also: the list is visible)
+    __syncthreads(); // (also: the records are visible)
     total_weight = wov ? ~static_cast<u128>(0) : ((static_cast<u128>(whi) << 64) | wlo);
     meet_count = count;
     const u128 pick = uniform_below_u128(rng, total_weight); // sampler.cpp:124
-    u32 *cur = scratch, *oth = scratch + count; // the active list and the buffer the next one is written to
-    u32 *cur_buf = scratch;
+    u64 *cur_buf = cur;
     u32 n_act = count;
     u128 acc = 0; // exact weight of the members below the active keys; acc <= pick
-    u32 ans = ld_cg(scratch);
+    u32 ans = static_cast<u32>(ld_cg(cur + 3));
 #pragma unroll 1
     while (n_act > 1) {
-        const u32 op = ld_cg(cur + (n_act >> 1));
-        const u64 kp = ld_cg(first + (op - olo));
+        const u64 *pv = cur + 4 * static_cast<u64>(n_act >> 1);
+        const u64 kp = ld_cg(pv);
+        const u128 wp = (static_cast<u128>(ld_cg(pv + 2)) << 64) | ld_cg(pv + 1);
+        ans = static_cast<u32>(ld_cg(pv + 3));
         u128 s_lt = 0;
         u32 n_lt = 0, n_gt = 0;
 #pragma unroll 1
-        for (u32 i0 = 0; i0 < n_act; i0 += PER * BLOCK) {
-            bool lt[PER], gt[PER];
-            u32 oi[PER];
-            u64 key[PER];
+        for (u32 i0 = 0; i0 < n_act; i0 += PR * BLOCK) {
+            u64 rec[PR][4];
 #pragma unroll
-            for (int q = 0; q < PER; ++q) {
+            for (int q = 0; q < PR; ++q) {
                 const u32 i = i0 + q * BLOCK + tid;
-                oi[q] = i < n_act ? ld_cg(cur + i) : op;
+                const u64 *w = cur + 4 * static_cast<u64>(i);
+                rec[q][0] = kp, rec[q][1] = rec[q][2] = rec[q][3] = 0;
+                if (i < n_act) {
+                    rec[q][0] = ld_cg(w);
+                    rec[q][1] = ld_cg(w + 1);
+                    rec[q][2] = ld_cg(w + 2);
+                    rec[q][3] = ld_cg(w + 3);
+                }
             }
+            bool lt[PR], gt[PR];
 #pragma unroll
-            for (int q = 0; q < PER; ++q)
-                key[q] = ld_cg(first + (oi[q] - olo));
-#pragma unroll
-            for (int q = 0; q < PER; ++q) {
-                lt[q] = key[q] < kp;
-                gt[q] = key[q] > kp;
+            for (int q = 0; q < PR; ++q) {
+                lt[q] = rec[q][0] < kp;
+                gt[q] = rec[q][0] > kp;
                 if (lt[q])
-                    s_lt += static_cast<u128>(ld_cg(sum + (oi[q] - olo))) * ld_cg(ot_sig + oi[q]);
+                    s_lt += (static_cast<u128>(rec[q][2]) << 64) | rec[q][1];
             }
-            append(lt, gt, oi, oth, oth + n_act, n_lt, n_gt);
+            u32 pa[PR], pb[PR];
+            place(std::integral_constant<int, PR>{}, lt, gt, pa, pb, n_lt, n_gt);
+#pragma unroll
+            for (int q = 0; q < PR; ++q)
+                if (lt[q] || gt[q]) {
+                    u64 *w = oth + 4 * static_cast<u64>(lt[q] ? pa[q] : n_act - 1 - pb[q]);
+                    st_cg(w + 0, rec[q][0]);
+                    st_cg(w + 1, rec[q][1]);
+                    st_cg(w + 2, rec[q][2]);
+                    st_cg(w + 3, rec[q][3]);
+                }
             if (WARPS > 1)
                 __syncthreads();
         }
         u64 lo, hi, ov;
         block_sum_u128<BLOCK>(s_lt, lo, hi, ov, sh.red64);
         const u128 below = acc + ((static_cast<u128>(hi) << 64) | lo);
-        ans = op;
         if (ov || below < acc || below > pick) { // the answer has a smaller key than the pivot
-            u32 *t = cur_buf;
+            u64 *t = cur_buf;
             cur = oth, cur_buf = oth, oth = t;
             n_act = n_lt;
         } else {
-            const u128 wp = static_cast<u128>(ld_cg(sum + (op - olo))) * ld_cg(ot_sig + op);
             const u128 incl = below + wp;
             if (incl < below || incl > pick || n_gt == 0)
                 n_act = 0; // the pivot it is
             else {
                 acc = incl;
-                u32 *t = cur_buf;
-                cur = oth + (n_act - n_gt), cur_buf = oth, oth = t;
+                u64 *t = cur_buf;
+                cur = oth + 4 * static_cast<u64>(n_act - n_gt), cur_buf = oth, oth = t;
                 n_act = n_gt;
             }
         }
         __syncthreads(); // the new lists are visible; red64 and warp_cnt may be reused
         if (n_act == 1)
-            ans = ld_cg(cur);
+            ans = static_cast<u32>(ld_cg(cur + 3));
     }
     return ans;
 }
@@ -2007,7 +2096,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) samp
         for (int c = 0; c < 6; ++c)
             EBC_STAT(sh.last[c] = 0;)
 #ifdef EBC_PHASE_TIMERS // experiment only: cycles per phase replace the work counters
-    long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long ph[11] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}; // 7: large meet sets, 8: small ones, 9: pick, 10: number of large ones
     long long ph_t = clock64();
 #define EBC_PH(i)                         \
     {                                     \
@@ -2110,6 +2199,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) samp
         // ---- level loop (sampler.cpp:81-116) ----
         EBC_PH(0)
         bool found = false, aborted = false, probed = false;
+        bool scratch_ready = false; // the last probe cleared pick_meet_large's scratch entries
         int e = 0;
         u32 contact_n = 0, edge_n = 0;
         while (!found) {
@@ -2126,8 +2216,13 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) samp
                 4 * side[e].pending >= p.probe_growth_x4 * sh.prev_pending[e] &&
                 static_cast<u64>(side[e].depth) + 2 <= p.aux_cap) {
                 u64 new_slots = 0, total_slots = 0;
+                // (scratch of pick_meet_large behind both sides' sigma arrays, if there is room for it)
+                const u64 o_front = side[1 - e].cnt - side[1 - e].fb;
+                scratch_ready = BITS && o_front + side[e].cnt <= p.cap && o_front + side[1 - e].cnt <= p.cap;
                 edge_n = probe_level<BLOCK, ITEMS, BITS>(p, sh.lab, sh.bits, vf, e, side[e], side[1 - e], sh.contact, edge_cap(), sh,
-                                                         new_slots, total_slots);
+                                                         new_slots, total_slots,
+                                                         scratch_ready ? side[e].pp->sig + side[e].cnt : nullptr,
+                                                         scratch_ready ? side[1 - e].pp->sig + side[1 - e].cnt : nullptr);
                 EBC_PH(2)
                 bool resolvable = edge_n > 0 && edge_n <= edge_cap();
                 if (resolvable && edge_n > static_cast<u32>(FinalEdgeCap<BLOCK>::value)) {
@@ -2212,10 +2307,19 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) samp
             EBC_STAT(if (tid == 0 && probed && edge_n > static_cast<u32>(FinalEdgeCap<BLOCK>::value)) sh.rec.flags |= 8u;) // resolved in global memory
             if constexpr (!FIXED)
                 if (probed && edge_n > static_cast<u32>(FinalEdgeCap<BLOCK>::value)) {
-                    const u32 oi = pick_meet_large<BLOCK, ITEMS>(sh.contact, edge_n, olo, ohi, sh.meetbuf, ex.pp->sig + ex.cnt,
-                                                                 ot.pp->sig + ot.cnt, ot.pp->sig, rng, sh, meet_count, total_weight);
+                    const u32 oi = pick_meet_large<BLOCK, ITEMS>(sh.contact, edge_n, olo, ohi, ex.pp->sig + ex.cnt, ot.pp->sig + ot.cnt,
+                                                                 ot.pp->sig, sh.sigma_small[e] != 0, scratch_ready && olo == ot.fb, rng, sh,
+                                                                 meet_count, total_weight);
                     meet = ld_cg(ot.pp->list + oi); // (a member's other-side idx names it)
                     searched = true;
+                    EBC_PH(7)
+#ifdef EBC_PHASE_TIMERS
+                    ph[10] += 1;
+#ifdef EBC_PHASE_COUNTS
+                    ph[8] += edge_n;
+                    ph[9] += meet_count;
+#endif
+#endif
                 }
             if (!searched) {
             // meet set in discovery order (sampler.cpp:109-113) -> sh.meetbuf
@@ -2224,6 +2328,9 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) samp
             else
                 meet_count = !probed ? meet_from_contacts<BLOCK, ITEMS>(sh.contact, contact_n, ex, olo, ohi, sh.meetbuf, sh)
                                      : meet_from_edges<BLOCK, ITEMS>(sh.contact, edge_n, olo, ohi, sh.meetbuf, sh);
+#ifndef EBC_PHASE_COUNTS
+            EBC_PH(8)
+#endif
 
             // total weight over the meet set (sampler.cpp:121-123), saturating at 2^128-1
             u128 wsum = 0;
@@ -2266,6 +2373,9 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) samp
                 if (meet == 0xffffffffu)
                     meet = ld_cg(sh.meetbuf + 4 * static_cast<u64>(meet_count - 1));
             }
+#ifndef EBC_PHASE_COUNTS
+            EBC_PH(9)
+#endif
             }
             if (tid == 0) {
                 EBC_STAT(sh.rec.weight_lo = static_cast<u64>(total_weight);)
@@ -2386,7 +2496,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) samp
         for (int c = 0; c < kWorkCounters; ++c)
             atomicAdd(p.work + c, static_cast<unsigned long long>(sh.wk[c]));
 #ifdef EBC_PHASE_TIMERS
-        for (int c = 0; c < 7; ++c)
+        for (int c = 0; c < 11; ++c)
             atomicAdd(p.work + c, static_cast<unsigned long long>(ph[c]) - static_cast<unsigned long long>(sh.wk[c]));
 #endif
     }
