@@ -1465,6 +1465,92 @@ __device__ u32 meet_from_edges(const u32 *edges, u32 m, u32 olo, u32 ohi, u32 *m
     return members;
 }
 
+// A probed final level with at most 32 contact edges -- more than half of the samples on R-MAT graphs: lane i of every
+// warp takes edge i and the whole choice of the meet vertex happens in registers (the warps of a CTA compute it
+// redundantly: no shared memory, no barrier).  Two round trips (the edges, sigma on the other side) instead of the
+// dozen of meet_from_edges + the prefix search over its global meet set, and a fraction of the instructions.
+//  * edges of one vertex find each other with match.any on the other-side idx; sigma_ex = saturating sum of their
+//    parents' sigma (sampler.cpp:11-13,97-98), the edge with the smallest discovery key represents the vertex;
+//  * weight = sigma_ex * sigma_other (sampler.cpp:121-123), total by a 5-step butterfly with carry count;
+//  * a member's exclusive prefix in discovery order = sum of the weights of the members with a smaller key, the
+//    chosen one is the member with exclusive <= pick < inclusive (sampler.cpp:126-132).
+// Returns the meet vertex; meet_count and total_weight as the reference would see them.
+static __device__ __noinline__ u32 pick_meet_warp(const u32 *contact, u32 m, u32 olo, u32 ohi, const u64 *ot_sig, SampleStream &rng,
+                                           u32 &meet_count, u128 &total_weight) {
+    constexpr u32 kAll = 0xffffffffu;
+    const u32 lane = lane_id();
+    const u64 *w = reinterpret_cast<const u64 *>(contact) + 3 * lane; // {position | index << 32, v | oi << 32, sigma}
+    u64 key = ~0ull, sg = 0;
+    u32 v = 0, oi = kAll - lane; // (lanes without an edge of the level `best`: alone in their group)
+    bool in = false;
+    if (lane < m) {
+        const u64 q0 = ld_cg(w), q1 = ld_cg(w + 1);
+        sg = ld_cg(w + 2);
+        if (static_cast<u32>(q1 >> 32) - olo < ohi - olo) {
+            in = true;
+            key = (q0 << 32) | (q0 >> 32);
+            v = static_cast<u32>(q1);
+            oi = static_cast<u32>(q1 >> 32);
+        }
+    }
+    const u64 so = in ? ld_cg(ot_sig + oi) : 0ull;
+    u32 rest = __match_any_sync(kAll, oi);
+    u64 sx = 0, kmin = ~0ull;
+    while (__any_sync(kAll, rest != 0)) { // as many rounds as the largest group has edges
+        const int src = rest ? __ffs(rest) - 1 : static_cast<int>(lane);
+        const u64 s2 = __shfl_sync(kAll, sg, src), k2 = __shfl_sync(kAll, key, src);
+        if (rest) {
+            sx = sx > ~0ull - s2 ? ~0ull : sx + s2;
+            kmin = k2 < kmin ? k2 : kmin;
+            rest &= rest - 1;
+        }
+    }
+    const bool member = in && key == kmin;
+    const u128 wt = member ? static_cast<u128>(sx) * so : static_cast<u128>(0);
+    const u64 wl = static_cast<u64>(wt), wh = static_cast<u64>(wt >> 64);
+    meet_count = __popc(__ballot_sync(kAll, member));
+    {
+        u64 a = wl, b = wh;
+        u32 c = 0;
+#pragma unroll 1
+        for (int o = 16; o > 0; o >>= 1) {
+            const u64 a2 = __shfl_xor_sync(kAll, a, o), b2 = __shfl_xor_sync(kAll, b, o);
+            const u32 c2 = __shfl_xor_sync(kAll, c, o);
+            const u128 x = (static_cast<u128>(b) << 64) | a, y = (static_cast<u128>(b2) << 64) | a2;
+            const u128 t = x + y;
+            c += c2 + (t < x ? 1u : 0u);
+            a = static_cast<u64>(t);
+            b = static_cast<u64>(t >> 64);
+        }
+        total_weight = c ? ~static_cast<u128>(0) : ((static_cast<u128>(b) << 64) | a);
+    }
+    const u128 pick = uniform_below_u128(rng, total_weight); // sampler.cpp:124
+    u128 excl = 0;
+    bool excl_ovf = false;
+#pragma unroll 1
+    for (u32 j = 0; j < m; ++j) {
+        const u64 kj = __shfl_sync(kAll, key, j), lj = __shfl_sync(kAll, wl, j), hj = __shfl_sync(kAll, wh, j);
+        if (kj < key) { // (an edge that does not represent a member carries weight 0)
+            const u128 t = excl + ((static_cast<u128>(hj) << 64) | lj);
+            excl_ovf = excl_ovf || t < excl;
+            excl = t;
+        }
+    }
+    const u128 incl = excl + wt;
+    const bool hit = member && !excl_ovf && excl <= pick && (incl < excl || incl > pick);
+    u32 found = __ballot_sync(kAll, hit);
+    if (found == 0) { // cannot happen (pick < total); the reference's default is the last member (sampler.cpp:125)
+        u64 kmax = member ? key : 0ull;
+#pragma unroll 1
+        for (int o = 16; o > 0; o >>= 1) {
+            const u64 k2 = __shfl_xor_sync(kAll, kmax, o);
+            kmax = k2 > kmax ? k2 : kmax;
+        }
+        found = __ballot_sync(kAll, member && key == kmax);
+    }
+    return __shfl_sync(kAll, v, __ffs(found) - 1);
+}
+
 // A probed final level with more contact edges than meet_from_edges holds in shared memory (R-MAT-20: a fifth of
 // the samples at one warp per sample, R-MAT-24: 16 % -- the ones with the largest final levels, which would otherwise
 // be expanded and settled in full; a hub on the other side's frontier alone brings thousands of contact edges).
@@ -2305,6 +2391,12 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) samp
             u32 meet = 0xffffffffu;
             bool searched = false; // a large probed level: the meet vertex is selected, the set is never ordered
             EBC_STAT(if (tid == 0 && probed && edge_n > static_cast<u32>(FinalEdgeCap<BLOCK>::value)) sh.rec.flags |= 8u;) // resolved in global memory
+            if constexpr (!FIXED) {
+                if (probed && edge_n <= 32) {
+                    meet = pick_meet_warp(sh.contact, edge_n, olo, ohi, ot.pp->sig, rng, meet_count, total_weight);
+                    searched = true;
+                }
+            }
             if constexpr (!FIXED)
                 if (probed && edge_n > static_cast<u32>(FinalEdgeCap<BLOCK>::value)) {
                     const u32 oi = pick_meet_large<BLOCK, ITEMS>(sh.contact, edge_n, olo, ohi, ex.pp->sig + ex.cnt, ot.pp->sig + ot.cnt,
