@@ -1465,6 +1465,27 @@ __device__ u32 meet_from_edges(const u32 *edges, u32 m, u32 olo, u32 ohi, u32 *m
     return members;
 }
 
+// Lanes 0 .. n-1 of a warp hold one candidate each (discovery key, 128-bit weight; weight 0 = not a candidate):
+// the lane of the first candidate in key order whose inclusive prefix of weights, on top of `acc`, exceeds `pick`
+// (sampler.cpp:126-132), or 32.  A prefix that leaves 128 bits exceeds.  acc <= pick.
+static __device__ __forceinline__ u32 warp_first_exceeding(u64 key, u64 wl, u64 wh, u32 n, u128 acc, u128 pick) {
+    u128 excl = acc;
+    bool excl_ovf = false;
+#pragma unroll 1
+    for (u32 j = 0; j < n; ++j) {
+        const u64 kj = __shfl_sync(0xffffffffu, key, j), lj = __shfl_sync(0xffffffffu, wl, j), hj = __shfl_sync(0xffffffffu, wh, j);
+        if (kj < key) {
+            const u128 t = excl + ((static_cast<u128>(hj) << 64) | lj);
+            excl_ovf = excl_ovf || t < excl;
+            excl = t;
+        }
+    }
+    const u128 incl = excl + ((static_cast<u128>(wh) << 64) | wl);
+    const bool hit = (wl | wh) != 0 && !excl_ovf && excl <= pick && (incl < excl || incl > pick);
+    const u32 found = __ballot_sync(0xffffffffu, hit);
+    return found ? __ffs(found) - 1 : 32u;
+}
+
 // A probed final level with at most 32 contact edges -- more than half of the samples on R-MAT graphs: lane i of every
 // warp takes edge i and the whole choice of the meet vertex happens in registers (the warps of a CTA compute it
 // redundantly: no shared memory, no barrier).  Two round trips (the edges, sigma on the other side) instead of the
@@ -1525,30 +1546,17 @@ static __device__ __noinline__ u32 pick_meet_warp(const u32 *contact, u32 m, u32
         total_weight = c ? ~static_cast<u128>(0) : ((static_cast<u128>(b) << 64) | a);
     }
     const u128 pick = uniform_below_u128(rng, total_weight); // sampler.cpp:124
-    u128 excl = 0;
-    bool excl_ovf = false;
-#pragma unroll 1
-    for (u32 j = 0; j < m; ++j) {
-        const u64 kj = __shfl_sync(kAll, key, j), lj = __shfl_sync(kAll, wl, j), hj = __shfl_sync(kAll, wh, j);
-        if (kj < key) { // (an edge that does not represent a member carries weight 0)
-            const u128 t = excl + ((static_cast<u128>(hj) << 64) | lj);
-            excl_ovf = excl_ovf || t < excl;
-            excl = t;
-        }
-    }
-    const u128 incl = excl + wt;
-    const bool hit = member && !excl_ovf && excl <= pick && (incl < excl || incl > pick);
-    u32 found = __ballot_sync(kAll, hit);
-    if (found == 0) { // cannot happen (pick < total); the reference's default is the last member (sampler.cpp:125)
+    u32 chosen = warp_first_exceeding(key, wl, wh, m, 0, pick); // (an edge that does not represent a member carries weight 0)
+    if (chosen == 32u) { // cannot happen (pick < total); the reference's default is the last member (sampler.cpp:125)
         u64 kmax = member ? key : 0ull;
 #pragma unroll 1
         for (int o = 16; o > 0; o >>= 1) {
             const u64 k2 = __shfl_xor_sync(kAll, kmax, o);
             kmax = k2 > kmax ? k2 : kmax;
         }
-        found = __ballot_sync(kAll, member && key == kmax);
+        chosen = __ffs(__ballot_sync(kAll, member && key == kmax)) - 1;
     }
-    return __shfl_sync(kAll, v, __ffs(found) - 1);
+    return __shfl_sync(kAll, v, chosen);
 }
 
 // A probed final level with more contact edges than meet_from_edges holds in shared memory (R-MAT-20: a fifth of
@@ -1578,7 +1586,17 @@ static __device__ __noinline__ u32 pick_meet_warp(const u32 *contact, u32 m, u32
 template <int BLOCK, int ITEMS>
 __device__ __noinline__ u32 pick_meet_large(u32 *contact, u32 m, u32 olo, u32 ohi, u64 *first, u64 *sum, const u64 *ot_sig,
                                             bool sigma_small, bool cleared, SampleStream &rng, BlockShared<BLOCK, ITEMS> &sh,
-                                            u32 &meet_count, u128 &total_weight) {
+                                            u32 &meet_count, u128 &total_weight
+#ifdef EBC_PHASE_COUNTS
+                                            , long long *pht
+#endif
+                                            ) {
+#ifdef EBC_PHASE_COUNTS
+    long long pt0 = clock64();
+#define EBC_PT(i) { const long long t = clock64(); pht[i] += t - pt0; pt0 = t; }
+#else
+#define EBC_PT(i)
+#endif
     constexpr int WARPS = BLOCK / 32;
     constexpr int PE = 4; // edges per thread and batch
     constexpr int PR = 2; // records per thread and batch
@@ -1673,6 +1691,7 @@ __device__ __noinline__ u32 pick_meet_large(u32 *contact, u32 m, u32 olo, u32 oh
             __syncthreads();
     }
     __syncthreads();
+    EBC_PT(0)
     // records of four 8-byte words {key, weight lo, weight hi, oi}: two buffers of `count` records
     u64 *cur = reinterpret_cast<u64 *>(contact + 8 * static_cast<u64>(m));
     u64 *oth = reinterpret_cast<u64 *>(contact); // (over the edges, which nobody reads any more)
@@ -1714,12 +1733,13 @@ __device__ __noinline__ u32 pick_meet_large(u32 *contact, u32 m, u32 olo, u32 oh
     total_weight = wov ? ~static_cast<u128>(0) : ((static_cast<u128>(whi) << 64) | wlo);
     meet_count = count;
     const u128 pick = uniform_below_u128(rng, total_weight); // sampler.cpp:124
+    EBC_PT(1)
     u64 *cur_buf = cur;
     u32 n_act = count;
     u128 acc = 0; // exact weight of the members below the active keys; acc <= pick
     u32 ans = static_cast<u32>(ld_cg(cur + 3));
 #pragma unroll 1
-    while (n_act > 1) {
+    while (n_act > 32) {
         const u64 *pv = cur + 4 * static_cast<u64>(n_act >> 1);
         const u64 kp = ld_cg(pv);
         const u128 wp = (static_cast<u128>(ld_cg(pv + 2)) << 64) | ld_cg(pv + 1);
@@ -1782,8 +1802,15 @@ __device__ __noinline__ u32 pick_meet_large(u32 *contact, u32 m, u32 olo, u32 oh
             }
         }
         __syncthreads(); // the new lists are visible; red64 and warp_cnt may be reused
-        if (n_act == 1)
-            ans = static_cast<u32>(ld_cg(cur + 3));
+    }
+    if (n_act > 0) { // the last 32: one record per lane, every warp for itself (as in pick_meet_warp)
+        const u64 *w = cur + 4 * static_cast<u64>(lane_id());
+        const bool have = lane_id() < n_act;
+        const u64 key = have ? ld_cg(w) : ~0ull, wl = have ? ld_cg(w + 1) : 0ull, wh = have ? ld_cg(w + 2) : 0ull;
+        const u32 oi = have ? static_cast<u32>(ld_cg(w + 3)) : 0u;
+        const u32 chosen = warp_first_exceeding(key, wl, wh, n_act, acc, pick);
+        if (chosen != 32u) // (else: cannot happen, the last pivot stands)
+            ans = __shfl_sync(0xffffffffu, oi, chosen);
     }
     return ans;
 }
@@ -2401,16 +2428,16 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) samp
                 if (probed && edge_n > static_cast<u32>(FinalEdgeCap<BLOCK>::value)) {
                     const u32 oi = pick_meet_large<BLOCK, ITEMS>(sh.contact, edge_n, olo, ohi, ex.pp->sig + ex.cnt, ot.pp->sig + ot.cnt,
                                                                  ot.pp->sig, sh.sigma_small[e] != 0, scratch_ready && olo == ot.fb, rng, sh,
-                                                                 meet_count, total_weight);
+                                                                 meet_count, total_weight
+#ifdef EBC_PHASE_COUNTS
+                                                                 , ph + 8
+#endif
+                                                                 );
                     meet = ld_cg(ot.pp->list + oi); // (a member's other-side idx names it)
                     searched = true;
                     EBC_PH(7)
 #ifdef EBC_PHASE_TIMERS
                     ph[10] += 1;
-#ifdef EBC_PHASE_COUNTS
-                    ph[8] += edge_n;
-                    ph[9] += meet_count;
-#endif
 #endif
                 }
             if (!searched) {
