@@ -277,7 +277,8 @@ typedef struct ebc_sample_record {
                            * read-only probe (not settled); bit2: a probe found contact edges it could not resolve
                            * (buffer or scratch too small) and the level was expanded instead; bit3: the probed
                            * level had more contact edges than the shared-memory meet path holds (resolved in the
-                           * slot's global arrays: config 2 12-20 % of the samples, tools/probe_stats.py) */
+                           * slot's global arrays: config 2 12-20 % of the samples, tools/probe_stats.py);
+                           * bit4: at most 32 contact edges, the meet vertex was chosen in registers */
     uint64_t weight_lo, weight_hi; /* total meet weight (saturating u128) */
 } ebc_sample_record;
 

@@ -186,9 +186,9 @@ constexpr int kPredCache = 32;
 
 // Final-level probe (see probe_level): a level with at least SamplerParams::probe_min_slots adjacency
 // slots (256 with visited bitmaps, else 512; set by the host) is first scanned read-only; if it touches
-// the other side, the meet set is resolved from the contact edges and the level is never settled: up to
-// FinalEdgeCap<BLOCK>::value edges in shared memory (meet_from_edges), more -- as many as the slot's
-// contact buffer holds -- in the slot's global arrays (meet_from_edges_large).
+// the other side, the meet vertex is chosen from the contact edges and the level is never settled: up to
+// 32 edges in registers (pick_meet_warp), up to FinalEdgeCap<BLOCK>::value in shared memory (meet_from_edges),
+// more -- as many as the slot's contact buffer holds -- in the slot's global arrays (pick_meet_large).
 #ifndef EBC_EDGE_CAP_MAX
 #define EBC_EDGE_CAP_MAX 512
 #endif
@@ -2339,7 +2339,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) samp
                 EBC_PH(2)
                 bool resolvable = edge_n > 0 && edge_n <= edge_cap();
                 if (resolvable && edge_n > static_cast<u32>(FinalEdgeCap<BLOCK>::value)) {
-                    // meet_from_edges_large needs ohi - olo scratch words behind both sides' sigma arrays
+                    // pick_meet_large needs ohi - olo scratch words behind both sides' sigma arrays
                     const SideRegs &ot = side[1 - e];
                     u32 best = ot.depth;
                     while (ld_cg(ot.pp->lvl + best) > sh.min_contact)
@@ -2422,6 +2422,7 @@ __global__ void __launch_bounds__(BLOCK, min_blocks_per_sm<BLOCK, FIXED>()) samp
                 if (probed && edge_n <= 32) {
                     meet = pick_meet_warp(sh.contact, edge_n, olo, ohi, ot.pp->sig, rng, meet_count, total_weight);
                     searched = true;
+                    EBC_STAT(if (tid == 0) sh.rec.flags |= 16u;)
                 }
             }
             if constexpr (!FIXED)

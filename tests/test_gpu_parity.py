@@ -212,9 +212,9 @@ def test_final_level_probe_is_result_identical(block, items):
 @pytest.mark.parametrize("block,bitmap", [(32, "0"), (32, "1"), (128, "0"), (128, "1")])
 def test_large_contact_sets_are_resolved_without_settling(block, bitmap, monkeypatch):
     """A probed final level with far more contact edges than the shared-memory resolver holds (7800 here)
-    goes through meet_from_edges_large: sigma sums per member by atomics in global scratch (they saturate at
-    2^64-1 here), members ordered by a bitonic sort -- in shared memory when they fit (130 <= 512 at 128
-    threads), in the meet buffer otherwise (130 > 128 at 32 threads).  Layers 40^12 -> 60 -> 130 <- 60 <- 40^12:
+    goes through pick_meet_large: sigma sums per member by atomics in global scratch (they saturate at
+    2^64-1 here), the meet vertex by a weighted quickselect over the 130 members' discovery keys whose weights
+    (2^128 each, the total saturates) leave 128 bits in every prefix.  Layers 40^12 -> 60 -> 130 <- 60 <- 40^12:
     the frontier more than doubles into the middle, sigma reaches 40^12 * 60 > 2^64 there."""
     monkeypatch.setenv("EBC_BITMAP", bitmap)
     widths = [2] + [40] * 12 + [60, 130, 60] + [40] * 12 + [2]
@@ -232,6 +232,29 @@ def test_large_contact_sets_are_resolved_without_settling(block, bitmap, monkeyp
     assert max(int(fs[v]) for v in o.last_meet_set()) == 2 ** 64 - 1 or max(int(bs[v]) for v in o.last_meet_set()) == 2 ** 64 - 1
     total = min(sum(int(fs[v]) * int(bs[v]) for v in o.last_meet_set()), 2 ** 128 - 1)
     assert (int(rec[0]["weight_hi"]) << 64) | int(rec[0]["weight_lo"]) == total
+
+
+@pytest.mark.parametrize("block", [32, 64, 256])
+def test_meet_vertex_by_all_three_paths(block):
+    """The meet vertex of a probed level is chosen in registers (at most 32 contact edges: flag 16), from shared
+    memory (up to 128 ... 512 edges), or by the weighted quickselect in the slot's global arrays (more: flag 8).  An
+    R-MAT graph takes all three; every sample's (s, t, d, meet, |meet set|, draws, path) and the total meet
+    weight equal the oracle's."""
+    g0 = ebc.gen_rmat(14, 24, seed=11).largest_connected_component()
+    off, tg = g0.offsets.copy(), g0.targets.copy()
+    s, o = check_samples((off, tg), 1200, ebc.RunConfig(block_threads=block, items_per_thread=2, slots=64), first=500)
+    rec, _ = s.sample_debug(SEED, 500, 1200, frame=1)
+    f = rec["flags"]
+    probed = (f & 2) != 0
+    assert ((f & 16) != 0).sum() > 100 and ((f & 8) != 0).sum() > (5 if block <= 64 else 0)
+    assert (probed & ((f & 24) == 0)).sum() > 20          # the shared-memory path
+    assert not ((f & 16) != 0)[~probed].any() and not ((f & 8) != 0)[~probed].any()
+    for i in range(0, 1200, 7):
+        o.sample(SEED, 500 + i)
+        fs, bs = o.last_state(0)[1], o.last_state(1)[1]
+        total = min(sum(int(fs[v]) * int(bs[v]) for v in o.last_meet_set()), 2 ** 128 - 1)
+        assert (int(rec[i]["weight_hi"]) << 64) | int(rec[i]["weight_lo"]) == total, i
+    s.close()
 
 
 def test_final_level_probe_with_tiny_edge_buffer_falls_back():
