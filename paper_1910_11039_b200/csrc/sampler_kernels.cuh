@@ -1087,13 +1087,10 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
 // Appends one contact edge (see probe_level); out of line, it runs a few dozen times per sample.
 static __device__ __noinline__ void record_contact_edge(u32 *edges, u32 pos, u32 frontier_pos, u32 index_in_row, u32 v, u32 oi,
                                                         u64 sg) {
-    u32 *w = edges + 6 * static_cast<u64>(pos);
-    st_cg(w + 0, frontier_pos);
-    st_cg(w + 1, index_in_row);
-    st_cg(w + 2, v);
-    st_cg(w + 3, oi);
-    st_cg(w + 4, static_cast<u32>(sg));
-    st_cg(w + 5, static_cast<u32>(sg >> 32));
+    u64 *w = reinterpret_cast<u64 *>(edges) + 3 * static_cast<u64>(pos); // (24-byte records in an 8-byte aligned array)
+    st_cg(w + 0, static_cast<u64>(frontier_pos) | (static_cast<u64>(index_in_row) << 32));
+    st_cg(w + 1, static_cast<u64>(v) | (static_cast<u64>(oi) << 32));
+    st_cg(w + 2, sg);
 }
 
 template <int BLOCK, int ITEMS, bool BITS>
@@ -1176,6 +1173,8 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
                         both[k] = BITS ? ld_cg(reinterpret_cast<const u64 *>(bits) + (vv[k] >> 5))
                                        : static_cast<u64>(ld_cg(lab + vv[k]));
                 }
+                u32 cmask = 0;   // bit k: entry k is a contact edge
+                u32 ois[4] = {0, 0, 0, 0};
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     if (!((need >> k) & 1u))
@@ -1196,14 +1195,24 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
                             continue; // visited before this level
                         fresh += 1;
                         oi = label_idx(lbl, ex.base, 1 - e);
+                        ois[k] = oi;
                     }
                     if (oi < ot.cnt) {
                         if (!BITS)
                             atomicMin(&sh.min_contact, oi);
-                        const u32 pos = atomicAdd(&sh.edge_cnt, 1u);
+                        cmask |= 1u << k;
+                    }
+                }
+                if (cmask) { // rare: one counter update per quad, one copy of the record code
+                    u32 pos = atomicAdd(&sh.edge_cnt, static_cast<u32>(__popc(cmask)));
+                    const u64 sg = sh.c_sig[row_c];
+#pragma unroll 1
+                    for (; cmask; cmask &= cmask - 1, ++pos) {
+                        const int k = __ffs(cmask) - 1;
                         if (pos < edge_cap)
-                            record_contact_edge(edges, pos, (c0 - fb) + row_c, static_cast<u32>(rel0_c + k), vv[k], oi,
-                                                sh.c_sig[row_c]);
+                            record_contact_edge(edges, pos, (c0 - fb) + row_c, static_cast<u32>(rel0_c + k),
+                                                k == 0 ? vv[0] : k == 1 ? vv[1] : k == 2 ? vv[2] : vv[3],
+                                                BITS ? 0u : k == 0 ? ois[0] : k == 1 ? ois[1] : k == 2 ? ois[2] : ois[3], sg);
                     }
                 }
             }
