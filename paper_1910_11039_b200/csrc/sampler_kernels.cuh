@@ -1107,6 +1107,12 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
     const u32 tid = threadIdx.x;
     const u32 gid = tid / G, q = tid % G;
     const u32 fb = ex.fb, fe = ex.cnt;
+    // The side as a value of its own (the compiler otherwise re-derives it from the two 64-bit pending counts at
+    // every use in the scan), the filter by its shared-window address (no generic-address arithmetic per look-up).
+    int e_opaque = e;
+    asm volatile("" : "+r"(e_opaque));
+    const bool backward = e_opaque != 0;
+    const u32 vf_base = smem_addr(vf);
     if (tid == 0) {
         sh.edge_cnt = 0;
         sh.min_contact = 0xffffffffu;
@@ -1156,8 +1162,9 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
             if (BITS) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    const u32 h = vv[k] & (VisitedFilter<BLOCK>::kPositions - 1);
-                    need |= ((vf[h >> 5] >> (h & 31)) & 1u) << k; // clear: certainly unvisited on both sides
+                    // (word (v mod kPositions) / 32 by its shared-window address; the shift takes v mod 32 by itself)
+                    const u32 word = lds_u32(vf_base + ((vv[k] >> 3) & (4 * VisitedFilter<BLOCK>::kWords - 4)));
+                    need |= ((word >> (vv[k] & 31)) & 1u) << k; // clear: certainly unvisited on both sides
                 }
                 need &= valid;
                 fresh += __popc(valid & ~need);
@@ -1181,10 +1188,11 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
                         continue;
                     u32 oi;
                     if (BITS) {
-                        if ((static_cast<u32>(both[k] >> (32 * e)) >> (vv[k] & 31)) & 1u)
+                        const u32 lo = static_cast<u32>(both[k]), hi = static_cast<u32>(both[k] >> 32);
+                        if (((backward ? hi : lo) >> (vv[k] & 31)) & 1u)
                             continue; // visited before this level
                         fresh += 1;
-                        if (!((static_cast<u32>(both[k] >> (32 * (1 - e))) >> (vv[k] & 31)) & 1u))
+                        if (!(((backward ? lo : hi) >> (vv[k] & 31)) & 1u))
                             continue; // not a contact
                         // The other side's bit already says "contact"; its idx is only needed for the record
                         // and is fetched for all contact edges at once after the scan.
@@ -1241,7 +1249,7 @@ __device__ u32 probe_level(const SamplerParams &p, const u32 *lab, const u32 *bi
                         nxt = __ldg(quads + qn);
                     // the row is a stream from DRAM: ask L2 for the sector three rounds ahead (config 4 +5 %; six
                     // rounds ahead +4 %; config 2, whose rows mostly sit in L2, +0)
-                    if (qi + 3 * BLOCK < nq && (tid & 1) == 0) // (one request per 32-byte sector)
+                    if (qi + 3 * BLOCK < nq && (qi & 1) == 0) // (one request per 32-byte sector; qi = tid mod 2)
                         asm volatile("prefetch.global.L2 [%0];" ::"l"(quads + qi + 3 * BLOCK));
                     u32 valid = 0xfu;
                     if (qi == 0)
