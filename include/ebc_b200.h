@@ -331,7 +331,8 @@ EBC_API ebc_status ebc_sampler_mark(ebc_sampler *s, int event);
 EBC_API ebc_status ebc_sampler_elapsed_ms(ebc_sampler *s, int from_event, int to_event, float *ms);
 EBC_API ebc_status ebc_sampler_sync(ebc_sampler *s);
 /* slots, block_threads, slot_capacity, device bytes in use, SM count,
- * launches (bits 0-47) | renumbered (bits 48-51) | fixed-stride rows in use (bit 52) | items_per_thread (bits 56-63). */
+ * launches (bits 0-47) | renumbered (bits 48-51) | fixed-stride rows in use (bit 52), of four entries (bit 53),
+ * of eight with a 16-byte copy for the expansion (bit 54) | items_per_thread (bits 56-63). */
 EBC_API ebc_status ebc_sampler_info(ebc_sampler *s, uint64_t info_out[6]);
 /* The sampler's cudaStream_t and the device address of epoch frame 0|1
  * (for callers that aggregate frames themselves, e.g. NCCL in bench.py). */

@@ -457,6 +457,7 @@ class Sampler:
                     device_bytes=int(w[3]), sm_count=int(w[4]), launches=int(w[5]) & ((1 << 48) - 1),
                     renumbered=(int(w[5]) >> 48) & 0xF, fixed_rows=bool((int(w[5]) >> 52) & 1),
                     fixed_row_width=(4 if (int(w[5]) >> 53) & 1 else 8) if (int(w[5]) >> 52) & 1 else 0,
+                    fixed_row_copy16=bool((int(w[5]) >> 54) & 1),
                     items_per_thread=int(w[5]) >> 56)
 
     def stream(self) -> int:

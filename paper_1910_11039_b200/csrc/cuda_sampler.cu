@@ -622,7 +622,8 @@ __global__ void __launch_bounds__(256) dense_rows_kernel(const u64 *ext_offsets,
 // and the target's degree - 1 in the upper bits, padded with kEllEmpty.  *bad is raised if that does not work out (a
 // row above kEllWidth entries, or an arc without its reverse -- an asymmetric input); the sampler then runs without them.
 // `width` = entries stored per row: kEllWidth, or kEllNarrow when the caller knows that no row is longer.
-__global__ void __launch_bounds__(256) ell_rows_kernel(const u64 *offsets, const u32 *targets, u64 n, u32 width, u32 *ell, u32 *bad) {
+__global__ void __launch_bounds__(256) ell_rows_kernel(const u64 *offsets, const u32 *targets, u64 n, u32 width, u32 *ell, u32 *ell4,
+                                                       u32 *bad) {
     for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v < n;
          v += static_cast<u64>(gridDim.x) * blockDim.x) {
         const u64 beg = offsets[v], deg = offsets[v + 1] - beg;
@@ -648,6 +649,8 @@ __global__ void __launch_bounds__(256) ell_rows_kernel(const u64 *offsets, const
         out[0] = make_uint4(row[0], row[1], row[2], row[3]);
         if (width == kEllWidth)
             out[1] = make_uint4(row[4], row[5], row[6], row[7]);
+        if (ell4) // the 16-byte copy: rows of more than four entries refer to `ell`
+            reinterpret_cast<uint4 *>(ell4)[v] = make_uint4(deg > kEllNarrow ? kEllEscape : row[0], row[1], row[2], row[3]);
     }
 }
 
@@ -795,6 +798,8 @@ struct CudaSampler::Impl {
     u32 *d_to_dense = nullptr, *d_to_ext = nullptr;
     u32 *d_ell = nullptr; // fixed-stride rows of the graph the kernel searches on (null: maximum degree above kEllWidth)
     u32 ell_width = kEllWidth; // entries per row: kEllNarrow when the maximum degree allows
+    u32 *d_ell4 = nullptr;     // 16-byte copy of 32-byte rows for the expansion (SamplerParams::ell4)
+    bool want_ell4 = false;
     std::vector<u32> h_to_ext; // fetched on demand (last_state)
     u32 block = 128;
     u32 items = 4;
@@ -848,6 +853,7 @@ struct CudaSampler::Impl {
         p.ext_targets = d_targets;
         p.ell = d_ell;
         p.ell_width = ell_width;
+        p.ell4 = d_ell4;
         p.lab = a.lab;
         p.list = a.list;
         p.sig = a.sig;
@@ -937,11 +943,13 @@ struct CudaSampler::Impl {
     void build_fixed_rows() {
         cudaStream_t st = s_sample;
         d_ell = dev_alloc<u32>(n * ell_width);
+        if (want_ell4)
+            d_ell4 = dev_alloc<u32>(n * kEllNarrow);
         u32 *bad = dev_alloc<u32>(1);
         EBC_CUDA(cudaMemsetAsync(bad, 0, 4, st));
         const u32 grid = static_cast<u32>(std::min<u64>((n + 255) / 256, static_cast<u64>(sm_count) * 8));
         ell_rows_kernel<<<grid, 256, 0, st>>>(d_dense_offsets ? d_dense_offsets : d_offsets,
-                                              d_dense_targets ? d_dense_targets : d_targets, n, ell_width, d_ell, bad);
+                                              d_dense_targets ? d_dense_targets : d_targets, n, ell_width, d_ell, d_ell4, bad);
         EBC_CUDA(cudaGetLastError());
         u32 h_bad = 0;
         EBC_CUDA(cudaMemcpyAsync(&h_bad, bad, 4, cudaMemcpyDeviceToHost, st));
@@ -949,9 +957,10 @@ struct CudaSampler::Impl {
         dev_free(bad);
         if (h_bad) {
             dev_free(d_ell);
-            d_ell = nullptr;
+            dev_free(d_ell4);
+            d_ell = d_ell4 = nullptr;
         } else {
-            graph_bytes += n * ell_width * 4;
+            graph_bytes += n * ell_width * 4 + (d_ell4 ? n * kEllNarrow * 4 : 0);
         }
     }
 
@@ -1184,6 +1193,12 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
     if (const char *env = std::getenv("EBC_ELL_WIDTH"))
         if (std::atoi(env) == static_cast<int>(kEllWidth))
             m.ell_width = kEllWidth;
+    // ... and, on request (EBC_ELL4=1), a 16-byte copy of 32-byte rows for the expansion (SamplerParams::ell4).  Not a
+    // default: on config 3 (0.2 % of the rows longer than four entries) it halves the row bytes and changes the rate by
+    // +0.5 % -- that kernel is bound by the number of random sector accesses, not by their bytes.
+    m.want_ell4 = false;
+    if (const char *env = std::getenv("EBC_ELL4"))
+        m.want_ell4 = want_ell && m.ell_width == kEllWidth && std::atoi(env) != 0;
     const int per_sm = occupancy_for(m.block, m.items, want_ell);
     m.per_sm = per_sm;
     lap("occupancy query");
@@ -1204,7 +1219,7 @@ CudaSampler::CudaSampler(const HostGraph &g, const SamplerOptions &opt) : impl_(
     const u64 fixed = (g.n + 1) * (4 * 2 + 8 + 8 + 16 + 12) + (u64{256} << 20) + kOverflowCap * 4 +
                       (cap < g.n ? kLargeSlots * SlotArrays::bytes_per_slot(g.n, g.n, want_ell) : 0) +
                       (want_dense ? g.n * 40 + m.arcs * 4 + (u64{16} << 20) : 0) + // the dense copy is built below
-                      (want_ell ? g.n * kEllWidth * 4 : 0);
+                      (want_ell ? g.n * (kEllWidth + kEllNarrow) * 4 : 0);
     // Buffers cached by the pool are reusable (or released on demand), so they count as free.
     const u64 avail = capacity > live ? capacity - live : 0;
     const u64 budget = avail > fixed ? (avail - fixed) / 10 * 8 : 0;
@@ -1287,6 +1302,7 @@ CudaSampler::Impl::~Impl() {
     dev_free(m.d_to_dense);
     dev_free(m.d_to_ext);
     dev_free(m.d_ell);
+    dev_free(m.d_ell4);
     for (int i = 0; i < 2; ++i) {
         dev_free(m.d_frame[i]);
         handles().give_words(m.h_result[i]);
@@ -1578,7 +1594,8 @@ void CudaSampler::info(std::uint64_t *out) {
     out[4] = static_cast<std::uint64_t>(m.sm_count);
     out[5] = (m.launches & ((std::uint64_t{1} << 48) - 1)) | (static_cast<std::uint64_t>(m.numbering) << 48) |
              (static_cast<std::uint64_t>(m.d_ell ? 1 : 0) << 52) |
-             (static_cast<std::uint64_t>(m.d_ell && m.ell_width == kEllNarrow ? 1 : 0) << 53) | (static_cast<std::uint64_t>(m.items) << 56);
+             (static_cast<std::uint64_t>(m.d_ell && m.ell_width == kEllNarrow ? 1 : 0) << 53) |
+             (static_cast<std::uint64_t>(m.d_ell4 ? 1 : 0) << 54) | (static_cast<std::uint64_t>(m.items) << 56);
 }
 
 void *CudaSampler::stream_handle() { return impl_->s_sample; }

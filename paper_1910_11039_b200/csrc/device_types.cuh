@@ -46,6 +46,7 @@ constexpr u32 kEllRevShift = 26;           // bits 26..28 of an entry: position 
 constexpr u32 kEllDegShift = 29;           // bits 29..31: degree of the target, minus one
 constexpr u32 kEllIdMask = (1u << kEllRevShift) - 1;
 constexpr u32 kEllEmpty = 0xffffffffu;     // (a graph with fixed-stride rows has fewer than 2^26 - 1 vertices)
+constexpr u32 kEllEscape = 0xfffffffeu;    // first word of a row of SamplerParams::ell4 whose vertex has more than four entries
 constexpr u32 kHdrWords = 16;              // per-slot header (u32)
 // header word indices
 enum : int { kHdrBase0 = 0, kHdrBase1 = 1, kHdrLastBase0 = 2, kHdrLastBase1 = 3, kHdrLastCnt0 = 4,
@@ -82,6 +83,10 @@ struct SamplerParams {
     // ell + 4 v, two rows per sector, the whole table half the size (config 3: 64 MB, below the L2 capacity).
     const u32 *ell;
     u32 ell_width;
+    // ell_width = 8 on a graph where FEW rows have more than four entries (a lattice with some shortcuts, config 3):
+    // ell4[4 v ..] = the first four entries of row v (16 bytes, the 64 MB the expansion streams), or kEllEscape in
+    // word 0 if the row is longer -- the expansion then reads the row in `ell`.  Null otherwise.
+    const u32 *ell4;
     u32 *pm;       // [slots][2][pm_words] with fixed-stride rows: per settled vertex (indexed like list, one byte each)
                    // the mask of row entries that lead to its parents
     u64 pm_words;

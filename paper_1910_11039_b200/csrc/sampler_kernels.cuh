@@ -856,13 +856,23 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
     // The frontier is known when the level starts, so a chunk's vertex is loaded two chunks ahead and its row one
     // chunk ahead: of the three trips only the labels' stays on a chunk's critical path.
     const uint4 *rows = reinterpret_cast<const uint4 *>(p.ell);
+    const uint4 *rows4 = W == 8 ? reinterpret_cast<const uint4 *>(p.ell4) : nullptr; // (uniform)
+    auto load_row = [&](u32 u, uint4 &a, uint4 &b) {
+        if constexpr (W == 8) {
+            if (rows4) { // 16 bytes unless the row has more than four entries
+                a = __ldg(rows4 + u);
+                if (a.x != kEllEscape)
+                    return;
+            }
+            a = __ldg(rows + 2 * static_cast<u64>(u));
+            b = __ldg(rows + 2 * static_cast<u64>(u) + 1);
+        } else {
+            a = __ldg(rows + u);
+        }
+    };
     uint4 a_nxt = empty4, b_nxt = empty4;
-    if (fb + tid < fe) {
-        const u32 u = ld_cg(ex.pp->list + fb + tid);
-        a_nxt = __ldg(rows + (W / 4) * static_cast<u64>(u));
-        if constexpr (W == 8)
-            b_nxt = __ldg(rows + 2 * static_cast<u64>(u) + 1);
-    }
+    if (fb + tid < fe)
+        load_row(ld_cg(ex.pp->list + fb + tid), a_nxt, b_nxt);
     u32 u_nxt = fb + BLOCK + tid < fe ? ld_cg(ex.pp->list + fb + BLOCK + tid) : 0u;
     const unsigned char *pm_in = reinterpret_cast<const unsigned char *>(ex.pp->pm);
     for (u32 c0 = fb; c0 < fe; c0 += BLOCK) {
@@ -875,11 +885,8 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
         // change nothing (sampler.cpp:92,97 both fail).  On a grid that is every second entry.
         const u32 parents = i < fe ? __ldcg(pm_in + i) : 0u;
         a_nxt = empty4, b_nxt = empty4;
-        if (i + BLOCK < fe) {
-            a_nxt = __ldg(rows + (W / 4) * static_cast<u64>(u_nxt));
-            if constexpr (W == 8)
-                b_nxt = __ldg(rows + 2 * static_cast<u64>(u_nxt) + 1);
-        }
+        if (i + BLOCK < fe)
+            load_row(u_nxt, a_nxt, b_nxt);
         u_nxt = i + 2 * BLOCK < fe ? ld_cg(ex.pp->list + i + 2 * BLOCK) : 0u;
         // Entries are handled in two groups of four; the second one exists in few warps (a row of more than four
         // entries), and its code is a copy of the first with other constants -- executed rarely, it costs no

@@ -378,6 +378,45 @@ def test_fixed_stride_rows_of_four_entries(block, width, monkeypatch):
         s.close()
 
 
+@pytest.mark.parametrize("block,copy16", [(32, "1"), (64, "1"), (128, "1"), (64, "0")])
+def test_fixed_stride_rows_with_16_byte_copy(block, copy16, monkeypatch):
+    """A lattice with a few shortcuts (config 3): rows of up to eight entries, but few have more than four.  The
+    expansion then reads a 16-byte copy of every row (SamplerParams::ell4) and follows an escape word to the 32-byte
+    row where it must; EBC_ELL4 forces the copy on (here also on a graph where EVERY row escapes) or off.  Samples,
+    paths, frames, work counters and dist / sigma arrays equal the oracle's."""
+    monkeypatch.setenv("EBC_ELL4", copy16)
+    off, tg = grid_graph(53, 49, drop=0.05, seed=8)
+    n = len(off) - 1
+    rng = np.random.default_rng(3)
+    src, dst = [], []
+    for u in range(n):
+        src += [u] * int(off[u + 1] - off[u]); dst += [int(x) for x in tg[off[u]:off[u + 1]]]
+    extra = rng.integers(0, n, size=(60, 2))
+    from helpers import csr_from_edges
+    off, tg = csr_from_edges(n, np.concatenate([np.array(src), extra[:, 0]]), np.concatenate([np.array(dst), extra[:, 1]]))
+    deg = np.diff(off)
+    assert 4 < deg.max() <= 8 and (deg > 4).sum() * 8 < n
+    for graph in ((off, tg), _ring_lattice(2000)):
+        o_, t_ = graph
+        g = ebc.Graph.from_csr(o_, t_)
+        o = Oracle(o_, t_)
+        s, _ = check_samples((o_, t_), 400, ebc.RunConfig(block_threads=block, slots=8))
+        info = s.info()
+        assert info["fixed_rows"] and info["fixed_row_width"] == 8 and info["fixed_row_copy16"] == (copy16 == "1")
+        s.close()
+        s = ebc.Sampler(g, ebc.RunConfig(block_threads=block))
+        s.sample(SEED, 1000, 5000)
+        assert np.array_equal(s.read_frame(0), o.accumulate(SEED, 1000, 5000))
+        w, ow = s.work(), o.work()
+        for i, k in enumerate(ebc.WORK_NAMES[:11]):
+            assert w[k] == int(ow[i]), k
+        s.close()
+        s = ebc.Sampler(g, ebc.RunConfig(block_threads=block, work_counters=0))
+        s.sample(SEED, 1000, 5000)
+        assert np.array_equal(s.read_frame(0), o.accumulate(SEED, 1000, 5000))
+        s.close()
+
+
 def test_fixed_stride_rows_need_a_symmetric_graph():
     """An arc without its reverse has no reverse position to record: the sampler notices while it builds the rows and
     runs the general kernel instead (validate=0 adopts the CSR as it is)."""
