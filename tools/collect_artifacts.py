@@ -14,7 +14,7 @@ copies = {
     "fa_fuzz_pipeline.txt": "r02_fuzz_pipeline.txt", "fa_overlap_timeline.txt": "r02_overlap_timeline_final.txt",
     "fa_traffic.json": "traffic.json",
 }
-for k in ("rmat20", "grid2000", "rmat24"):
+for k in ("rmat20", "grid2000", "rmat24", "rmat26", "er10k"):
     copies[f"fa_ncu_summary_{k}.txt"] = f"r02_final_{k}_sample_kernel_ncu_summary.txt"
     copies[f"fa_ncu_details_{k}.txt"] = f"r02_final_{k}_sample_kernel_ncu_details.txt"
 for src, dst in copies.items():

@@ -3,15 +3,16 @@
 # and are copied into profiles/ by tools/collect_artifacts.py here).  Every number judged comes from this script:
 #   bench lines (own arm + reference arm) for the default workload and for configs 1, 3, 4, 5;
 #   the ncu launch list of the default bench command; ncu --set full of one bench-sized sampling launch of configs
-#   2, 3 and 4 (the DRAM bytes per sample behind roofline.traffic); all five configs end to end; the fuzz sweeps.
+#   1 to 5 (the DRAM bytes per sample behind roofline.traffic); all five configs end to end; the fuzz sweeps.
 set -x
 O=gpurun_out
 python bench.py --impl reference --steps 2 --warmup 1 > $O/fa_bench_reference.json 2> $O/fa_bench_reference.err
 # DRAM traffic of bench-sized launches first: bench.py reads profiles/traffic.json
-for spec in "rmat20 524288" "grid2000 32768" "rmat24 262144"; do
+# (third field: sampling launches before the measured one -- warm-up main + re-run pass; config 1 has no re-run pass)
+for spec in "rmat20 524288 2" "grid2000 32768 2" "rmat24 262144 2" "rmat26 131072 2" "er10k 1048576 1"; do
   set -- $spec
   python tools/prof_launch.py $1 $2 > $O/fa_plain_$1.log 2>&1 || exit 1      # exits 0 without ncu first; launches: warm-up main + re-run pass, then the measured main (+ re-run) pass
-  ncu --set full --import-source on --clock-control none -k regex:sample_kernel --launch-skip 2 --launch-count 2 \
+  ncu --set full --import-source on --clock-control none -k regex:sample_kernel --launch-skip $3 --launch-count 2 \
       -o $O/fa_ncu_$1 -f python tools/prof_launch.py $1 $2 > $O/fa_ncu_$1.log 2>&1
   python tools/record_traffic.py $1 $O/fa_ncu_$1.ncu-rep $2 r02_final_$1 > $O/fa_traffic_$1.log 2>&1
   python tools/ncu_summary.py $O/fa_ncu_$1.ncu-rep > $O/fa_ncu_summary_$1.txt 2>&1

@@ -30,6 +30,9 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_ou
 rows = list(csv.reader(out.splitlines()))
 hdr = rows[1]; ci = {h: i for i, h in enumerate(hdr)}
 data = rows[2:]
+for k, r in enumerate(data): # (a report with several launches: the first one's table)
+    if not r or r[0] in ("Kernel Name", "Address"):
+        data = data[:k]; break
 num = lambda x: float(x) if x not in ("", "-") else 0.0
 base = int(data[0][ci["Address"]], 16) if data[0][ci["Address"]].startswith("0x") else int(data[0][ci["Address"]])
 src = open("paper_1910_11039_b200/csrc/sampler_kernels.cuh").read().splitlines()
