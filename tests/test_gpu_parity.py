@@ -257,6 +257,40 @@ def test_meet_vertex_by_all_three_paths(block):
     s.close()
 
 
+@pytest.mark.parametrize("block,bitmap", [(32, "1"), (32, "0"), (128, "1")])
+def test_meet_paths_with_saturated_sigma_and_weights(block, bitmap, monkeypatch):
+    """Every level is probed here (EBC_PROBE_MIN_SLOTS / EBC_PROBE_GROWTH_X4), so small contact sets reach the register
+    path and the shared-memory path, too.  Seventy diamonds on either side double sigma seventy times: both sides'
+    sigma are 2^64 - 1 where the searches meet, every weight is (2^64 - 1)^2 and the total saturates at 2^128 - 1 --
+    carries of the butterfly total, prefixes that leave 128 bits, the quickselect's 'exceeds' rule.  The two layers in
+    the middle decide the number of contact edges: 16 / 25 (registers), 64 / 120 (shared memory), 256 / 576 (global
+    memory).  Records (meet vertex, |meet set|, draws, full paths) and total weights equal the oracle's."""
+    monkeypatch.setenv("EBC_BITMAP", bitmap)
+    monkeypatch.setenv("EBC_PROBE_MIN_SLOTS", "1")
+    monkeypatch.setenv("EBC_PROBE_GROWTH_X4", "0")
+    monkeypatch.setenv("EBC_ELL", "0")             # (the thin chains would otherwise take the fixed-stride-row kernel)
+    seen = {"registers": 0, "shared": 0, "global": 0}
+    for mid in ((4, 4), (5, 5), (8, 8), (3, 40, 3), (16, 16), (24, 24)):
+        widths = [1] + [2, 1] * 70 + list(mid) + [1, 2] * 70 + [1]
+        off, tg = complete_bipartite_chain(widths)
+        core = len(off) - 1
+        n = 30000                                  # isolated padding: the contact-edge buffer scales with n
+        off = np.concatenate([off, np.full(n - core, off[-1], dtype=np.uint64)])
+        pairs = np.array([[0, core - 1], [core - 1, 0], [1, core - 2], [core - 3, 2]], dtype=np.uint32)
+        s, o = check_samples((off, tg), len(pairs), ebc.RunConfig(block_threads=block, slots=2), pairs=pairs, stride=320)
+        rec, _ = s.sample_debug(SEED, 0, len(pairs), pairs=pairs, frame=1)
+        for i in range(len(pairs)):
+            o.sample(SEED, i, pair=tuple(int(x) for x in pairs[i]))
+            fs, bs = o.last_state(0)[1], o.last_state(1)[1]
+            total = min(sum(int(fs[v]) * int(bs[v]) for v in o.last_meet_set()), 2 ** 128 - 1)
+            assert (int(rec[i]["weight_hi"]) << 64) | int(rec[i]["weight_lo"]) == total, (mid, i)
+            f = int(rec[i]["flags"])
+            if (f & 2) and total == 2 ** 128 - 1:
+                seen["registers" if f & 16 else "global" if f & 8 else "shared"] += 1
+        s.close()
+    assert seen["registers"] > 0 and seen["shared"] > 0 and seen["global"] > 0, seen
+
+
 def test_final_level_probe_with_tiny_edge_buffer_falls_back():
     """slot_capacity so small that the contact-edge buffer overflows: expand_level / large-slot fallbacks."""
     g = ebc.gen_rmat(13, 16, seed=9).largest_connected_component()
