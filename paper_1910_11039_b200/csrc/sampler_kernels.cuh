@@ -1092,7 +1092,7 @@ __device__ bool expand_level_ell(const SamplerParams &p, u32 *lab, int e, SideRe
 #define EBC_PROBE_G 8
 #endif
 // Appends one contact edge (see probe_level); out of line, it runs a few dozen times per sample.
-static __device__ __noinline__ void record_contact_edge(u32 *edges, u32 pos, u32 frontier_pos, u32 index_in_row, u32 v, u32 oi,
+static __device__ __forceinline__ void record_contact_edge(u32 *edges, u32 pos, u32 frontier_pos, u32 index_in_row, u32 v, u32 oi,
                                                         u64 sg) {
     u64 *w = reinterpret_cast<u64 *>(edges) + 3 * static_cast<u64>(pos); // (24-byte records in an 8-byte aligned array)
     st_cg(w + 0, static_cast<u64>(frontier_pos) | (static_cast<u64>(index_in_row) << 32));
