@@ -6,6 +6,7 @@
 #   1 to 5 (the DRAM bytes per sample behind roofline.traffic); all five configs end to end; the fuzz sweeps.
 set -x
 O=gpurun_out
+R=/tmp/fa_ncu_reports; mkdir -p $R
 python bench.py --impl reference --steps 2 --warmup 1 > $O/fa_bench_reference.json 2> $O/fa_bench_reference.err
 # DRAM traffic of bench-sized launches first: bench.py reads profiles/traffic.json
 # (third field: sampling launches before the measured one -- warm-up main + re-run pass; config 1 has no re-run pass)
@@ -13,11 +14,12 @@ for spec in "rmat20 524288 2" "grid2000 32768 2" "rmat24 262144 2" "rmat26 13107
   set -- $spec
   python tools/prof_launch.py $1 $2 > $O/fa_plain_$1.log 2>&1 || exit 1      # exits 0 without ncu first; launches: warm-up main + re-run pass, then the measured main (+ re-run) pass
   ncu --set full --import-source on --clock-control none -k regex:sample_kernel --launch-skip $3 --launch-count 2 \
-      -o $O/fa_ncu_$1 -f python tools/prof_launch.py $1 $2 > $O/fa_ncu_$1.log 2>&1
-  python tools/record_traffic.py $1 $O/fa_ncu_$1.ncu-rep $2 r02_final_$1 > $O/fa_traffic_$1.log 2>&1
-  python tools/ncu_summary.py $O/fa_ncu_$1.ncu-rep > $O/fa_ncu_summary_$1.txt 2>&1
-  ncu -i $O/fa_ncu_$1.ncu-rep --page details > $O/fa_ncu_details_$1.txt 2>/dev/null
+      -o $R/fa_ncu_$1 -f python tools/prof_launch.py $1 $2 > $O/fa_ncu_$1.log 2>&1
+  python tools/record_traffic.py $1 $R/fa_ncu_$1.ncu-rep $2 r02_final_$1 > $O/fa_traffic_$1.log 2>&1
+  python tools/ncu_summary.py $R/fa_ncu_$1.ncu-rep > $O/fa_ncu_summary_$1.txt 2>&1
+  ncu -i $R/fa_ncu_$1.ncu-rep --page details > $O/fa_ncu_details_$1.txt 2>/dev/null
 done
+cp $R/fa_ncu_rmat20.ncu-rep $O/   # (gpurun brings back at most 64 MiB: one report for line-level work, not five)
 cp profiles/traffic.json $O/fa_traffic.json
 python bench.py > $O/fa_bench.json 2> $O/fa_bench.err
 python bench.py --strong > $O/fa_bench_strong.json 2> $O/fa_bench_strong.err
