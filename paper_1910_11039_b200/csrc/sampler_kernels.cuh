@@ -456,10 +456,10 @@ __device__ __forceinline__ uint4 ldg_targets4(const u32 *p) { return __ldg(reint
 // Loads the chunk of BLOCK frontier vertices at list positions [c0, c0 + BLOCK) (clipped to fe): row
 // start and sigma of each into c_beg / c_sig, the exclusive prefix of their degrees into
 // c_scan[0..BLOCK]; returns the chunk's number of adjacency slots.  Starts with a barrier (the previous
-// chunk's readers of c_* are done) and ends with one.  Out of line: one copy serves expand_level and
-// probe_level, and it runs once per 128 frontier vertices.
+// chunk's readers of c_* are done) and ends with one.  Inline in expand_level and probe_level (out of line
+// it cost config 4 1.5 % and config 1 3 %: a call per BLOCK frontier vertices).
 template <int BLOCK>
-__device__ __noinline__ u64 load_chunk(const SamplerParams &p, const SidePtrs *pp, u32 c0, u32 fe, u64 *c_beg, u64 *c_scan,
+__device__ __forceinline__ u64 load_chunk(const SamplerParams &p, const SidePtrs *pp, u32 c0, u32 fe, u64 *c_beg, u64 *c_scan,
                                        u64 *c_sig, u64 *red64) {
     const u32 tid = threadIdx.x;
     const u32 i = c0 + tid;
